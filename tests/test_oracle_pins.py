@@ -1,0 +1,288 @@
+"""Pins of the numeric oracle (oracle/oracle.c) against things other than itself.
+
+Each test names what fixes the expected value: exact rational arithmetic
+(determinant ratios of the centred Gram matrix), textbook closed forms,
+invariants of least squares, SPEC/paper-printed values.  A plausible bug in the
+oracle (dropped reflection, wrong column gathered, off-by-one in the tail, sign
+error, wrong BIC constant, wrong index compression) fails at least one.
+"""
+import itertools
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+
+# ---------------------------------------------------------------- exact helpers
+def frac_det(M):
+    """Exact determinant by fraction Gaussian elimination (textbook)."""
+    A = [list(r) for r in M]
+    n = len(A)
+    det = Fraction(1)
+    for c in range(n):
+        p = next((r for r in range(c, n) if A[r][c] != 0), None)
+        if p is None:
+            return Fraction(0)
+        if p != c:
+            A[c], A[p] = A[p], A[c]
+            det = -det
+        det *= A[c][c]
+        for r in range(c + 1, n):
+            f = A[r][c] / A[c][c]
+            for j in range(c, n):
+                A[r][j] -= f * A[c][j]
+    return det
+
+
+def exact_centred_gram(rows):
+    n = len(rows)
+    m = len(rows[0])
+    cols = [[Fraction(rows[i][j]) for i in range(n)] for j in range(m)]
+    for j in range(m):
+        mu = sum(cols[j]) / n
+        cols[j] = [x - mu for x in cols[j]]
+    return [[sum(a * b for a, b in zip(cols[u], cols[v])) for v in range(m)] for u in range(m)]
+
+
+def exact_rss(G, child, parents):
+    """RSS(v|S) = det G_{S+v} / det G_S (Schur complement closed form)."""
+    S = sorted(parents)
+    Sv = S + [child]
+    num = frac_det([[G[a][b] for b in Sv] for a in Sv])
+    den = frac_det([[G[a][b] for b in S] for a in S]) if S else Fraction(1)
+    return num / den
+
+
+def mask_bits(mask):
+    return [u for u in range(32) if (mask >> u) & 1]
+
+
+# ---------------------------------------------------------------- golden m=3
+def test_golden_m3_table(golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "m3_table.json")))
+    rows = g["rows"]
+    G = exact_centred_gram(rows)
+    assert G == [[Fraction(x) for x in r] for r in g["centred_gram"]]
+    assert frac_det(G) == g["det_gram"]
+    X = np.asfortranarray(np.array(rows, dtype=float))
+    Xc = oracle.centre(X)
+    rss, bic = oracle.table(Xc)
+    for e in g["table"]:
+        # the fixture itself is re-derived exactly here
+        ex = exact_rss(G, e["child"], mask_bits(e["mask"]))
+        assert ex == Fraction(e["rss"])
+        assert oracle.index(3, e["child"], e["mask"]) == e["idx"]
+        assert rss[e["idx"]] == pytest.approx(float(ex), rel=1e-13)
+        assert bic[e["idx"]] == pytest.approx(e["bic"], abs=1e-11)
+    bm, _ = oracle.best(bic, 3)
+    assert [int(x) for x in bm] == [g["best"][str(v)] for v in range(3)]
+
+
+# ---------------------------------------------------------------- brute force
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_rss_exact_rational_bruteforce(seed):
+    """All families of a small integer dataset against exact rational det ratios."""
+    rng = np.random.default_rng(seed)
+    n, m = 9, 5
+    rows = rng.integers(-6, 7, size=(n, m)).tolist()
+    G = exact_centred_gram(rows)
+    assert frac_det(G) != 0
+    Xc = oracle.centre(np.asfortranarray(np.array(rows, dtype=float)))
+    rss, _ = oracle.table(Xc, want_bic=False)
+    for idx in range(m << (m - 1)):
+        v, S = oracle.mask_of(m, idx)
+        ex = float(exact_rss(G, v, mask_bits(S)))
+        assert rss[idx] == pytest.approx(ex, rel=1e-12, abs=1e-12 * float(G[v][v]))
+
+
+def test_empty_parent_closed_form():
+    """RSS(v|{}) = ||x_v - mean(x_v)||^2 (G4 / SPEC.md:257), summed with fsum."""
+    X = datagen.gaussian(200, 6, seed=7, offset=50.0)
+    Xc = oracle.centre(X)
+    for v in range(6):
+        col = X[:, v]
+        mu = math.fsum(col) / len(col)
+        ex = math.fsum((x - mu) ** 2 for x in col)
+        assert oracle.rss(Xc, v, 0) == pytest.approx(ex, rel=1e-13)
+
+
+def test_single_parent_closed_form():
+    """RSS(v|{u}) = ||x_v||^2 (1 - rho_uv^2) for centred columns."""
+    X = datagen.config_data(2)
+    Xc = oracle.centre(X)
+    for v, u in [(0, 1), (5, 3), (15, 2), (7, 8)]:
+        a, b = Xc[:, u], Xc[:, v]
+        suu, svv, suv = math.fsum(a * a), math.fsum(b * b), math.fsum(a * b)
+        ex = svv * (1.0 - suv * suv / (suu * svv))
+        assert oracle.rss(Xc, v, 1 << u) == pytest.approx(ex, rel=1e-10)
+
+
+def test_full_parent_set_inverse_gram():
+    """RSS(v|V\\v) = 1/(G^-1)_vv on well-conditioned data (Schur complement)."""
+    X = datagen.gaussian(300, 7, seed=11)
+    Xc = oracle.centre(X)
+    Gi = np.linalg.inv(Xc.T @ Xc)
+    full = (1 << 7) - 1
+    for v in range(7):
+        assert oracle.rss(Xc, v, full & ~(1 << v)) == pytest.approx(1.0 / Gi[v, v], rel=1e-10)
+
+
+def test_monotone_nonincreasing_in_parents():
+    """Adding a parent never increases RSS (nested least squares), slack 1e-9."""
+    X = datagen.config_data(1)
+    Xc = oracle.centre(X)
+    m = 8
+    rss, _ = oracle.table(Xc, want_bic=False)
+    for idx in range(m << (m - 1)):
+        v, S = oracle.mask_of(m, idx)
+        for u in range(m):
+            if u != v and not (S >> u) & 1:
+                j = oracle.index(m, v, S | (1 << u))
+                assert rss[j] <= rss[idx] * (1 + 1e-9)
+
+
+def test_planted_zero_noise_relation():
+    """x3 = 2 x0 - x1 exactly (integers): RSS(3|{0,1}) ~ 0 absolutely (G13),
+    while RSS(3|{0}) is not."""
+    rng = np.random.default_rng(5)
+    n = 40
+    X = rng.integers(-20, 21, size=(n, 5)).astype(float)
+    X[:, 3] = 2 * X[:, 0] - X[:, 1]
+    Xc = oracle.centre(np.asfortranarray(X))
+    y2 = float(np.sum(Xc[:, 3] ** 2))
+    assert oracle.rss(Xc, 3, 0b00011) <= 1e-20 * y2
+    assert oracle.rss(Xc, 3, 0b10111 & ~(1 << 3)) <= 1e-20 * y2
+    assert oracle.rss(Xc, 3, 0b00001) > 1e-3 * y2
+    assert math.isinf(oracle.bic(0.0, n, 2)) and oracle.bic(0.0, n, 2) > 0
+
+
+def test_chain_rule_and_determinant():
+    """RSS(u|S) RSS(v|S+u) = RSS(v|S) RSS(u|S+v) (both = det G_{S+u+v}/det G_S);
+    product of RSS along any full chain = det G."""
+    X = datagen.config_data(1)
+    Xc = oracle.centre(X)
+    m = 8
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        u, v = rng.choice(m, 2, replace=False)
+        S = int(rng.integers(0, 1 << m)) & ~(1 << u) & ~(1 << v)
+        lhs = oracle.rss(Xc, u, S) * oracle.rss(Xc, v, S | (1 << u))
+        rhs = oracle.rss(Xc, v, S) * oracle.rss(Xc, u, S | (1 << v))
+        assert lhs == pytest.approx(rhs, rel=1e-11)
+    sign, logdet = np.linalg.slogdet(Xc.T @ Xc)
+    for perm in [range(m), [3, 1, 7, 0, 2, 6, 5, 4]]:
+        S, acc = 0, 0.0
+        for v in perm:
+            acc += math.log(oracle.rss(Xc, v, S))
+            S |= 1 << v
+        assert acc == pytest.approx(logdet, rel=1e-12)
+
+
+def test_residual_self_check():
+    """factorization RSS == explicit residual RSS (1e-9 rel)."""
+    X = datagen.config_data(2)
+    Xc = oracle.centre(X)
+    m = 16
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        idx = int(rng.integers(0, m << (m - 1)))
+        v, S = oracle.mask_of(m, idx)
+        assert oracle.rss_residual(Xc, v, S) == pytest.approx(oracle.rss(Xc, v, S), rel=1e-9)
+
+
+def test_qr_r_gram_and_spec_example():
+    """R^T R = X^T X within 1e-12 ||G||; SPEC.md:57 2x2 example."""
+    R = oracle.qr_r(np.asfortranarray(np.array([[2.0, 1.0], [0.0, 1.0]])))
+    assert np.allclose(R, [[2.0, 1.0], [0.0, 1.0]], atol=1e-15)
+    X = datagen.config_data(3)
+    Xc = oracle.centre(X)
+    R = oracle.qr_r(Xc)
+    G = Xc.T @ Xc
+    assert np.linalg.norm(R.T @ R - G) <= 1e-12 * np.linalg.norm(G)
+    assert np.all(np.diag(R) > 0)
+    assert np.allclose(np.tril(R, -1), 0)
+
+
+def test_reduced_oracle_matches_o1():
+    """O2 (Householder on slices of R0) == O1 on a seeded sample."""
+    X = datagen.config_data(2)
+    Xc = oracle.centre(X)
+    R0 = oracle.qr_r(Xc)
+    idx = datagen.sample_indices(16, 2000, seed=4)
+    a = oracle.rss_indices(Xc, idx)
+    b = oracle.rss_reduced_indices(R0, idx)
+    np.testing.assert_allclose(b, a, rtol=1e-10)
+
+
+def test_bic_spec_value():
+    """n=50, rss=50 -> log-likelihood -25(1 + ln 2 pi) = -70.946926660;
+    with no parents BIC equals the log-likelihood; each parent costs ln(n)/2."""
+    assert oracle.bic(50.0, 50, 0) == pytest.approx(-70.946926660, abs=1e-9)
+    assert oracle.bic(50.0, 50, 3) == pytest.approx(-70.946926660 - 1.5 * math.log(50), abs=1e-9)
+
+
+def test_index_roundtrip_and_order():
+    """D6: index = child 2^(m-1) + compress(S, child); sorting by index equals
+    sorting by (child, mask)."""
+    m = 6
+    seen = []
+    for v in range(m):
+        for S in range(1 << m):
+            if (S >> v) & 1:
+                assert oracle.index(m, v, S) == -1
+                continue
+            i = oracle.index(m, v, S)
+            assert oracle.mask_of(m, i) == (v, S)
+            seen.append((i, v, S))
+    seen.sort()
+    assert [s[0] for s in seen] == list(range(m << (m - 1)))
+    assert [(s[1], s[2]) for s in seen] == sorted((s[1], s[2]) for s in seen)
+    v, S = oracle.masks_of(m, np.arange(m << (m - 1)))
+    assert all(oracle.mask_of(m, i) == (int(a), int(b)) for i, (a, b) in enumerate(zip(v, S)))
+
+
+def test_best_tiebreak():
+    """G14: larger BIC, then smaller |S|, then smaller mask."""
+    m = 3
+    b = np.full(m << (m - 1), -100.0)
+    # child 0: masks (ascending compressed) 0, 2, 4, 6 -> make {1} and {2} tie
+    b[oracle.index(m, 0, 0b010)] = -1.0
+    b[oracle.index(m, 0, 0b100)] = -1.0
+    b[oracle.index(m, 0, 0b110)] = -1.0
+    # child 1: a strict max at {0,2}
+    b[oracle.index(m, 1, 0b101)] = 5.0
+    bm, bb = oracle.best(b, m)
+    assert int(bm[0]) == 0b010 and bb[0] == -1.0
+    assert int(bm[1]) == 0b101
+    assert int(bm[2]) == 0
+
+
+def test_centre_and_nonfinite():
+    X = datagen.gaussian(100, 4, seed=1, offset=1e3)
+    Xc = oracle.centre(X)
+    for v in range(4):
+        assert abs(math.fsum(Xc[:, v])) <= 1e-12 * np.linalg.norm(Xc[:, v]) * 100
+    X[3, 2] = np.nan
+    with pytest.raises(ValueError):
+        oracle.centre(X)
+
+
+def test_permutation_invariance():
+    """Relabelling the variables permutes the table."""
+    X = datagen.config_data(1)
+    perm = [5, 2, 7, 0, 1, 6, 4, 3]  # new column j = old column perm[j]
+    Xp = np.asfortranarray(X[:, perm])
+    r1, _ = oracle.table(oracle.centre(X), want_bic=False)
+    r2, _ = oracle.table(oracle.centre(Xp), want_bic=False)
+    m = 8
+    for idx in range(0, m << (m - 1), 7):
+        v, S = oracle.mask_of(m, idx)  # in permuted labels
+        ov = perm[v]
+        oS = sum(1 << perm[u] for u in range(m) if (S >> u) & 1)
+        assert r2[idx] == pytest.approx(r1[oracle.index(m, ov, oS)], rel=1e-12)
