@@ -1,0 +1,157 @@
+/*
+ * bnreg.h -- C ABI of the B200-native all-family regression library.
+ *
+ * The method (arXiv 1901.07643): for m continuous variables compute, for every
+ * child v and every parent set S not containing v (m 2^(m-1) "families",
+ * PAPER.md:15, §1), the least-squares residual sum of squares RSS(v|S) of the
+ * regression of the centred x_v on the centred x_S, and the Gaussian BIC local
+ * score.  It starts from ONE QR decomposition of the data ("The algorithm
+ * starts with calculating the QRD of the data matrix", §2) and
+ * walks the paper's shortest sequence of adjacent-column swaps re-triangularised
+ * by Givens rotations (GRC, Eq.3-4; schedule Alg.1
+ * and Eq.10 :207-212), split over workers as in Alg.2.
+ *
+ * Conventions (all functions):
+ *   - fp64 throughout; all calls are synchronous with respect to the host unless
+ *     named *_async; status codes are returned, never thrown; the message of the
+ *     last failing call is in bnreg_last_error() (thread-local).
+ *   - Table layout (reading D6): entry of family (child v, parent
+ *     mask S, bit u of S = user variable u, 0-based) is at
+ *         index = v * 2^(m-1) + compress(S, v)
+ *     where compress deletes bit v.  Sorting by index = sorting by (v, S).
+ *     With world > 1 a rank writes only its shard: the concatenation, in index
+ *     order, of the ranges bnreg_shard_ranges reports (bnreg_local_index maps).
+ *   - BIC (reading G5): -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi) - (|S|/2) ln n,
+ *     higher is better; +INF when RSS <= 1e-300 (perfect fit, G13).
+ *   - Best (reading G14): per child the parent set of largest BIC; on exact ties
+ *     the smaller |S|, then the smaller mask.
+ *   - A handle is not thread-safe; distinct handles are independent.  Output is
+ *     bit-identical across runs at a fixed world size and build.
+ *   - Limits: 2 <= m <= 30 (device memory limits m far below: the RSS+BIC tables
+ *     take 16 m 2^(m-1) bytes, 60 GB at m = 28), n >= m + 1.
+ */
+#ifndef BNREG_H
+#define BNREG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bnreg bnreg_t;   /* opaque; owns all device state it allocates */
+
+typedef enum {
+    BNREG_OK = 0,
+    BNREG_E_INVAL = 1,      /* bad argument (sizes, NULL handle, world/rank, k)              */
+    BNREG_E_NONFINITE = 2,  /* X holds a NaN or Inf (SPEC.md:54 NonFinite)                    */
+    BNREG_E_RANK = 3,       /* |r_jj| <= 1e-12 max_j ||x_j - mean||  (reading G26) */
+    BNREG_E_NOMEM = 4,      /* device allocation failed                                       */
+    BNREG_E_CUDA = 5,       /* any other CUDA error (message in bnreg_last_error)             */
+    BNREG_E_STATE = 6       /* call out of order (e.g. run before data/root is loaded)        */
+} bnreg_status;
+
+typedef struct {
+    int32_t free_vars;        /* k, the free block each worker permutes with Upsilon(k);
+                                 0 = auto (min(m, 8)); 2 <= k <= min(m, 16)              */
+    int32_t levels_in_warp;   /* seed-tree levels each warp derives itself; -1 = auto (4) */
+    int32_t world;            /* ranks sharing the walk (power of two); 0 or 1 = single */
+    int32_t rank;             /* this rank, 0 <= rank < world                             */
+    int32_t warps_per_cta;    /* traversal CTA size in warps; 0 = auto (2)                */
+    int32_t ctas_per_sm;      /* traversal CTAs per SM; 0 = occupancy maximum             */
+} bnreg_options;
+
+/* Create a handle for n x m data and load X (centre + QR, steps a1-a2).
+ * X: HOST pointer, column-major n x m (ld = n), read-only, copied; the caller
+ * keeps ownership.  On error *out = NULL.  Equivalent to
+ * bnreg_create_ex(NULL options) + bnreg_load(h, X, 0). */
+bnreg_status bnreg_create(const double* X, int64_t n, int32_t m, bnreg_t** out);
+
+/* Create without loading data.  opt may be NULL (defaults).  Allocates the
+ * device state on the current CUDA device. */
+bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* opt, bnreg_t** out);
+
+/* (Re)load data of the handle's n, m: centre each column (a1; reading G4) and
+ * factor it (a2: TSQR of 256-row Householder leaves).  X: column-major n x m,
+ * a HOST pointer when x_on_device == 0 (copied host->device here), else a
+ * DEVICE pointer (read in place).  Errors: BNREG_E_NONFINITE, BNREG_E_RANK. */
+bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device);
+
+/* Number of table entries this handle writes: m 2^(m-1), or this rank's share. */
+int64_t bnreg_num_families(const bnreg_t* h);
+
+/* Global index of (child, mask); -1 if bit `child` is set or child is out of range. */
+int64_t bnreg_index(int32_t m, int32_t child, uint32_t mask);
+
+/* Rank-local offset of a global index, -1 if another rank owns it. */
+int64_t bnreg_local_index(const bnreg_t* h, int64_t global_index);
+
+/* The fused hot path (a5-a11): seed tree, traversal with harvest, BIC, stores,
+ * per-child best.  out_rss / out_bic: caller-owned DEVICE buffers of
+ * bnreg_num_families(h) doubles; either may be NULL (not written).
+ * best_mask / best_bic: HOST arrays of m entries (either may be NULL); with
+ * world > 1 they hold this rank's best only (merge with bnreg_best_merge). */
+bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask, double* best_bic);
+
+/* As bnreg_run but asynchronous on the handle's stream; best_mask / best_bic
+ * are DEVICE arrays of m entries (either may be NULL).  Errors surface on the
+ * next synchronous call. */
+bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask_dev,
+                             double* best_bic_dev);
+
+/* The north-star calls: the RSS table alone / the BIC table alone. */
+bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
+bnreg_status bnreg_bic(bnreg_t* h, double* out);
+
+/* Use this CUDA stream (a cudaStream_t) for all further work; NULL = the
+ * handle's own stream. */
+bnreg_status bnreg_set_stream(bnreg_t* h, void* stream);
+
+/* Root factor R (m x m row-major, diag > 0) in the walk's root variable order,
+ * and that order (order[pos] = user id).  Either pointer may be NULL. HOST. */
+bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host);
+
+/* Multi-GPU step a3: copy the root R (m*m doubles, row-major, root order) into
+ * / out of a caller-owned DEVICE buffer, so the harness can broadcast it from
+ * rank 0 with NCCL over NVLink.  Ranks that receive it call
+ * bnreg_set_root_device instead of bnreg_load.  Both are stream-ordered on the
+ * handle's stream and synchronise before returning. */
+bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev);
+bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev);
+
+/* Index ranges of this rank's shard (global index space).  *count receives the
+ * number of ranges (<= 2m); starts/lens (capacity 2m) receive them in order. */
+bnreg_status bnreg_shard_ranges(const bnreg_t* h, int64_t* count, int64_t* starts, int64_t* lens);
+
+/* Deterministic merge of per-rank bests (step a11 after the all-gather):
+ * masks/bics are nparts x m row-major HOST arrays. */
+bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, const double* bics,
+                              uint32_t* out_mask, double* out_bic);
+
+/* Per-phase device time of the runs since the last reset, from CUDA events on
+ * the launching stream.  enable: 1 = start recording (and reset), 0 = stop,
+ * -1 = just read.  out_ms[0] = whole run, [1] = seed tree, [2] = traversal
+ * kernel, [3] = best reduce; *runs = number of runs accumulated. */
+bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* runs);
+
+/* Plan introspection (host only, no GPU): info[0..11] = k, b, p, bh, L1, LW,
+ * npacks (this rank), schedule length, local families, total families,
+ * traversal smem bytes per warp, r (rank selector bits). */
+bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* opt, int64_t* info);
+
+/* Upsilon(k) (1-based swap positions) as the kernels use it; returns its length
+ * (2^k - k - 1) or -1; writes min(length, cap) entries. Host only. */
+int64_t bnreg_schedule(int32_t k, int8_t* out, int64_t cap);
+
+/* Pack ids of a plan in launch order (host only); returns the count. */
+int64_t bnreg_plan_packs(int32_t m, int64_t n, const bnreg_options* opt, uint32_t* out, int64_t cap);
+
+const char* bnreg_last_error(void);
+
+void bnreg_destroy(bnreg_t* h);   /* NULL-safe; frees device state */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BNREG_H */

@@ -1,0 +1,253 @@
+"""bnreg -- B200-native exact all-family regressions (arXiv 1901.07643).
+
+Thin ctypes binding of the C ABI in include/bnreg.h: argument marshalling only,
+every step of the method runs in the sm_100a kernels of libbnreg.so.  There is
+no CPU fallback: importing this package on a machine without the built library
+raises, and calls that need a GPU fail with the CUDA error the library reports.
+
+Device buffers are passed as raw pointers (ints) or any object with a
+``data_ptr()`` method (e.g. a torch CUDA tensor); host arrays are numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbnreg.so")
+
+OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE = range(7)
+_NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNREG_E_NOMEM",
+          5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
+
+# every symbol include/bnreg.h declares (checked by tests/test_abi.py)
+SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_all_rss", "bnreg_bic",
+           "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
+           "bnreg_shard_ranges", "bnreg_best_merge", "bnreg_timing", "bnreg_plan_query",
+           "bnreg_schedule", "bnreg_plan_packs", "bnreg_last_error", "bnreg_destroy"]
+
+
+class BnregError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("free_vars", ctypes.c_int32), ("levels_in_warp", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+
+
+def options(free_vars=0, levels_in_warp=-1, world=1, rank=0, warps_per_cta=0, ctas_per_sm=0):
+    return Options(free_vars, levels_in_warp, world, rank, warps_per_cta, ctas_per_sm)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u32, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double
+    H = ctypes.c_void_p
+    PH = ctypes.POINTER(ctypes.c_void_p)
+    POPT = ctypes.POINTER(Options)
+    sig = {
+        "bnreg_create": ([P, i64, i32, PH], i32),
+        "bnreg_create_ex": ([i64, i32, POPT, PH], i32),
+        "bnreg_load": ([H, P, i32], i32),
+        "bnreg_num_families": ([H], i64),
+        "bnreg_index": ([i32, i32, u32], i64),
+        "bnreg_local_index": ([H, i64], i64),
+        "bnreg_run": ([H, P, P, P, P], i32),
+        "bnreg_run_async": ([H, P, P, P, P], i32),
+        "bnreg_all_rss": ([H, P], i32),
+        "bnreg_bic": ([H, P], i32),
+        "bnreg_set_stream": ([H, P], i32),
+        "bnreg_root_r": ([H, P, P], i32),
+        "bnreg_get_root_device": ([H, P], i32),
+        "bnreg_set_root_device": ([H, P], i32),
+        "bnreg_shard_ranges": ([H, P, P, P], i32),
+        "bnreg_best_merge": ([i32, i32, P, P, P, P], i32),
+        "bnreg_timing": ([H, i32, P, P], i32),
+        "bnreg_plan_query": ([i32, i64, POPT, P], i32),
+        "bnreg_schedule": ([i32, P, i64], i64),
+        "bnreg_plan_packs": ([i32, i64, POPT, P, i64], i64),
+        "bnreg_last_error": ([], ctypes.c_char_p),
+        "bnreg_destroy": ([H], None),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(st):
+    if st != OK:
+        raise BnregError(st, lib().bnreg_last_error().decode())
+
+
+def _dptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _hptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- host-only calls
+def bnreg_index(m: int, child: int, mask: int) -> int:
+    return lib().bnreg_index(m, child, mask)
+
+
+def bnreg_schedule(k: int) -> np.ndarray:
+    n = lib().bnreg_schedule(k, None, 0)
+    if n < 0:
+        raise ValueError("k out of range")
+    out = np.zeros(n, dtype=np.int8)
+    lib().bnreg_schedule(k, _hptr(out), n)
+    return out
+
+
+def bnreg_plan_query(m: int, n: int, opt: Options | None = None) -> dict:
+    info = np.zeros(16, dtype=np.int64)
+    _check(lib().bnreg_plan_query(m, n, ctypes.byref(opt) if opt else None, _hptr(info)))
+    keys = ["k", "b", "p", "bh", "L1", "LW", "npacks", "sched_len", "local_families", "total_families",
+            "smem_per_warp", "r"]
+    return {k: int(v) for k, v in zip(keys, info)}
+
+
+def bnreg_plan_packs(m: int, n: int, opt: Options | None = None) -> np.ndarray:
+    o = ctypes.byref(opt) if opt else None
+    cnt = lib().bnreg_plan_packs(m, n, o, None, 0)
+    if cnt < 0:
+        raise BnregError(E_INVAL, lib().bnreg_last_error().decode())
+    out = np.zeros(cnt, dtype=np.uint32)
+    lib().bnreg_plan_packs(m, n, o, _hptr(out), cnt)
+    return out
+
+
+def bnreg_best_merge(m: int, masks: np.ndarray, bics: np.ndarray):
+    masks = np.ascontiguousarray(masks, dtype=np.uint32).reshape(-1, m)
+    bics = np.ascontiguousarray(bics, dtype=np.float64).reshape(-1, m)
+    om = np.zeros(m, dtype=np.uint32)
+    ob = np.zeros(m)
+    _check(lib().bnreg_best_merge(m, masks.shape[0], _hptr(masks), _hptr(bics), _hptr(om), _hptr(ob)))
+    return om, ob
+
+
+# ---------------------------------------------------------------- handle
+class Bnreg:
+    """One handle = the device state for n x m data (bnreg_create_ex)."""
+
+    def __init__(self, n: int, m: int, opt: Options | None = None):
+        self.n, self.m = int(n), int(m)
+        self.opt = opt
+        h = ctypes.c_void_p()
+        _check(lib().bnreg_create_ex(self.n, self.m, ctypes.byref(opt) if opt else None, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def create(cls, X: np.ndarray, opt: Options | None = None):
+        """bnreg_create: host X (column-major n x m) -> loaded handle."""
+        X = np.asfortranarray(X, dtype=np.float64)
+        self = cls(X.shape[0], X.shape[1], opt)
+        self.load(X)
+        return self
+
+    def load(self, X):
+        """bnreg_load: host numpy X (copied H2D) or a device pointer / CUDA tensor."""
+        if isinstance(X, np.ndarray):
+            X = np.asfortranarray(X, dtype=np.float64)
+            if X.shape != (self.n, self.m):
+                raise ValueError("shape mismatch")
+            _check(lib().bnreg_load(self._h, _hptr(X), 0))
+        else:
+            _check(lib().bnreg_load(self._h, _dptr(X), 1))
+
+    def num_families(self) -> int:
+        return lib().bnreg_num_families(self._h)
+
+    def local_index(self, g: int) -> int:
+        return lib().bnreg_local_index(self._h, g)
+
+    def run(self, out_rss=None, out_bic=None, best=True):
+        """bnreg_run: device tables (pointers / tensors, None = skip) -> (best_mask, best_bic) host."""
+        bm = np.zeros(self.m, dtype=np.uint32)
+        bb = np.zeros(self.m)
+        _check(lib().bnreg_run(self._h, _dptr(out_rss), _dptr(out_bic),
+                               _hptr(bm) if best else None, _hptr(bb) if best else None))
+        return bm, bb
+
+    def run_async(self, out_rss=None, out_bic=None, best_mask_dev=None, best_bic_dev=None):
+        _check(lib().bnreg_run_async(self._h, _dptr(out_rss), _dptr(out_bic), _dptr(best_mask_dev),
+                                     _dptr(best_bic_dev)))
+
+    def all_rss(self, out):
+        _check(lib().bnreg_all_rss(self._h, _dptr(out)))
+
+    def bic(self, out):
+        _check(lib().bnreg_bic(self._h, _dptr(out)))
+
+    def set_stream(self, stream_handle: int | None):
+        _check(lib().bnreg_set_stream(self._h, stream_handle))
+
+    def root_r(self):
+        R = np.zeros((self.m, self.m))
+        order = np.zeros(self.m, dtype=np.int32)
+        _check(lib().bnreg_root_r(self._h, _hptr(R), _hptr(order)))
+        return R, order
+
+    def get_root_device(self, R_dev):
+        """Copy the root R (m*m doubles) into a device buffer (for the broadcast)."""
+        _check(lib().bnreg_get_root_device(self._h, _dptr(R_dev)))
+
+    def set_root_device(self, R_dev):
+        """Install a broadcast root R from a device buffer (instead of load)."""
+        _check(lib().bnreg_set_root_device(self._h, _dptr(R_dev)))
+
+    def shard_ranges(self):
+        cnt = ctypes.c_int64(0)
+        starts = np.zeros(2 * self.m, dtype=np.int64)
+        lens = np.zeros(2 * self.m, dtype=np.int64)
+        _check(lib().bnreg_shard_ranges(self._h, ctypes.byref(cnt), _hptr(starts), _hptr(lens)))
+        c = cnt.value
+        return starts[:c].copy(), lens[:c].copy()
+
+    def timing(self, enable: int = -1):
+        ms = np.zeros(4)
+        runs = ctypes.c_int64(0)
+        _check(lib().bnreg_timing(self._h, enable, _hptr(ms), ctypes.byref(runs)))
+        return ms, runs.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bnreg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

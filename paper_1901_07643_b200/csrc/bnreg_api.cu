@@ -1,0 +1,447 @@
+// bnreg_api.cu -- the C ABI (include/bnreg.h): argument checks, device state,
+// host plan (plan.h) and the launch sequence of the sm_100a kernels.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+#include <stdexcept>
+
+#include "../../include/bnreg.h"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace bnr;
+
+static thread_local std::string g_err;
+
+static bnreg_status fail(bnreg_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess) {                                                                    \
+            return fail(e_ == cudaErrorMemoryAllocation ? BNREG_E_NOMEM : BNREG_E_CUDA,             \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+        }                                                                                           \
+    } while (0)
+
+struct bnreg {
+    Plan plan;
+    bnreg_options opt{};
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    // device buffers
+    double* dX = nullptr;          // host-loaded copy of X (n*m)
+    double* dXr = nullptr;         // centred, root-ordered X
+    int* d_order = nullptr;        // root order
+    double* d_rbuf = nullptr;      // TSQR tree slots
+    unsigned* d_tcnt = nullptr;    // TSQR arrival counters
+    int nleaf2 = 1;
+    int rb = 256;
+    double* d_root = nullptr;      // root R (m*m)
+    double* d_nodes[2] = {nullptr, nullptr};
+    uint32_t* d_packs = nullptr;
+    int8_t* d_sched = nullptr;
+    unsigned* d_counter = nullptr;
+    double* d_part_bic = nullptr;
+    uint32_t* d_part_mask = nullptr;
+    double* d_best_bic = nullptr;
+    uint32_t* d_best_mask = nullptr;
+    int* d_status = nullptr;
+    int grid_ctas = 0, wpc = 2;
+    bool loaded = false;
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    double acc_ms[4] = {0, 0, 0, 0};
+    int64_t runs = 0;
+};
+
+static bnreg_options defaults(const bnreg_options* o)
+{
+    bnreg_options d{};
+    d.free_vars = 0; d.levels_in_warp = -1; d.world = 1; d.rank = 0; d.warps_per_cta = 0; d.ctas_per_sm = 0;
+    if (o) {
+        d = *o;
+        if (d.world <= 0) d.world = 1;
+    }
+    return d;
+}
+
+static void free_all(bnreg* h)
+{
+    if (!h) return;
+    void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
+                    h->d_packs, h->d_sched, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
+                    h->d_best_mask, h->d_status};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+}
+
+extern "C" {
+
+const char* bnreg_last_error(void) { return g_err.c_str(); }
+
+int64_t bnreg_index(int32_t m, int32_t child, uint32_t mask)
+{
+    if (m < 2 || m > kMaxM) return -1;
+    return family_index(m, child, mask);
+}
+
+int64_t bnreg_schedule(int32_t k, int8_t* out, int64_t cap)
+{
+    if (k < 2 || k > kMaxFree) return -1;
+    auto s = greedy_swaps(k);
+    if (out)
+        for (int64_t t = 0; t < (int64_t)s.size() && t < cap; ++t) out[t] = s[t];
+    return (int64_t)s.size();
+}
+
+bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* o, int64_t* info)
+{
+    if (!info) return fail(BNREG_E_INVAL, "info is NULL");
+    bnreg_options d = defaults(o);
+    try {
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        info[0] = P.k; info[1] = P.b; info[2] = P.p; info[3] = P.bh; info[4] = P.L1; info[5] = P.LW;
+        info[6] = (int64_t)P.packs.size(); info[7] = (int64_t)P.sched.size(); info[8] = P.local_families;
+        info[9] = P.total_families; info[10] = (int64_t)traverse_smem_per_warp(P.m, P.k); info[11] = P.r;
+    } catch (std::exception& e) {
+        return fail(BNREG_E_INVAL, e.what());
+    }
+    return BNREG_OK;
+}
+
+int64_t bnreg_plan_packs(int32_t m, int64_t n, const bnreg_options* o, uint32_t* out, int64_t cap)
+{
+    bnreg_options d = defaults(o);
+    try {
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        if (out)
+            for (int64_t i = 0; i < (int64_t)P.packs.size() && i < cap; ++i) out[i] = P.packs[i];
+        return (int64_t)P.packs.size();
+    } catch (std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg_t** out)
+{
+    if (!out) return fail(BNREG_E_INVAL, "out is NULL");
+    *out = nullptr;
+    bnreg_options d = defaults(o);
+    Plan P;
+    try {
+        P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+    } catch (std::exception& e) {
+        return fail(BNREG_E_INVAL, e.what());
+    }
+    bnreg* h = new bnreg();
+    h->plan = P;
+    h->opt = d;
+    auto bail = [&](bnreg_status s) {
+        free_all(h);
+        delete h;
+        return s;
+    };
+#define CKH(call)                                                                                  \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return bail(fail(e_ == cudaErrorMemoryAllocation ? BNREG_E_NOMEM : BNREG_E_CUDA,      \
+                             std::string(#call) + ": " + cudaGetErrorString(e_)));               \
+    } while (0)
+    CKH(cudaGetDevice(&h->device));
+    CKH(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+    CKH(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    const size_t nm = (size_t)n * m;
+    CKH(cudaMalloc(&h->dX, nm * sizeof(double)));
+    CKH(cudaMalloc(&h->dXr, nm * sizeof(double)));
+    CKH(cudaMalloc(&h->d_order, m * sizeof(int)));
+    CKH(cudaMemcpy(h->d_order, P.root_order.data(), m * sizeof(int), cudaMemcpyHostToDevice));
+    int nleaf = (int)((n + h->rb - 1) / h->rb);
+    h->nleaf2 = 1;
+    while (h->nleaf2 < nleaf) h->nleaf2 <<= 1;
+    CKH(cudaMalloc(&h->d_rbuf, (size_t)2 * h->nleaf2 * m * m * sizeof(double)));
+    CKH(cudaMalloc(&h->d_tcnt, (size_t)h->nleaf2 * sizeof(unsigned)));
+    CKH(cudaMemset(h->d_tcnt, 0, (size_t)h->nleaf2 * sizeof(unsigned)));
+    CKH(cudaMalloc(&h->d_root, (size_t)m * m * sizeof(double)));
+    if (P.L1 > 0) {
+        size_t nodes = (size_t)1 << P.L1;
+        CKH(cudaMalloc(&h->d_nodes[0], nodes * m * m * sizeof(double)));
+        CKH(cudaMalloc(&h->d_nodes[1], nodes * m * m * sizeof(double)));
+    }
+    CKH(cudaMalloc(&h->d_packs, std::max<size_t>(1, P.packs.size()) * sizeof(uint32_t)));
+    if (!P.packs.empty())
+        CKH(cudaMemcpy(h->d_packs, P.packs.data(), P.packs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CKH(cudaMalloc(&h->d_sched, std::max<size_t>(1, P.sched.size())));
+    if (!P.sched.empty()) CKH(cudaMemcpy(h->d_sched, P.sched.data(), P.sched.size(), cudaMemcpyHostToDevice));
+    CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
+    h->wpc = d.warps_per_cta > 0 ? d.warps_per_cta : 2;
+    int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
+    int64_t want = (int64_t)h->num_sms * per_sm;
+    int64_t need = ((int64_t)P.packs.size() + h->wpc - 1) / h->wpc;
+    h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
+    size_t gw = (size_t)h->grid_ctas * h->wpc;
+    CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
+    CKH(cudaMalloc(&h->d_part_mask, gw * m * sizeof(uint32_t)));
+    CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
+    CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
+    CKH(cudaMalloc(&h->d_status, sizeof(int)));
+    for (auto& e : h->ev) CKH(cudaEventCreate(&e));
+#undef CKH
+    *out = h;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_create(const double* X, int64_t n, int32_t m, bnreg_t** out)
+{
+    if (!X) return fail(BNREG_E_INVAL, "X is NULL");
+    bnreg_status s = bnreg_create_ex(n, m, nullptr, out);
+    if (s != BNREG_OK) return s;
+    s = bnreg_load(*out, X, 0);
+    if (s != BNREG_OK) {
+        std::string keep = g_err;
+        bnreg_destroy(*out);
+        *out = nullptr;
+        g_err = keep;
+    }
+    return s;
+}
+
+bnreg_status bnreg_set_stream(bnreg_t* h, void* stream)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
+{
+    if (!h || !X) return fail(BNREG_E_INVAL, "NULL handle or X");
+    const Plan& P = h->plan;
+    const size_t nm = (size_t)P.n * P.m;
+    const double* src = X;
+    if (!x_on_device) {
+        CK(cudaMemcpyAsync(h->dX, X, nm * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        src = h->dX;
+    }
+    CK(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
+    CK(launch_centre(src, P.n, P.m, h->d_order, h->dXr, h->d_status, h->stream));
+    CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
+    int status = 0;
+    CK(cudaMemcpyAsync(&status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->loaded = false;
+    if (status & 2) return fail(BNREG_E_NONFINITE, "X contains NaN or Inf");
+    if (status & 4) return fail(BNREG_E_RANK, "data is rank deficient (|r_jj| <= 1e-12 max column norm)");
+    h->loaded = true;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev)
+{
+    if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
+    if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
+    const int m = h->plan.m;
+    CK(cudaMemcpyAsync(R_dev, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev)
+{
+    if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
+    const int m = h->plan.m;
+    CK(cudaMemcpyAsync(h->d_root, R_dev, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->loaded = true;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
+    const int m = h->plan.m;
+    if (R_host) {
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpy(R_host, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    if (order_host)
+        for (int j = 0; j < m; ++j) order_host[j] = h->plan.root_order[j];
+    return BNREG_OK;
+}
+
+int64_t bnreg_num_families(const bnreg_t* h) { return h ? h->plan.local_families : -1; }
+
+int64_t bnreg_local_index(const bnreg_t* h, int64_t g)
+{
+    if (!h || g < 0 || g >= h->plan.total_families) return -1;
+    return local_index(h->plan, g);
+}
+
+bnreg_status bnreg_shard_ranges(const bnreg_t* h, int64_t* count, int64_t* starts, int64_t* lens)
+{
+    if (!h || !count) return fail(BNREG_E_INVAL, "NULL argument");
+    const Plan& P = h->plan;
+    std::vector<std::pair<int64_t, int64_t>> r;
+    for (int v = 0; v < P.m; ++v) {
+        int64_t cb = (int64_t)v << (P.m - 1);
+        if (P.world == 1) {
+            r.push_back({cb, (int64_t)1 << (P.m - 1)});
+            continue;
+        }
+        bool sel = v >= P.m - P.r;
+        int sh = sel ? (P.m - P.r) : P.shard_shift;
+        r.push_back({cb + ((int64_t)P.pat_lo[v] << sh), (int64_t)1 << sh});
+        if (!sel) r.push_back({cb + ((int64_t)P.pat_hi[v] << sh), (int64_t)1 << sh});
+    }
+    *count = (int64_t)r.size();
+    for (size_t i = 0; i < r.size(); ++i) {
+        if (starts) starts[i] = r[i].first;
+        if (lens) lens[i] = r[i].second;
+    }
+    return BNREG_OK;
+}
+
+static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded (bnreg_load / bnreg_root_received first)");
+    const Plan& P = h->plan;
+    cudaStream_t st = h->stream;
+    if (h->timing) CK(cudaEventRecord(h->ev[0], st));
+    // a5: seed tree levels 0 -> L1 in global memory
+    const double* nodes = h->d_root;
+    for (int L = 0; L < P.L1; ++L) {
+        const double* par = (L == 0) ? h->d_root : h->d_nodes[(L - 1) & 1];
+        double* ch = h->d_nodes[L & 1];
+        CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
+        nodes = ch;
+    }
+    if (h->timing) CK(cudaEventRecord(h->ev[1], st));
+    TravParams T{};
+    T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p;
+    T.NCS = P.m; T.SA = P.m | 1;
+    T.sched_len = (int)P.sched.size();
+    T.npacks = (int)P.packs.size();
+    T.sched = h->d_sched; T.nodes = nodes; T.packs = h->d_packs; T.counter = h->d_counter;
+    T.out_rss = out_rss; T.out_bic = out_bic;
+    T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
+    T.mhalf_n = P.mhalf_n;
+    for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
+    for (int v = 0; v < 32; ++v) {
+        T.child_base[v] = v < P.m ? P.child_base[v] : 0;
+        bool sel = (P.world > 1) && v >= P.m - P.r;
+        T.sh[v] = (P.world == 1) ? P.m - 1 : (sel ? P.m - P.r : P.shard_shift);
+        T.pat_lo[v] = v < P.m ? P.pat_lo[v] : 0;
+    }
+    CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
+    CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
+    if (h->timing) CK(cudaEventRecord(h->ev[2], st));
+    CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->grid_ctas * h->wpc, P.m,
+                          bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask, st));
+    if (h->timing) CK(cudaEventRecord(h->ev[3], st));
+    return BNREG_OK;
+}
+
+static bnreg_status collect_timing(bnreg_t* h)
+{
+    if (!h->timing) return BNREG_OK;
+    CK(cudaEventSynchronize(h->ev[3]));
+    float a = 0, b = 0, c = 0, d = 0;
+    CK(cudaEventElapsedTime(&a, h->ev[0], h->ev[3]));
+    CK(cudaEventElapsedTime(&b, h->ev[0], h->ev[1]));
+    CK(cudaEventElapsedTime(&c, h->ev[1], h->ev[2]));
+    CK(cudaEventElapsedTime(&d, h->ev[2], h->ev[3]));
+    h->acc_ms[0] += a; h->acc_ms[1] += b; h->acc_ms[2] += c; h->acc_ms[3] += d;
+    h->runs += 1;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask, double* best_bic)
+{
+    bnreg_status s = run_impl(h, out_rss, out_bic, nullptr, nullptr);
+    if (s != BNREG_OK) return s;
+    const int m = h->plan.m;
+    if (best_mask)
+        CK(cudaMemcpyAsync(best_mask, h->d_best_mask, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+    if (best_bic)
+        CK(cudaMemcpyAsync(best_bic, h->d_best_bic, m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaGetLastError());
+    return collect_timing(h);
+}
+
+bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev)
+{
+    bnreg_status s = run_impl(h, out_rss, out_bic, bm_dev, bb_dev);
+    if (s != BNREG_OK) return s;
+    if (h->timing) return collect_timing(h);   // timing needs the events: synchronises
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_all_rss(bnreg_t* h, double* out) { return bnreg_run(h, out, nullptr, nullptr, nullptr); }
+bnreg_status bnreg_bic(bnreg_t* h, double* out) { return bnreg_run(h, nullptr, out, nullptr, nullptr); }
+
+bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, const double* bics,
+                              uint32_t* out_mask, double* out_bic)
+{
+    if (m < 2 || m > kMaxM || nparts < 1 || !masks || !bics) return fail(BNREG_E_INVAL, "bad arguments");
+    for (int v = 0; v < m; ++v) {
+        double bb = -INFINITY;
+        uint32_t bm = 0xffffffffu;
+        int bs = 1 << 30;
+        for (int q = 0; q < nparts; ++q) {
+            uint32_t mk = masks[(size_t)q * m + v];
+            if (mk == 0xffffffffu) continue;
+            double b = bics[(size_t)q * m + v];
+            int s = popc(mk);
+            if (b > bb || (b == bb && (s < bs || (s == bs && mk < bm)))) { bb = b; bm = mk; bs = s; }
+        }
+        if (out_mask) out_mask[v] = bm;
+        if (out_bic) out_bic[v] = bb;
+    }
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* runs)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (out_ms)
+        for (int i = 0; i < 4; ++i) out_ms[i] = h->acc_ms[i];
+    if (runs) *runs = h->runs;
+    if (enable == 1) {
+        h->timing = true;
+        for (double& a : h->acc_ms) a = 0;
+        h->runs = 0;
+    } else if (enable == 0) {
+        h->timing = false;
+    }
+    return BNREG_OK;
+}
+
+void bnreg_destroy(bnreg_t* h)
+{
+    if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+}
+
+}  // extern "C"

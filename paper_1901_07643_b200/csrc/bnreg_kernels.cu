@@ -1,0 +1,611 @@
+// bnreg_kernels.cu -- sm_100a kernels of the bnreg hot path.
+//
+//   centre_kernel      a1  centre the columns (fixed-order sums), NaN/Inf flag
+//   tsqr_kernel        a2  TSQR: Householder QR of 256-row leaves in shared
+//                          memory, then a binary tree of [R_a; R_b] merges
+//                          (last-arriving CTA merges), diag > 0, rank check
+//   tree_level_kernel  a5  one level of the Alg.2 seed tree: a node's R for
+//                          the residual of the not-yet-decided variables
+//                          after projecting out the front set F; a pinned
+//                          variable either joins F (drop the leading row and
+//                          column) or the back set B (bubble it behind the
+//                          free block with GRCs)
+//   traverse_kernel    a5-a11 (the hot kernel): one warp runs a PACK of 4
+//                          Alg.2 workers in lockstep (their pinned sets differ
+//                          only in variables 0 and 1), walking d + Upsilon(k)
+//                          with one GRC per step per worker, harvesting every
+//                          new family from suffix sums of squares, computing
+//                          its BIC, storing RSS and BIC (the 4 workers' entries
+//                          of a family are adjacent -> full 32 B sectors), and
+//                          keeping a per-child running best
+//   best_reduce_kernel a11 deterministic argmax over per-warp bests
+//
+// Notation follows the paper: R the triangular factor, GRC_i the swap of
+// positions i,i+1 plus one Givens rotation (Eq.3-4 with the
+// fix G1: c = r_{i,i+1}/h, s = r_{i+1,i+1}/h), Upsilon(k) the greedy schedule.
+#include <cstdint>
+#include <cmath>
+#include "kernels.h"
+
+namespace bnr {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+// Givens coefficients for the GRC (Eq.4 read with G1).  h2 == 0 can only
+// happen on rank-deficient data (rejected at create); identity then.
+__device__ __forceinline__ void givens(double a, double b, double& c, double& s, double& h)
+{
+    double h2 = fma(a, a, b * b);
+    if (h2 > 0.0) {
+        double rh = rsqrt(h2);
+        c = a * rh; s = b * rh; h = h2 * rh;
+    } else {
+        c = 1.0; s = 0.0; h = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------- a1 centre
+// grid = m CTAs (root position j), 256 threads.  Xr is column-major n x m in
+// ROOT order: Xr[:, j] = X[:, root_order[j]] - mean.
+__global__ void __launch_bounds__(256) centre_kernel(const double* __restrict__ X, int64_t n, int m,
+                                                     const int* __restrict__ root_order,
+                                                     double* __restrict__ Xr, int* status)
+{
+    __shared__ double red[8];
+    int j = blockIdx.x;
+    int u = root_order[j];
+    const double* x = X + (int64_t)u * n;
+    double s = 0.0;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double v = x[i];
+        bad |= !isfinite(v);
+        s += v;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, 2);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];   // fixed order
+    double mu = tot / (double)n;
+    double* y = Xr + (int64_t)j * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) y[i] = x[i] - mu;
+}
+
+// ---------------------------------------------------------------- a2 TSQR
+// Householder QR in shared memory of a column-major nr x m tile (ld = nr),
+// 256 threads.  On return the upper triangle holds R (diag may be negative).
+__device__ void householder_tile(double* T, int nr, int m, double* sh)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int j = 0; j < m && j < nr; ++j) {
+        double* cj = T + (int64_t)j * nr;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int i = j + lane; i < nr; i += 32) s = fma(cj[i], cj[i], s);
+            s = warp_sum(s);
+            if (lane == 0) {
+                double x0 = cj[j];
+                double nrm = sqrt(s);
+                double alpha = (x0 > 0.0) ? -nrm : nrm;
+                double v0 = x0 - alpha;
+                double vtv = s - x0 * x0 + v0 * v0;
+                cj[j] = v0;
+                sh[0] = alpha;
+                sh[1] = vtv;
+            }
+        }
+        __syncthreads();
+        double vtv = sh[1];
+        if (vtv > 0.0) {
+            for (int c = j + 1 + warp; c < m; c += nwarp) {
+                double* cc = T + (int64_t)c * nr;
+                double d = 0.0;
+                for (int i = j + lane; i < nr; i += 32) d = fma(cj[i], cc[i], d);
+                d = warp_sum(d);
+                double f = 2.0 * d / vtv;
+                for (int i = j + lane; i < nr; i += 32) cc[i] = fma(-f, cj[i], cc[i]);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) cj[j] = (vtv > 0.0) ? sh[0] : cj[j];
+        for (int i = j + 1 + (int)threadIdx.x; i < nr; i += blockDim.x) cj[i] = 0.0;
+        __syncthreads();
+    }
+}
+
+// rbuf: heap-ordered binary tree of R's (slot 1 = root, leaves at nleaf2 + b),
+// each m*m row-major.  counters: nleaf2 zeroed arrival counters (self-resetting).
+__global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr, int64_t n, int m, int rb,
+                                                   double* rbuf, unsigned* counters, int nleaf2,
+                                                   double* Rroot, int* status)
+{
+    extern __shared__ double smem[];
+    __shared__ double sh[4];
+    __shared__ int s_old;
+    const int b = blockIdx.x;
+    const int64_t r0 = (int64_t)b * rb;
+    int nr = 0;
+    if (r0 < n) nr = (int)((n - r0) < rb ? (n - r0) : rb);
+    int nrp = nr < m ? m : nr;                    // pad to at least m rows
+    double* T = smem;                             // nrp x m, column-major
+    for (int c = 0; c < m; ++c)
+        for (int i = threadIdx.x; i < nrp; i += blockDim.x)
+            T[(int64_t)c * nrp + i] = (i < nr) ? Xr[(int64_t)c * n + r0 + i] : 0.0;
+    __syncthreads();
+    householder_tile(T, nrp, m, sh);
+    int node = nleaf2 + b;
+    double* dst = rbuf + (int64_t)node * m * m;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        int i = e / m, c = e % m;
+        dst[e] = (c >= i) ? T[(int64_t)c * nrp + i] : 0.0;
+    }
+    while (node > 1) {
+        __threadfence();
+        __syncthreads();
+        int parent = node >> 1;
+        if (threadIdx.x == 0) s_old = (int)atomicAdd(&counters[parent], 1u);
+        __syncthreads();
+        if (s_old == 0) return;                   // first arriver: sibling will merge
+        if (threadIdx.x == 0) counters[parent] = 0u;   // reset for the next launch
+        // second arriver: stack [R_left; R_right] (2m x m) and re-factor
+        const double* Lr = rbuf + (int64_t)(2 * parent) * m * m;
+        const double* Rr = rbuf + (int64_t)(2 * parent + 1) * m * m;
+        int nr2 = 2 * m;
+        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+            int i = e / m, c = e % m;
+            T[(int64_t)c * nr2 + i] = __ldcg(Lr + e);
+            T[(int64_t)c * nr2 + m + i] = __ldcg(Rr + e);
+        }
+        __syncthreads();
+        householder_tile(T, nr2, m, sh);
+        node = parent;
+        dst = rbuf + (int64_t)node * m * m;
+        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+            int i = e / m, c = e % m;
+            dst[e] = (c >= i) ? T[(int64_t)c * nr2 + i] : 0.0;
+        }
+        nrp = nr2;
+    }
+    // root: sign-normalise rows (diag > 0), rank check (G26)
+    __syncthreads();
+    const double* R = rbuf + (int64_t)1 * m * m;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        int i = e / m, c = e % m;
+        double d = __ldcg(R + i * m + i);
+        double v = __ldcg(R + e);
+        Rroot[e] = (c < i) ? 0.0 : (d < 0.0 ? -v : v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int c = 0; c < m; ++c) {
+            double s = 0.0;
+            for (int i = 0; i <= c; ++i) s = fma(Rroot[i * m + c], Rroot[i * m + c], s);
+            mx = fmax(mx, sqrt(s));
+        }
+        bool deficient = !(mx > 0.0);
+        for (int j = 0; j < m; ++j)
+            if (!(fabs(Rroot[j * m + j]) > 1e-12 * mx)) deficient = true;
+        if (deficient) atomicOr(status, 4);
+    }
+}
+
+// ---------------------------------------------------------------- GRC on a square R in smem
+// A: row-major with stride SA.  Swap (physical) columns J, J+1 and restore the
+// triangle with one rotation of rows J, J+1.  Columns
+// J+2..end-1 are rotated; rows above J only swap their two entries.
+// Warp-collective (lane = row index for the swap, column index for the rotation).
+__device__ __forceinline__ void grc_square(double* A, int SA, int J, int end, int lane)
+{
+    double a = A[J * SA + J + 1];
+    double b = A[(J + 1) * SA + J + 1];
+    double rjj = A[J * SA + J];
+    double c, s, h;
+    givens(a, b, c, s, h);
+    __syncwarp();
+    int q = lane;
+    if (q < J) {
+        double t0 = A[q * SA + J], t1 = A[q * SA + J + 1];
+        A[q * SA + J] = t1;
+        A[q * SA + J + 1] = t0;
+    } else if (q == J) {
+        A[J * SA + J] = h;
+        A[(J + 1) * SA + J] = 0.0;
+        A[J * SA + J + 1] = c * rjj;
+        A[(J + 1) * SA + J + 1] = -s * rjj;
+    } else if (q >= J + 2 && q < end) {
+        double x = A[J * SA + q], y = A[(J + 1) * SA + q];
+        A[J * SA + q] = fma(c, x, s * y);
+        A[(J + 1) * SA + q] = fma(c, y, -s * x);
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- a5 seed tree level
+// One warp per child node at depth L+1.  Node layout: m*m doubles row-major,
+// top-left s x s used, s = m - |F|.  Node order: [hv[L..bh-1], pack, free, B].
+__global__ void __launch_bounds__(128) tree_level_kernel(const double* __restrict__ parent, double* __restrict__ child,
+                                                         int m, int L, int bh, int p, int k)
+{
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int SA = m | 1;
+    double* A = smem + (size_t)wib * m * SA;
+    const uint32_t q = (uint32_t)(blockIdx.x * (blockDim.x >> 5) + wib);
+    if (q >= (1u << (L + 1))) return;
+    const uint32_t par = q & ((1u << L) - 1u);
+    const int bit = (q >> L) & 1;
+    const int sp = m - __popc(par);
+    const double* src = parent + (size_t)par * m * m;
+    for (int e = lane; e < sp * sp; e += 32) {
+        int r = e / sp, c = e % sp;
+        A[r * SA + c] = src[r * m + c];
+    }
+    __syncwarp();
+    int org = 0;
+    if (bit) {
+        org = 1;
+    } else {
+        int T = (bh - L - 1) + p + k;
+        for (int j = 0; j < T; ++j) grc_square(A, SA, j, sp, lane);
+    }
+    const int sc = sp - bit;
+    double* dst = child + (size_t)q * m * m;
+    for (int e = lane; e < sc * sc; e += 32) {
+        int r = e / sc, c = e % sc;
+        dst[r * m + c] = A[(org + r) * SA + org + c];
+    }
+}
+
+// ---------------------------------------------------------------- a5-a11 traversal
+struct WarpSmem {
+    double* A;       // m x SA square (seed derivation)
+    double* W;       // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k)
+    double* bb;      // [4][32] best BIC
+    uint32_t* bm;    // [4][32] best mask
+    uint32_t* bs;    // [4][32] best |S|
+    uint32_t* pm;    // [17] free-prefix masks (user ids)
+    uint8_t* slotvar;// [32] slot -> user id
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(int m, int k)
+{
+    int SA = m | 1;
+    size_t a = (size_t)m * SA * 8;
+    size_t w = (size_t)(2 * k - 1) * m * 4 * 8;
+    size_t best = 4 * 32 * (8 + 4 + 4);
+    size_t misc = 17 * 4 + 32;
+    size_t tot = a + w + best + misc;
+    return (tot + 15) & ~(size_t)15;
+}
+
+size_t traverse_smem_per_warp(int m, int k) { return warp_smem_bytes(m, k); }
+
+__device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((r * NCS + slot) << 2) + w; }
+
+// One family: index (rank-local), BIC, the two 8 B stores, running best.
+__device__ __forceinline__ void harvest(const TravParams& P, int v, uint32_t S, int size, double rss,
+                                        int w, const WarpSmem& ws)
+{
+    uint32_t lo = S & ((1u << v) - 1u);
+    uint32_t hi = S >> (v + 1);
+    uint32_t cpr = lo | (hi << v);
+    int sh = P.sh[v];
+    long long idx = P.child_base[v] + (long long)(cpr & ((1u << sh) - 1u)) +
+                    (((cpr >> sh) != P.pat_lo[v]) ? (1LL << sh) : 0LL);
+    double bic = (rss <= 1e-300) ? __longlong_as_double(0x7ff0000000000000LL)
+                                 : fma(P.mhalf_n, log(rss), P.Kc[size]);
+    if (P.out_rss) P.out_rss[idx] = rss;
+    if (P.out_bic) P.out_bic[idx] = bic;
+    int bi = (w << 5) + v;
+    double cur = ws.bb[bi];
+    if (bic >= cur) {
+        uint32_t cs = ws.bs[bi], cm = ws.bm[bi];
+        if (bic > cur || (uint32_t)size < cs || ((uint32_t)size == cs && S < cm)) {
+            ws.bb[bi] = bic; ws.bs[bi] = (uint32_t)size; ws.bm[bi] = S;
+        }
+    }
+}
+
+// Logical position (relative to the snapshot origin) of a walk slot for worker
+// w, or -1 when the slot's variable is in that worker's front set.
+__device__ __forceinline__ int slot_pos(int slot, int w, int k, int p, int nw)
+{
+    if (slot < k) return slot;
+    if (slot < k + p) {
+        int j = slot - k;
+        if ((w >> j) & 1) return -1;
+        uint32_t absent_below = (~(uint32_t)w) & ((1u << j) - 1u) & (uint32_t)(nw - 1);
+        return k + __popc(absent_below);
+    }
+    int present = p - __popc((uint32_t)w & (uint32_t)(nw - 1));
+    return k + present + (slot - k - p);
+}
+
+// Snapshot: convert the sub-triangle of A starting at physical origin `org` into
+// worker w's walk state (free rows of R, suffix sums U) and harvest the seed
+// prefixes of sizes d..d+k (reading G11).  Lanes = walk slots.
+__device__ void snapshot(const TravParams& P, const WarpSmem& ws, int org, int w, uint32_t Fmask, int d,
+                         int lane, int NCS, int ncsp)
+{
+    const int k = P.k;
+    if (w >= P.nw) return;
+    int slot = lane;
+    if (slot < ncsp) {
+        int pos = slot_pos(slot, w, k, P.p, P.nw);
+        if (pos < 0) {
+            for (int r = 0; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
+            for (int u = 2; u <= k; ++u) ws.W[Ridx(k + u - 2, slot, w, NCS)] = 0.0;
+        } else {
+            int v = ws.slotvar[slot];
+            double acc = 0.0;
+            const int SA = P.SA;
+            for (int r = pos; r >= 0; --r) {
+                double x = ws.A[(org + r) * SA + org + pos];
+                acc = fma(x, x, acc);
+                if (r < k) ws.W[Ridx(r, slot, w, NCS)] = x;
+                if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
+                if (r <= k) {
+                    uint32_t S = Fmask | (((1u << r) - 1u) << P.p);
+                    harvest(P, v, S, d + r, acc, w, ws);
+                }
+            }
+            for (int r = pos + 1; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
+            for (int u = (pos + 1 > 2 ? pos + 1 : 2); u <= k; ++u) ws.W[Ridx(k + u - 2, slot, w, NCS)] = 0.0;
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ TravParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh, NCS = P.NCS, SA = P.SA;
+    const size_t per = warp_smem_bytes(m, k);
+    unsigned char* base = smem_raw + (size_t)wib * per;
+    WarpSmem ws;
+    ws.A = (double*)base;
+    ws.W = ws.A + (size_t)m * SA;
+    ws.bb = ws.W + (size_t)(2 * k - 1) * NCS * 4;
+    ws.bm = (uint32_t*)(ws.bb + 4 * 32);
+    ws.bs = ws.bm + 4 * 32;
+    ws.pm = ws.bs + 4 * 32;
+    ws.slotvar = (uint8_t*)(ws.pm + 17);
+
+    for (int e = lane; e < 4 * 32; e += 32) {
+        ws.bb[e] = -__longlong_as_double(0x7ff0000000000000LL);
+        ws.bm[e] = 0xffffffffu;
+        ws.bs[e] = 0xffffffffu;
+    }
+    for (int e = lane; e < (2 * k - 1) * NCS * 4; e += 32) ws.W[e] = 0.0;
+    __syncwarp();
+    const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+    const int w = lane & 3;           // worker of this lane within the pack
+    const int cl = lane >> 2;         // lane's column group (0..7)
+    const int NB = NCS - k;           // back slots (pack vars + hi vars in B)
+
+    for (;;) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(P.counter, 1u);
+        item = __shfl_sync(FULLMASK, item, 0);
+        if ((int)item >= P.npacks) break;
+        const uint32_t pack = P.packs[item];
+
+        // ---- seed: load the depth-L1 node, derive the remaining hi levels (a5)
+        const uint32_t nid = pack & ((1u << P.L1) - 1u);
+        const int sn = m - __popc(nid);
+        const double* src = P.nodes + (size_t)nid * m * m;
+        for (int e = lane; e < sn * sn; e += 32) {
+            int r = e / sn, c = e % sn;
+            ws.A[r * SA + c] = src[r * m + c];
+        }
+        __syncwarp();
+        int org = 0;
+        for (int l = P.L1; l < bh; ++l) {
+            if ((pack >> l) & 1u) {
+                ++org;
+            } else {
+                int T = (bh - l - 1) + p + k;
+                for (int j = 0; j < T; ++j) grc_square(ws.A, SA, org + j, sn, lane);
+            }
+        }
+        // slot -> user id: free, pack, then hi vars in B (ascending id = latest deferred first)
+        uint32_t Fhi = 0;
+        for (int l = 0; l < bh; ++l)
+            if ((pack >> l) & 1u) Fhi |= 1u << (m - 1 - l);
+        if (lane < NCS) {
+            int v;
+            if (lane < k) v = p + lane;
+            else if (lane < k + p) v = lane - k;
+            else {
+                int q = lane - k - p, cnt = 0;
+                v = -1;
+                for (int id = p + k; id < m; ++id)
+                    if (!((Fhi >> id) & 1u)) { if (cnt == q) { v = id; break; } ++cnt; }
+                if (v < 0) v = 0;
+            }
+            ws.slotvar[lane] = (uint8_t)v;
+        }
+        const int dh = __popc(pack);
+        const int nbhi = bh - dh;
+        const int NCSp = k + p + nbhi;        // slots in use for this pack
+        __syncwarp();
+
+        // ---- pack derivation: the 2^p workers' seeds by one GRC path (a5)
+        const int o = org;
+        const int end = sn;
+        if (p == 2) {
+            snapshot(P, ws, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
+            for (int j = 1; j <= k; ++j) grc_square(ws.A, SA, o + j, end, lane);
+            snapshot(P, ws, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_square(ws.A, SA, o + j, end, lane);
+            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
+            for (int j = k; j >= 0; --j) grc_square(ws.A, SA, o + j, end, lane);
+            snapshot(P, ws, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
+        } else if (p == 1) {
+            snapshot(P, ws, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_square(ws.A, SA, o + j, end, lane);
+            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
+        } else {
+            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
+        }
+        // slots beyond this pack's back set are never in the walk list
+        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << p) : 0u;
+        __syncwarp();
+
+        // ---- the walk: d + Upsilon(k) in lockstep (a6-a11)
+        uint64_t perm = 0;
+        for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
+        const uint32_t Fw = Fhi | (uint32_t)w;          // pack var j = user id j
+        const int dw = dh + __popc((uint32_t)w);
+        const bool wvalid = w < P.nw;
+        const int NBp = NCSp - k;
+        for (int t = 0; t < P.sched_len; ++t) {
+            const int i = (int)__ldg(P.sched + t) - 1;
+            const int X = (int)((perm >> (4 * i)) & 15u);
+            const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
+            double c, s, h;
+            {
+                double a = ws.W[Ridx(i, Y, w, NCS)];
+                double b = ws.W[Ridx(i + 1, Y, w, NCS)];
+                givens(a, b, c, s, h);
+            }
+            const uint32_t T = ws.pm[i] | (1u << (p + Y));
+            __syncwarp();
+            const uint32_t S = Fw | T;
+            const int size = dw + i + 1;
+            const int nf = k - 1 - i;
+            const int L = nf + NBp;
+            for (int e = cl; e < L; e += 8) {
+                int slot = (e == 0) ? X : (e < nf ? (int)((perm >> (4 * (i + 1 + e))) & 15u) : k + (e - nf));
+                int r0 = Ridx(i, slot, w, NCS), r1 = Ridx(i + 1, slot, w, NCS);
+                double x = ws.W[r0], y = ws.W[r1];
+                double u2 = ws.W[Ridx(k + i, slot, w, NCS)];        // U[i+2]
+                double xn = fma(c, x, s * y);
+                double yn = fma(c, y, -s * x);
+                ws.W[r0] = xn;
+                ws.W[r1] = yn;
+                double rss = fma(yn, yn, u2);
+                if (i >= 1) ws.W[Ridx(k + i - 1, slot, w, NCS)] = rss;   // U[i+1]
+                bool present = wvalid && (slot < k || slot >= k + p || !((w >> (slot - k)) & 1));
+                if (present) harvest(P, ws.slotvar[slot], S, size, rss, w, ws);
+            }
+            if (cl == 0) {
+                ws.W[Ridx(i, Y, w, NCS)] = h;
+                ws.W[Ridx(i + 1, Y, w, NCS)] = 0.0;
+                if (i >= 1) ws.W[Ridx(k + i - 1, Y, w, NCS)] = 0.0;
+            }
+            {
+                uint64_t d = ((perm >> (4 * i)) ^ (perm >> (4 * (i + 1)))) & 15u;
+                perm ^= (d << (4 * i)) | (d << (4 * (i + 1)));
+            }
+            if (lane == 0) ws.pm[i + 1] = T;
+            __syncwarp();
+        }
+        (void)NB;
+    }
+    // ---- per-warp best over its 4 workers -> global partials (a11)
+    __syncwarp();
+    if (lane < m) {
+        double bb = -__longlong_as_double(0x7ff0000000000000LL);
+        uint32_t bm = 0xffffffffu, bs = 0xffffffffu;
+        for (int ww = 0; ww < 4; ++ww) {
+            double b = ws.bb[(ww << 5) + lane];
+            uint32_t s2 = ws.bs[(ww << 5) + lane], m2 = ws.bm[(ww << 5) + lane];
+            if (b > bb || (b == bb && (s2 < bs || (s2 == bs && m2 < bm)))) { bb = b; bs = s2; bm = m2; }
+        }
+        P.part_bic[(size_t)gwarp * m + lane] = bb;
+        P.part_mask[(size_t)gwarp * m + lane] = bm;
+    }
+}
+
+// ---------------------------------------------------------------- a11 best reduce
+__global__ void best_reduce_kernel(const double* __restrict__ part_bic, const uint32_t* __restrict__ part_mask,
+                                   int nparts, int m, double* best_bic, uint32_t* best_mask)
+{
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= m) return;
+    double bb = -__longlong_as_double(0x7ff0000000000000LL);
+    uint32_t bm = 0xffffffffu;
+    int bs = 1 << 30;
+    for (int q = 0; q < nparts; ++q) {
+        double b = part_bic[(size_t)q * m + v];
+        uint32_t mk = part_mask[(size_t)q * m + v];
+        int s = __popc(mk);
+        if (mk == 0xffffffffu) continue;
+        if (b > bb || (b == bb && (s < bs || (s == bs && mk < bm)))) { bb = b; bm = mk; bs = s; }
+    }
+    best_bic[v] = bb;
+    best_mask[v] = bm;
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev, double* Xr, int* status,
+                          cudaStream_t st)
+{
+    centre_kernel<<<m, 256, 0, st>>>(X, n, m, root_order_dev, Xr, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsigned* counters, int nleaf2, int rb,
+                        double* Rroot, int* status, cudaStream_t st)
+{
+    int rows = rb > 2 * m ? rb : 2 * m;
+    if (rows < m) rows = m;
+    size_t smem = (size_t)rows * m * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tsqr_kernel<<<nleaf2, 256, smem, st>>>(Xr, n, m, rb, rbuf, counters, nleaf2, Rroot, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
+                              cudaStream_t st)
+{
+    const int wpc = 4;
+    int nchild = 1 << (L + 1);
+    int grid = (nchild + wpc - 1) / wpc;
+    size_t smem = (size_t)wpc * m * (m | 1) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(tree_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tree_level_kernel<<<grid, wpc * 32, smem, st>>>(parent, child, m, L, bh, p, k);
+    return cudaGetLastError();
+}
+
+int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta)
+{
+    size_t smem = warp_smem_bytes(m, k) * warps_per_cta;
+    cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, traverse_kernel, warps_per_cta * 32, smem) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st)
+{
+    size_t smem = warp_smem_bytes(P.m, P.k) * warps_per_cta;
+    cudaError_t e = cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    traverse_kernel<<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
+                               double* best_bic, uint32_t* best_mask, cudaStream_t st)
+{
+    best_reduce_kernel<<<1, 32, 0, st>>>(part_bic, part_mask, nparts, m, best_bic, best_mask);
+    return cudaGetLastError();
+}
+
+}  // namespace bnr

@@ -1,0 +1,45 @@
+// kernels.h -- launch interface between the C-ABI (bnreg_api.cu) and the
+// sm_100a kernels (bnreg_kernels.cu).  Plain structs, no torch types.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bnr {
+
+// Parameters of the fused traversal kernel (K4 seed derivation + K5 walk +
+// a8 harvest + a9 BIC + a10 store + a11 per-child running best).
+struct TravParams {
+    int m, k, p, bh, L1, nw, NCS, SA;
+    int sched_len;
+    int npacks;
+    int n_int;                  // unused padding / reserved
+    const int8_t* sched;        // Upsilon(k), 1-based swap positions
+    const double* nodes;        // seed-tree nodes at depth L1, m*m doubles each
+    const uint32_t* packs;      // this rank's pack ids (costliest first)
+    unsigned int* counter;      // work-queue counter (zeroed before launch)
+    double* out_rss;            // rank-local RSS table (device) or nullptr
+    double* out_bic;            // rank-local BIC table (device) or nullptr
+    double* part_bic;           // [grid warps][m] per-warp best BIC
+    uint32_t* part_mask;        // [grid warps][m] per-warp best mask
+    double mhalf_n;             // -n/2
+    double Kc[33];              // BIC constant per parent-set size
+    long long child_base[32];   // rank-local layout (plan.h)
+    int sh[32];
+    unsigned pat_lo[32];
+};
+
+// smem bytes per warp of the traversal kernel
+size_t traverse_smem_per_warp(int m, int k);
+
+cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev,
+                          double* Xr, int* status, cudaStream_t st);
+cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsigned* counters,
+                        int nleaf2, int rb, double* Rroot, int* status, cudaStream_t st);
+cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
+                              cudaStream_t st);
+cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st);
+int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta);
+cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
+                               double* best_bic, uint32_t* best_mask, cudaStream_t st);
+
+}  // namespace bnr

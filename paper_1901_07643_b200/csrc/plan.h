@@ -1,0 +1,206 @@
+// plan.h -- host-side plan for the bnreg traversal (pure C++, no CUDA).
+//
+// Everything here is integer bookkeeping that tells the kernels WHAT to walk:
+//   * Upsilon(k), the paper's greedy swap schedule (Alg.1 GreedySwaps with the
+//     +1 of Eq.10; reading G2),
+//   * the Alg.2 partition (readings G7-G11) re-labelled for
+//     the B200 layout: which variables are pinned / free, the pack of 2^p
+//     lockstep workers a warp runs, the order packs are scheduled in, and
+//     which packs a rank owns (complementary top-bit patterns),
+//   * the rank-local table layout (index ranges a rank writes),
+//   * the BIC constants per parent-set size (reading G5).
+//
+// Variable roles (reading G27: any relabelling is valid; the table stays keyed
+// by user ids):
+//   pack vars  ids 0..p-1            (p = min(2, b)); lowest ids so the 2^p
+//                                     workers of a pack write adjacent entries
+//   free vars  ids p..p+k-1           the k variables Upsilon(k) permutes
+//   hi vars    ids p+k..m-1           processed in DEScending id order by the
+//                                     seed tree: hv[l] = m-1-l is bit l of the
+//                                     pack id P (1 = in front set F)
+// A worker = (pack P, w) with w bit j = 1 iff pack var j is in F.
+#pragma once
+#include <cstdint>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+namespace bnr {
+
+constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
+constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
+constexpr int kPackBits = 2;     // 4 lockstep workers per warp
+
+// Alg.1 GreedySwaps(m) with Eq.10's +1.
+// Returns 1-based swap positions, length 2^m - m - 1 (Eq.9).
+inline std::vector<int8_t> greedy_swaps(int m)
+{
+    std::vector<int8_t> s;
+    if (m < 2) return s;
+    s.push_back(1);
+    for (int q = 3; q <= m; ++q) {              // Upsilon(q) from Upsilon(q-1)
+        size_t prev = s.size();
+        for (int i = q - 1; i >= 1; --i) s.push_back((int8_t)i);
+        for (size_t t = 0; t < prev; ++t) s.push_back((int8_t)(s[t] + 1));
+    }
+    return s;
+}
+
+struct Plan {
+    int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh hi bits
+    int L1 = 0, LW = 0;                       // tree depth in global memory / levels derived in-warp
+    int world = 1, rank = 0, r = 0;           // rank selector bits r (0 when world == 1)
+    int64_t n = 0;
+    int64_t total_families = 0;               // m 2^(m-1)
+    int64_t local_families = 0;               // this rank's share
+    std::vector<int8_t> sched;                // Upsilon(k), 1-based
+    std::vector<uint32_t> packs;              // this rank's pack ids, costliest first
+    std::vector<int> root_order;              // position -> user id of the root R
+    // rank-local layout: per child, up to 2 ranges of the child's 2^(m-1) block
+    int64_t child_base[32] = {0};             // local offset of child v's first range
+    int32_t shard_shift = 0;                  // m-1-r : low bits kept inside a range
+    uint32_t pat_lo[32] = {0}, pat_hi[32] = {0}; // per child: selector patterns of range 0 / 1
+    int32_t nrange[32] = {0};
+    double bic_const[33] = {0};               // K(s) = (n/2)ln n - (n/2)(1+ln 2pi) - (s/2) ln n
+    double mhalf_n = 0;                       // -n/2
+};
+
+inline int popc(uint32_t x) { return __builtin_popcount(x); }
+
+// Cost of a pack in families (sum over its 2^p workers of 2^(k-1)(2(m-d)-k)).
+inline int64_t pack_cost(const Plan& P, uint32_t pack)
+{
+    int64_t c = 0;
+    int dh = popc(pack);
+    for (int w = 0; w < (1 << P.p); ++w) {
+        int d = dh + popc((uint32_t)w);
+        c += (int64_t(1) << (P.k - 1)) * (2 * (P.m - d) - P.k);
+    }
+    return c;
+}
+
+// k: requested free count (0 = auto).  lw: tree levels derived in-warp (-1 = auto).
+inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
+{
+    Plan P;
+    if (m < 2 || m > kMaxM) throw std::invalid_argument("m must be in [2, 30]");
+    if (n < m + 1) throw std::invalid_argument("need n >= m + 1");
+    if (world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
+        throw std::invalid_argument("world must be a power of two and 0 <= rank < world");
+    if (k <= 0) k = std::min(m, 8);
+    if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
+    P.m = m; P.n = n; P.k = k; P.b = m - k;
+    P.p = std::min(kPackBits, P.b);
+    P.bh = P.b - P.p;
+    if (lw < 0) lw = 4;
+    P.LW = std::min(lw, P.bh);
+    P.L1 = P.bh - P.LW;
+    P.world = world; P.rank = rank;
+    P.total_families = (int64_t)m << (m - 1);
+    P.sched = greedy_swaps(k);
+    // root order: [hv[0..bh-1], pack 0..p-1, free p..p+k-1]
+    for (int l = 0; l < P.bh; ++l) P.root_order.push_back(m - 1 - l);
+    for (int j = 0; j < P.p; ++j) P.root_order.push_back(j);
+    for (int f = 0; f < k; ++f) P.root_order.push_back(P.p + f);
+
+    // rank selector: top r hi bits (hv[0..r-1] = ids m-1..m-r), complementary patterns
+    if (world > 1) {
+        int r = 0;
+        while ((1 << r) < 2 * world) ++r;
+        if (r > P.bh) throw std::invalid_argument("too few pinned variables for this world size (lower k)");
+        P.r = r;
+    }
+    uint32_t tmask = (1u << P.r) - 1u;
+    uint32_t t0 = (uint32_t)rank, t1 = tmask ^ (uint32_t)rank;
+    std::vector<uint32_t> all;
+    for (uint32_t q = 0; q < (1u << P.bh); ++q)
+        if (world == 1 || (q & tmask) == t0 || (q & tmask) == t1) all.push_back(q);
+    std::stable_sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) {
+        int64_t ca = pack_cost(P, a), cb = pack_cost(P, b);
+        return ca != cb ? ca > cb : a < b;
+    });
+    P.packs = all;
+
+    // rank-local layout.  Bits of the compressed mask of child v: the top r
+    // positions (m-1-r .. m-2) hold hv[0..r-1] when v is not one of them.
+    if (world == 1) {
+        P.shard_shift = m - 1;
+        for (int v = 0; v < m; ++v) {
+            P.child_base[v] = (int64_t)v << (m - 1);
+            P.nrange[v] = 1; P.pat_lo[v] = 0; P.pat_hi[v] = 0;
+        }
+        P.local_families = P.total_families;
+    } else {
+        int64_t off = 0;
+        for (int v = 0; v < m; ++v) {
+            P.child_base[v] = off;
+            int lv = m - 1 - v;                          // hi level of v, if v is a selector var
+            bool sel = v >= m - P.r;
+            if (!sel) {
+                // selector bits sit at compressed positions m-1-r..m-2, bit order:
+                // compressed bit (m-1-r)+j  <->  user id m-r+j  <->  hi level r-1-j
+                auto to_comp = [&](uint32_t t) {
+                    uint32_t c = 0;
+                    for (int l = 0; l < P.r; ++l)
+                        if ((t >> l) & 1u) c |= 1u << (P.r - 1 - l);
+                    return c;
+                };
+                uint32_t a = to_comp(t0), b = to_comp(t1);
+                P.pat_lo[v] = std::min(a, b); P.pat_hi[v] = std::max(a, b);
+                P.nrange[v] = 2;
+                off += (int64_t)2 << (m - 1 - P.r);
+            } else {
+                // v is hv[lv]; it must be in B, so only the pattern with bit lv = 0 owns it
+                uint32_t t = ((t0 >> lv) & 1u) ? t1 : t0;
+                // remaining r-1 selector bits, compressed: positions m-r..m-2 after deleting v
+                uint32_t c = 0;
+                int pos = 0;
+                for (int id = m - P.r; id < m; ++id) {
+                    if (id == v) continue;
+                    int l = m - 1 - id;
+                    if ((t >> l) & 1u) c |= 1u << pos;
+                    ++pos;
+                }
+                P.pat_lo[v] = c; P.pat_hi[v] = c;
+                P.nrange[v] = 1;
+                off += (int64_t)1 << (m - P.r);
+            }
+        }
+        P.local_families = off;
+    }
+    P.shard_shift = (world == 1) ? (m - 1) : (m - 1 - P.r);
+
+    long double nn = (long double)n;
+    long double l2pi = logl(2.0L * 3.14159265358979323846264338327950288L);
+    for (int s = 0; s <= 32; ++s)
+        P.bic_const[s] = (double)((nn / 2) * logl(nn) - (nn / 2) * (1.0L + l2pi) - ((long double)s / 2) * logl(nn));
+    P.mhalf_n = -(double)n / 2.0;
+    return P;
+}
+
+// Global flat index (SPEC.md:179 / D6): child 2^(m-1) + compress(mask, child).
+inline int64_t family_index(int m, int child, uint32_t mask)
+{
+    if (child < 0 || child >= m || ((mask >> child) & 1u)) return -1;
+    uint64_t lo = mask & ((1u << child) - 1u);
+    uint64_t hi = (uint64_t)mask >> (child + 1);
+    return ((int64_t)child << (m - 1)) + (int64_t)(lo | (hi << child));
+}
+
+// Rank-local offset of a global index, or -1 if another rank owns it.
+inline int64_t local_index(const Plan& P, int64_t gidx)
+{
+    int v = (int)(gidx >> (P.m - 1));
+    uint64_t c = (uint64_t)gidx & ((1ull << (P.m - 1)) - 1ull);
+    if (P.world == 1) return gidx;
+    bool sel = v >= P.m - P.r;
+    int sh = sel ? (P.m - P.r) : P.shard_shift;
+    uint64_t pat = c >> sh, low = c & ((1ull << sh) - 1ull);
+    if (pat == P.pat_lo[v]) return P.child_base[v] + (int64_t)low;
+    if (!sel && pat == P.pat_hi[v]) return P.child_base[v] + ((int64_t)1 << sh) + (int64_t)low;
+    return -1;
+}
+
+}  // namespace bnr

@@ -1,0 +1,34 @@
+"""Helpers for the GPU parity tests: run the C-ABI path on torch device buffers."""
+from __future__ import annotations
+
+import numpy as np
+
+import paper_1901_07643_b200 as bn
+
+
+def run_tables(X, opt=None, want_rss=True, want_bic=True, fill=np.nan, device_load=False):
+    """Create + load + run; returns (rss, bic, best_mask, best_bic, handle) with
+    tables as numpy arrays in the handle's (rank-local) layout."""
+    import torch
+    X = np.asfortranarray(X, dtype=np.float64)
+    n, m = X.shape
+    h = bn.Bnreg(n, m, opt)
+    if device_load:
+        Xd = torch.from_numpy(X.T.copy()).cuda()  # (m, n) row-major == column-major (n, m)
+        h.load(Xd.data_ptr())
+    else:
+        h.load(X)
+    F = h.num_families()
+    r = torch.full((F,), fill, dtype=torch.float64, device="cuda") if want_rss else None
+    b = torch.full((F,), fill, dtype=torch.float64, device="cuda") if want_bic else None
+    bm, bb = h.run(r, b)
+    torch.cuda.synchronize()
+    rr = r.cpu().numpy() if r is not None else None
+    bbt = b.cpu().numpy() if b is not None else None
+    return rr, bbt, bm, bb, h
+
+
+def rel_err(got, ref):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    return np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)

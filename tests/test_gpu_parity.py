@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
+element, on seeded inputs.  Tolerances (north_star):
+RSS relative <= 1e-9, BIC absolute <= 1e-6, per-child argmax exact."""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RSS_RTOL = 1e-9
+BIC_ATOL = 1e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1901_07643_b200 as bn
+    bn.lib()
+
+
+def _bn():
+    import paper_1901_07643_b200 as bn
+    return bn
+
+
+def _check_full(X, opt=None, o2=False, threads=0):
+    from gpu_util import run_tables
+    Xc = oracle.centre(X)
+    n, m = X.shape
+    rss, bic, bm, bb, h = run_tables(X, opt)
+    assert not np.isnan(rss).any(), f"{np.isnan(rss).sum()} RSS entries never written"
+    assert not np.isnan(bic).any(), f"{np.isnan(bic).sum()} BIC entries never written"
+    if o2:
+        R0 = oracle.qr_r(Xc)
+        ref = oracle.rss_reduced_indices(R0, None, threads)
+    else:
+        ref, _ = oracle.table(Xc, want_bic=False, threads=threads)
+    err = np.abs(rss - ref) / ref
+    assert err.max() <= RSS_RTOL, f"max rel RSS err {err.max():.3e} at {int(err.argmax())}"
+    # BIC from the oracle's RSS through the oracle's BIC (reading G5)
+    _, S = oracle.masks_of(m, np.arange(m << (m - 1)))
+    ks = np.array([bin(int(s)).count("1") for s in S])
+    ref_bic = -(n / 2) * np.log(ref / n) - (n / 2) * (1 + np.log(2 * np.pi)) - (ks / 2) * np.log(n)
+    berr = np.abs(bic - ref_bic)
+    assert berr.max() <= BIC_ATOL, f"max abs BIC err {berr.max():.3e}"
+    om, ob = oracle.best(ref_bic, m)
+    assert np.array_equal(bm, om), f"argmax mismatch: {bm} vs {om}"
+    np.testing.assert_allclose(bb, ob, atol=BIC_ATOL)
+    h.close()
+    return rss, bic
+
+
+def test_golden_m3():
+    from gpu_util import run_tables
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "m3_table.json")))
+    X = np.asfortranarray(np.array(g["rows"], dtype=float))
+    rss, bic, bm, bb, h = run_tables(X)
+    for e in g["table"]:
+        assert rss[e["idx"]] == pytest.approx(float(Fraction(e["rss"])), rel=1e-12)
+        assert bic[e["idx"]] == pytest.approx(e["bic"], abs=1e-10)
+    assert [int(x) for x in bm] == [g["best"][str(v)] for v in range(3)]
+    h.close()
+
+
+@pytest.mark.parametrize("k", [8, 6, 4, 3, 2])
+def test_cfg1_full_all_k(k):
+    """cfg1 (m=8, n=100): every free-block size, so packs, tree levels and the
+    single-worker case (k = m) are all exercised."""
+    bn = _bn()
+    X = datagen.config_data(1)
+    _check_full(X, bn.options(free_vars=k))
+
+
+@pytest.mark.parametrize("lw", [0, 1, 2, 5])
+def test_tree_split_levels(lw):
+    """Same table whatever split of the seed tree between global levels and
+    in-warp derivation."""
+    bn = _bn()
+    X = datagen.dag_data(11, 300, 0.3, 0.5, 2.0, seed=77)
+    _check_full(X, bn.options(free_vars=4, levels_in_warp=lw))
+
+
+@pytest.mark.parametrize("m,k,seed", [(5, 2, 1), (6, 3, 2), (9, 5, 3), (10, 7, 4), (12, 8, 5), (13, 6, 6)])
+def test_small_random(m, k, seed):
+    bn = _bn()
+    X = datagen.gaussian(4 * m + 7, m, seed=seed, offset=3.0)
+    _check_full(X, bn.options(free_vars=k))
+
+
+def test_cfg2_full_o1():
+    X = datagen.config_data(2)
+    _check_full(X)
+
+
+def test_cfg3_collinear_full_o2_and_o1_sample():
+    """m=20, n=5000 with a near-collinear pair: full table against O2 (O2 itself
+    pinned to O1 in test_oracle_pins), plus an O1 sample touching the pair."""
+    from gpu_util import run_tables
+    meta = {}
+    X = datagen.config_data(3, meta=meta)
+    rss, bic = _check_full(X, o2=True)
+    Xc = oracle.centre(X)
+    m = 20
+    i, j = meta["pair"]
+    rng = np.random.default_rng(5)
+    idx = []
+    for _ in range(300):
+        v = int(rng.integers(0, m))
+        S = int(rng.integers(0, 1 << m)) & ~(1 << v)
+        if v not in (i, j):
+            S |= (1 << i) if rng.random() < 0.5 else (1 << j)
+        idx.append(oracle.index(m, v, S))
+    idx = np.array(sorted(set(idx)), dtype=np.int64)
+    ref = oracle.rss_indices(Xc, idx)
+    err = np.abs(rss[idx] - ref) / ref
+    assert err.max() <= RSS_RTOL
+
+
+def test_errors_nonfinite_and_rank():
+    bn = _bn()
+    X = datagen.gaussian(50, 5, seed=1)
+    X[7, 2] = np.inf
+    with pytest.raises(bn.BnregError) as e:
+        bn.Bnreg.create(X)
+    assert e.value.status == bn.E_NONFINITE
+    X = datagen.gaussian(50, 5, seed=1)
+    X[:, 3] = 2.0 * X[:, 1]
+    with pytest.raises(bn.BnregError) as e:
+        bn.Bnreg.create(X)
+    assert e.value.status == bn.E_RANK
+    with pytest.raises(bn.BnregError) as e:
+        bn.Bnreg(3, 5)
+    assert e.value.status == bn.E_INVAL
+
+
+def test_root_r_gram():
+    bn = _bn()
+    X = datagen.config_data(3)
+    Xc = oracle.centre(X)
+    h = bn.Bnreg.create(X)
+    R, order = h.root_r()
+    G = Xc[:, order].T @ Xc[:, order]
+    assert np.linalg.norm(R.T @ R - G) <= 1e-10 * np.linalg.norm(G)
+    assert np.all(np.diag(R) > 0) and np.allclose(np.tril(R, -1), 0)
+    Ro = oracle.qr_r(np.asfortranarray(Xc[:, order]))
+    np.testing.assert_allclose(np.abs(np.diag(R)), np.abs(np.diag(Ro)), rtol=1e-7)
+    h.close()
+
+
+def test_deterministic_and_device_load():
+    from gpu_util import run_tables
+    X = datagen.config_data(2)
+    a = run_tables(X)
+    b = run_tables(X, device_load=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2])
+    a[4].close(); b[4].close()
+
+
+def test_all_rss_and_bic_entry_points():
+    import torch
+    bn = _bn()
+    X = datagen.config_data(1)
+    h = bn.Bnreg.create(X, bn.options(free_vars=4))
+    F = h.num_families()
+    r = torch.full((F,), np.nan, dtype=torch.float64, device="cuda")
+    b = torch.full((F,), np.nan, dtype=torch.float64, device="cuda")
+    h.all_rss(r)
+    h.bic(b)
+    r2 = torch.zeros(F, dtype=torch.float64, device="cuda")
+    b2 = torch.zeros(F, dtype=torch.float64, device="cuda")
+    h.run(r2, b2)
+    assert torch.equal(r, r2) and torch.equal(b, b2)
+    h.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_logical_ranks_union(world):
+    """Multi-GPU partition run rank by rank on one GPU: shards are disjoint,
+    their union is the whole table, and the merged best is the global best."""
+    from gpu_util import run_tables
+    bn = _bn()
+    X = datagen.dag_data(12, 200, 0.25, 0.5, 2.0, seed=12)
+    m = 12
+    full, fullb, fbm, fbb, h0 = run_tables(X, bn.options(free_vars=5))
+    h0.close()
+    seen = np.zeros(m << (m - 1), dtype=np.int32)
+    masks, bics = [], []
+    for rank in range(world):
+        rss, bic, bm, bb, h = run_tables(X, bn.options(free_vars=5, world=world, rank=rank))
+        starts, lens = h.shard_ranges()
+        gidx = np.concatenate([np.arange(s, s + l) for s, l in zip(starts, lens)])
+        assert len(gidx) == h.num_families() == len(rss)
+        step = max(1, len(gidx) // 500)
+        assert all(h.local_index(int(gidx[q])) == q for q in range(0, len(gidx), step))
+        seen[gidx] += 1
+        assert not np.isnan(rss).any()
+        np.testing.assert_array_equal(rss, full[gidx])
+        np.testing.assert_array_equal(bic, fullb[gidx])
+        masks.append(bm); bics.append(bb)
+        h.close()
+    assert (seen == 1).all()
+    mm, mb = bn.bnreg_best_merge(m, np.array(masks), np.array(bics))
+    assert np.array_equal(mm, fbm)
