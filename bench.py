@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- families (child, parent-set) RSS+BIC per second on B200.
+
+One "step" = the whole hot path over one synthetic dataset: centre + TSQR of X
+(a1-a2), [multi-GPU: NCCL broadcast of R (a3)], seed tree + fused traversal
+(a4-a10: GRCs, suffix-sum harvest, BIC, RSS+BIC stores into the (child, mask)
+table) + per-child best (a11) [multi-GPU: NCCL all-gather of the per-rank bests
+and the deterministic merge].  Workload: BASELINE.json configs[4] (m=28,
+n=2000; the config the north-star metric is quoted on; it fits one B200: the
+RSS+BIC tables are 60 GB).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C] [--impl reference]
+
+Prints ONE JSON line on rank 0.  value = all families of all ranks / the max
+over ranks of the device time of K steps (CUDA events on the launching stream,
+barrier + synchronize on both sides).  e2e = the same metric through the
+public C-ABI with X in pinned HOST memory (H2D inside the step) and the
+per-child best read back to the host (D2H) every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "families (child,parent-set) RSS+BIC per second"
+UNIT = "families/s"
+BYTES_PER_FAMILY = 16  # 8 B RSS + 8 B BIC written per family
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--k", type=int, default=0, help="free block size (0 = library default)")
+    ap.add_argument("--lw", type=int, default=-1, help="seed-tree levels derived in-warp (-1 = default)")
+    ap.add_argument("--wpc", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg):
+    """dram read+write bytes per traverse launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "traverse_ncu_summary.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if d.get("config") == cfg and d.get("traffic_bytes_per_launch"):
+            return float(d["traffic_bytes_per_launch"])
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle timing
+def oracle_rate(X, seconds, seed=1234, batch=256):
+    """The oracle (O1, per-family Householder, OpenMP over families) as it stands,
+    on a bounded uniform sample of the workload's families."""
+    import numpy as np
+    import datagen
+    import oracle
+    n, m = X.shape
+    Xc = oracle.centre(X)
+    idx = datagen.sample_indices(m, 200000, seed)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds and done < len(idx):
+        oracle.rss_indices(Xc, idx[done:done + batch])
+        done += min(batch, len(idx) - done)
+        batch = min(batch * 2, 8192)
+    el = time.perf_counter() - t0
+    return done / el, done, el, oracle.num_threads()
+
+
+def bench_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import datagen
+    X = datagen.config_data(args.config, args.seed)
+    n, m = X.shape
+    import numpy as np
+    import oracle
+    Xc = oracle.centre(X)
+    per_step = 2048
+    idx = datagen.sample_indices(m, per_step * (args.steps + args.warmup), 99)
+    for s in range(args.warmup):
+        oracle.rss_indices(Xc, idx[s * per_step:(s + 1) * per_step])
+    t0 = time.perf_counter()
+    for s in range(args.warmup, args.warmup + args.steps):
+        r = oracle.rss_indices(Xc, idx[s * per_step:(s + 1) * per_step])
+        _, S = oracle.masks_of(m, idx[s * per_step:(s + 1) * per_step])
+        oracle.bic_array(r, n, [bin(int(q)).count("1") for q in S])
+    el = time.perf_counter() - t0
+    val = per_step * args.steps / el
+    sample = (f"{per_step} families per step, uniform over the m*2^(m-1) = {m << (m - 1)} families "
+              f"of cfg{args.config} (O1 per-family Householder QR + BIC, n={n})")
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": f"cfg{args.config}", "m": m, "n": n},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------- ours
+def bench_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import datagen
+    import paper_1901_07643_b200 as bn
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    X = datagen.config_data(args.config, args.seed)
+    n, m = X.shape
+    opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, warps_per_cta=args.wpc)
+    h = bn.Bnreg(n, m, opt)
+    plan = bn.bnreg_plan_query(m, n, opt)
+    stream = torch.cuda.current_stream(dev)
+    h.set_stream(stream.cuda_stream)
+    F = h.num_families()
+    total = m << (m - 1)
+    rss = torch.empty(F, dtype=torch.float64, device=dev)
+    bic = torch.empty(F, dtype=torch.float64, device=dev)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)       # column-major n x m
+    Rt = torch.empty(m * m, dtype=torch.float64, device=dev)
+    bm_d = torch.empty(m, dtype=torch.int32, device=dev)
+    bb_d = torch.empty(m, dtype=torch.float64, device=dev)
+    Xpin = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()
+    Xpin_np = Xpin.numpy().T                                         # Fortran view of pinned memory
+
+    def broadcast_root():
+        if world > 1:
+            if rank == 0:
+                h.get_root_device(Rt)
+            dist.broadcast(Rt, 0)
+            if rank != 0:
+                h.set_root_device(Rt)
+
+    def gather_best(bm_host=None, bb_host=None):
+        if world == 1:
+            return
+        gm = [torch.empty_like(bm_d) for _ in range(world)]
+        gb = [torch.empty_like(bb_d) for _ in range(world)]
+        dist.all_gather(gm, bm_d)
+        dist.all_gather(gb, bb_d)
+        M = torch.stack(gm).cpu().numpy().view(np.uint32)
+        B = torch.stack(gb).cpu().numpy()
+        bn.bnreg_best_merge(m, M, B)
+
+    def step_device():
+        if rank == 0:
+            h.load(Xd)
+        broadcast_root()
+        h.run_async(rss, bic, bm_d, bb_d)
+        gather_best()
+
+    def step_e2e():
+        if rank == 0:
+            h.load(Xpin_np)                      # H2D of X from pinned host memory
+        broadcast_root()
+        bm, bb = h.run(rss, bic)                 # D2H of the per-child best
+        if world > 1:
+            bm_d.copy_(torch.from_numpy(bm.view(np.int32)))
+            bb_d.copy_(torch.from_numpy(bb))
+            gather_best()
+
+    def timed(step, k, w, with_clocks=False):
+        for _ in range(w):
+            step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clk = Clocks(local) if with_clocks else None
+        if clk:
+            clk.start()
+            time.sleep(0.3)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        clocks = clk.stop() if clk else None
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, clocks
+
+    # device-resident inputs: the headline value + the traversal kernel's own time
+    h.timing(1)
+    ms, clocks = timed(step_device, args.steps, args.warmup, with_clocks=True)
+    h.timing(1)
+    ms_chk, _ = timed(step_device, args.steps, 0)
+    tms, runs = h.timing(0)
+    trav_ms = tms[2] / max(runs, 1)
+    run_ms = tms[0] / max(runs, 1)
+    value = total * args.steps / (ms / 1e3)
+    e2e = None
+    if not args.no_e2e:
+        ms_e2e, _ = timed(step_e2e, args.steps, 1)
+        e2e = {"value": total * args.steps / (ms_e2e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": world * m * (4 + 8),
+               "ms_per_step": ms_e2e / args.steps}
+    peak, peak_src = load_peaks()
+    achieved = BYTES_PER_FAMILY * F / (trav_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(f"cfg{args.config}"), "kernel": "traverse_kernel",
+            "kernel_ms": trav_ms, "algorithmic_bytes_per_launch": BYTES_PER_FAMILY * F,
+            "peak_source": peak_src,
+            "step_frac": (BYTES_PER_FAMILY * total * args.steps / (ms / 1e3) / 1e9) / peak / world}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, done, el, cores = oracle_rate(X, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{done} families uniformly sampled from cfg{args.config}'s {total} "
+                         f"(O1 per-family Householder QR, n={n}), {el:.1f} s on the host"}
+    launches = args.steps * (plan["L1"] + 2 + (2 if rank == 0 else 0))
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded linear-Gaussian DAG, BASELINE.json configs recipe; datagen/)",
+               "config": {"workload": f"cfg{args.config}", "m": m, "n": n,
+                          "seed": args.seed if args.seed is not None else 1000 * args.config + 1,
+                          "families": total, "k": plan["k"], "pinned": plan["b"], "tree_levels_global": plan["L1"],
+                          "packs": plan["npacks"], "parallelism": f"lattice-sharded x{world}",
+                          "l2": "outputs (16 B/family, %.1f GB) >> L2 126 MB: every step evicts L2" % (
+                              BYTES_PER_FAMILY * total / 1e9)},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+               "ms_per_step_recheck": ms_chk / args.steps, "run_ms_device": run_ms}
+        print(json.dumps(out), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()
