@@ -146,6 +146,10 @@ int64_t bnreg_schedule(int32_t k, int8_t* out, int64_t cap);
 /* Pack ids of a plan in launch order (host only); returns the count. */
 int64_t bnreg_plan_packs(int32_t m, int64_t n, const bnreg_options* opt, uint32_t* out, int64_t cap);
 
+/* Test hook: the fp64 natural log the BIC epilogue uses (a9), applied to
+ * count DEVICE doubles x_dev (> 1e-300, finite) -> out_dev.  Synchronous. */
+bnreg_status bnreg_debug_ln(bnreg_t* h, const double* x_dev, double* out_dev, int64_t count);
+
 const char* bnreg_last_error(void);
 
 void bnreg_destroy(bnreg_t* h);   /* NULL-safe; frees device state */

@@ -27,7 +27,7 @@ SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families"
            "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_best_merge", "bnreg_timing", "bnreg_plan_query",
-           "bnreg_schedule", "bnreg_plan_packs", "bnreg_last_error", "bnreg_destroy"]
+           "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_last_error", "bnreg_destroy"]
 
 
 class BnregError(RuntimeError):
@@ -82,6 +82,7 @@ def lib():
         "bnreg_plan_query": ([i32, i64, POPT, P], i32),
         "bnreg_schedule": ([i32, P, i64], i64),
         "bnreg_plan_packs": ([i32, i64, POPT, P, i64], i64),
+        "bnreg_debug_ln": ([H, P, P, i64], i32),
         "bnreg_last_error": ([], ctypes.c_char_p),
         "bnreg_destroy": ([H], None),
     }
@@ -234,6 +235,10 @@ class Bnreg:
         runs = ctypes.c_int64(0)
         _check(lib().bnreg_timing(self._h, enable, _hptr(ms), ctypes.byref(runs)))
         return ms, runs.value
+
+    def debug_ln(self, x_dev, out_dev, count: int):
+        """Test hook: the BIC epilogue's fp64 log on device buffers."""
+        _check(lib().bnreg_debug_ln(self._h, _dptr(x_dev), _dptr(out_dev), count))
 
     def close(self):
         if getattr(self, "_h", None):

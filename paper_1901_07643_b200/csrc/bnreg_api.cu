@@ -8,6 +8,7 @@
 #include <vector>
 #include <algorithm>
 #include <stdexcept>
+#include <cmath>
 
 #include "../../include/bnreg.h"
 #include "kernels.h"
@@ -57,6 +58,7 @@ struct bnreg {
     double* d_best_bic = nullptr;
     uint32_t* d_best_mask = nullptr;
     int* d_status = nullptr;
+    double2* d_lntab = nullptr;    // fast-log table (a9)
     int grid_ctas = 0, wpc = 2;
     bool loaded = false;
     // timing
@@ -82,7 +84,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_sched, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status};
+                    h->d_best_mask, h->d_status, h->d_lntab};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -202,6 +204,18 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
     CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
+    {
+        // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/128)); -ln r_j in long double
+        std::vector<double2> tab(128);
+        for (int j = 0; j < 128; ++j) {
+            long double t = 1.0L + ((long double)j + 0.5L) / 128.0L;
+            double r = (double)(1.0L / t);
+            tab[j].x = r;
+            tab[j].y = (double)(-logl((long double)r));
+        }
+        CKH(cudaMalloc(&h->d_lntab, 128 * sizeof(double2)));
+        CKH(cudaMemcpy(h->d_lntab, tab.data(), 128 * sizeof(double2), cudaMemcpyHostToDevice));
+    }
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
 #undef CKH
     *out = h;
@@ -344,6 +358,8 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.out_rss = out_rss; T.out_bic = out_bic;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
+    T.lntab = h->d_lntab;
+    T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
     for (int v = 0; v < 32; ++v) {
         T.child_base[v] = v < P.m ? P.child_base[v] : 0;
@@ -433,6 +449,14 @@ bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* r
     } else if (enable == 0) {
         h->timing = false;
     }
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_debug_ln(bnreg_t* h, const double* x_dev, double* out_dev, int64_t count)
+{
+    if (!h || (!x_dev && count > 0) || (!out_dev && count > 0)) return fail(BNREG_E_INVAL, "NULL argument");
+    CK(launch_debug_ln(x_dev, out_dev, count, h->d_lntab, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     return BNREG_OK;
 }
 

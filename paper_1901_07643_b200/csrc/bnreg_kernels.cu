@@ -267,51 +267,117 @@ __global__ void __launch_bounds__(128) tree_level_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------- a5-a11 traversal
+// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 7 bits of
+// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/128) (host,
+// long double); u = f r_j - 1 (|u| <= 3.9e-3);  ln x = e ln2 + (-ln r_j) + log1p(u),
+// log1p by its degree-6 Taylor polynomial (truncation u^7/7 < 2e-18).
+// Absolute error ~1e-15 for the RSS range of the table (|e| < 1024), i.e. a
+// BIC error < 1e-11 at n = 1e4.
+__device__ __forceinline__ double fast_ln(double x, const double2* __restrict__ tab)
+{
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) - 1023;
+    const int j = (hi >> 13) & 127;
+    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 t = __ldg(tab + j);
+    const double u = fma(f, t.x, -1.0);
+    double q = fma(u, -1.0 / 6.0, 0.2);
+    q = fma(u, q, -0.25);
+    q = fma(u, q, 1.0 / 3.0);
+    q = fma(u, q, -0.5);
+    q = fma(u, q, 1.0);
+    const double ed = (double)e;
+    return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(u, q, t.y)));
+}
+
+__device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((r * NCS + slot) << 2) + w; }
+
+// Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
+__device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
+
+// GRC on the packed triangle (same operation as grc_square).
+__device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int lane)
+{
+    const int oJ = poff(J, s), oJ1 = poff(J + 1, s);
+    double a = A[oJ + 1];
+    double b = A[oJ1];
+    double rjj = A[oJ];
+    double c, sn, h;
+    givens(a, b, c, sn, h);
+    __syncwarp();
+    const int q = lane;
+    if (q < J) {
+        const int oq = poff(q, s);
+        double t0 = A[oq + J - q], t1 = A[oq + J + 1 - q];
+        A[oq + J - q] = t1;
+        A[oq + J + 1 - q] = t0;
+    } else if (q == J) {
+        A[oJ] = h;
+        A[oJ + 1] = c * rjj;
+        A[oJ1] = -sn * rjj;
+    } else if (q >= J + 2 && q < end) {
+        double x = A[oJ + q - J], y = A[oJ1 + q - J - 1];
+        A[oJ + q - J] = fma(c, x, sn * y);
+        A[oJ1 + q - J - 1] = fma(c, y, -sn * x);
+    }
+    __syncwarp();
+}
+
 struct WarpSmem {
-    double* A;       // m x SA square (seed derivation)
-    double* W;       // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k)
-    double* bb;      // [4][32] best BIC
-    uint32_t* bm;    // [4][32] best mask
-    uint32_t* bs;    // [4][32] best |S|
-    uint32_t* pm;    // [17] free-prefix masks (user ids)
-    uint8_t* slotvar;// [32] slot -> user id
+    double* A;        // packed triangle, side <= m (seed derivation)
+    double* W;        // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k)
+    double* bb;       // [4][32] best BIC
+    uint32_t* bm;     // [4][32] best mask
+    uint32_t* pm;     // [17] free-prefix masks (user ids) by prefix length
+    uint8_t* posmap;  // [16] free position -> free slot
+    uint8_t* slotvar; // [32] slot -> user id
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int m, int k)
 {
-    int SA = m | 1;
-    size_t a = (size_t)m * SA * 8;
+    size_t a = (size_t)(m * (m + 1) / 2) * 8;
     size_t w = (size_t)(2 * k - 1) * m * 4 * 8;
-    size_t best = 4 * 32 * (8 + 4 + 4);
-    size_t misc = 17 * 4 + 32;
+    size_t best = 4 * 32 * (8 + 4);
+    size_t misc = 17 * 4 + 16 + 32;
     size_t tot = a + w + best + misc;
     return (tot + 15) & ~(size_t)15;
 }
+__host__ __device__ inline size_t cta_smem_extra(int world1) { return world1 ? 0 : 32 * (8 + 4 + 4); }
 
 size_t traverse_smem_per_warp(int m, int k) { return warp_smem_bytes(m, k); }
 
-__device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((r * NCS + slot) << 2) + w; }
+struct ShardTabs {
+    const long long* cb;
+    const int* sh;
+    const uint32_t* pl;
+};
 
-// One family: index (rank-local), BIC, the two 8 B stores, running best.
-__device__ __forceinline__ void harvest(const TravParams& P, int v, uint32_t S, int size, double rss,
-                                        int w, const WarpSmem& ws)
+// One family (a8-a11): table index (rank-local), BIC, the two 8 B stores,
+// running best of worker w for child v.
+template <bool WORLD1>
+__device__ __forceinline__ void harvest(const TravParams& P, const ShardTabs& st, int v, uint32_t S, double Kw,
+                                        double rss, int w, const WarpSmem& ws)
 {
-    uint32_t lo = S & ((1u << v) - 1u);
-    uint32_t hi = S >> (v + 1);
-    uint32_t cpr = lo | (hi << v);
-    int sh = P.sh[v];
-    long long idx = P.child_base[v] + (long long)(cpr & ((1u << sh) - 1u)) +
-                    (((cpr >> sh) != P.pat_lo[v]) ? (1LL << sh) : 0LL);
-    double bic = (rss <= 1e-300) ? __longlong_as_double(0x7ff0000000000000LL)
-                                 : fma(P.mhalf_n, log(rss), P.Kc[size]);
-    if (P.out_rss) P.out_rss[idx] = rss;
-    if (P.out_bic) P.out_bic[idx] = bic;
-    int bi = (w << 5) + v;
-    double cur = ws.bb[bi];
+    const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
+    long long idx;
+    if (WORLD1) {
+        idx = ((long long)v << (P.m - 1)) + cpr;
+    } else {
+        const int sh = st.sh[v];
+        idx = st.cb[v] + (long long)(cpr & ((1u << sh) - 1u)) + (((cpr >> sh) != st.pl[v]) ? (1LL << sh) : 0LL);
+    }
+    const double bic = (rss > 1e-300) ? fma(P.mhalf_n, fast_ln(rss, P.lntab), Kw)
+                                      : __longlong_as_double(0x7ff0000000000000LL);
+    if (P.out_rss) __stcs(P.out_rss + idx, rss);
+    if (P.out_bic) __stcs(P.out_bic + idx, bic);
+    const int bi = (w << 5) + v;
+    const double cur = ws.bb[bi];
     if (bic >= cur) {
-        uint32_t cs = ws.bs[bi], cm = ws.bm[bi];
-        if (bic > cur || (uint32_t)size < cs || ((uint32_t)size == cs && S < cm)) {
-            ws.bb[bi] = bic; ws.bs[bi] = (uint32_t)size; ws.bm[bi] = S;
+        const uint32_t cm = ws.bm[bi];
+        const int cs = __popc(cm), s = __popc(S);
+        if (bic > cur || s < cs || (s == cs && S < cm)) {
+            ws.bb[bi] = bic;
+            ws.bm[bi] = S;
         }
     }
 }
@@ -334,29 +400,29 @@ __device__ __forceinline__ int slot_pos(int slot, int w, int k, int p, int nw)
 // Snapshot: convert the sub-triangle of A starting at physical origin `org` into
 // worker w's walk state (free rows of R, suffix sums U) and harvest the seed
 // prefixes of sizes d..d+k (reading G11).  Lanes = walk slots.
-__device__ void snapshot(const TravParams& P, const WarpSmem& ws, int org, int w, uint32_t Fmask, int d,
-                         int lane, int NCS, int ncsp)
+template <bool WORLD1>
+__device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSmem& ws, int s, int org, int w,
+                         uint32_t Fmask, int d, int lane, int NCS, int ncsp)
 {
     const int k = P.k;
     if (w >= P.nw) return;
-    int slot = lane;
+    const int slot = lane;
     if (slot < ncsp) {
-        int pos = slot_pos(slot, w, k, P.p, P.nw);
+        const int pos = slot_pos(slot, w, k, P.p, P.nw);
         if (pos < 0) {
             for (int r = 0; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
             for (int u = 2; u <= k; ++u) ws.W[Ridx(k + u - 2, slot, w, NCS)] = 0.0;
         } else {
-            int v = ws.slotvar[slot];
+            const int v = ws.slotvar[slot];
             double acc = 0.0;
-            const int SA = P.SA;
             for (int r = pos; r >= 0; --r) {
-                double x = ws.A[(org + r) * SA + org + pos];
+                double x = ws.A[poff(org + r, s) + pos - r];
                 acc = fma(x, x, acc);
                 if (r < k) ws.W[Ridx(r, slot, w, NCS)] = x;
                 if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
                 if (r <= k) {
                     uint32_t S = Fmask | (((1u << r) - 1u) << P.p);
-                    harvest(P, v, S, d + r, acc, w, ws);
+                    harvest<WORLD1>(P, st, v, S, P.Kc[d + r], acc, w, ws);
                 }
             }
             for (int r = pos + 1; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
@@ -366,33 +432,52 @@ __device__ void snapshot(const TravParams& P, const WarpSmem& ws, int org, int w
     __syncwarp();
 }
 
+template <bool WORLD1>
 __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ TravParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int m = P.m, k = P.k, p = P.p, bh = P.bh, NCS = P.NCS, SA = P.SA;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh, NCS = P.NCS;
+    ShardTabs st{};
+    unsigned char* wbase = smem_raw;
+    if (!WORLD1) {
+        long long* cb = (long long*)smem_raw;
+        int* sh = (int*)(cb + 32);
+        uint32_t* pl = (uint32_t*)(sh + 32);
+        for (int v = threadIdx.x; v < 32; v += blockDim.x) {
+            cb[v] = P.child_base[v]; sh[v] = P.sh[v]; pl[v] = P.pat_lo[v];
+        }
+        st.cb = cb; st.sh = sh; st.pl = pl;
+        wbase += cta_smem_extra(0);
+        __syncthreads();
+    }
     const size_t per = warp_smem_bytes(m, k);
-    unsigned char* base = smem_raw + (size_t)wib * per;
+    unsigned char* base = wbase + (size_t)wib * per;
     WarpSmem ws;
     ws.A = (double*)base;
-    ws.W = ws.A + (size_t)m * SA;
+    ws.W = ws.A + (m * (m + 1) / 2);
     ws.bb = ws.W + (size_t)(2 * k - 1) * NCS * 4;
     ws.bm = (uint32_t*)(ws.bb + 4 * 32);
-    ws.bs = ws.bm + 4 * 32;
-    ws.pm = ws.bs + 4 * 32;
-    ws.slotvar = (uint8_t*)(ws.pm + 17);
+    ws.pm = ws.bm + 4 * 32;
+    ws.posmap = (uint8_t*)(ws.pm + 17);
+    ws.slotvar = ws.posmap + 16;
 
     for (int e = lane; e < 4 * 32; e += 32) {
         ws.bb[e] = -__longlong_as_double(0x7ff0000000000000LL);
         ws.bm[e] = 0xffffffffu;
-        ws.bs[e] = 0xffffffffu;
     }
     for (int e = lane; e < (2 * k - 1) * NCS * 4; e += 32) ws.W[e] = 0.0;
     __syncwarp();
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
     const int w = lane & 3;           // worker of this lane within the pack
     const int cl = lane >> 2;         // lane's column group (0..7)
-    const int NB = NCS - k;           // back slots (pack vars + hi vars in B)
+    const int RS = NCS << 2;          // W row stride (doubles)
+    // slots of pack variables in a worker's front set are never harvested
+    uint32_t absent = 0;
+    if (w >= P.nw) absent = 0xffffffffu;
+    else
+        for (int j = 0; j < p; ++j)
+            if ((w >> j) & 1) absent |= 1u << (k + j);
 
     for (;;) {
         uint32_t item = 0;
@@ -405,18 +490,16 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
         const int sn = m - __popc(nid);
         const double* src = P.nodes + (size_t)nid * m * m;
-        for (int e = lane; e < sn * sn; e += 32) {
-            int r = e / sn, c = e % sn;
-            ws.A[r * SA + c] = src[r * m + c];
-        }
+        for (int r = 0; r < sn; ++r)
+            for (int c = r + lane; c < sn; c += 32) ws.A[poff(r, sn) + c - r] = src[r * m + c];
         __syncwarp();
         int org = 0;
         for (int l = P.L1; l < bh; ++l) {
             if ((pack >> l) & 1u) {
                 ++org;
             } else {
-                int T = (bh - l - 1) + p + k;
-                for (int j = 0; j < T; ++j) grc_square(ws.A, SA, org + j, sn, lane);
+                const int T = (bh - l - 1) + p + k;
+                for (int j = 0; j < T; ++j) grc_packed(ws.A, sn, org + j, sn, lane);
             }
         }
         // slot -> user id: free, pack, then hi vars in B (ascending id = latest deferred first)
@@ -429,99 +512,93 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             else if (lane < k + p) v = lane - k;
             else {
                 int q = lane - k - p, cnt = 0;
-                v = -1;
+                v = 0;
                 for (int id = p + k; id < m; ++id)
                     if (!((Fhi >> id) & 1u)) { if (cnt == q) { v = id; break; } ++cnt; }
-                if (v < 0) v = 0;
             }
             ws.slotvar[lane] = (uint8_t)v;
         }
+        if (lane < 16) ws.posmap[lane] = (uint8_t)lane;
+        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << p) : 0u;
         const int dh = __popc(pack);
-        const int nbhi = bh - dh;
-        const int NCSp = k + p + nbhi;        // slots in use for this pack
+        const int NCSp = k + p + (bh - dh);   // slots in use for this pack
         __syncwarp();
 
-        // ---- pack derivation: the 2^p workers' seeds by one GRC path (a5)
-        const int o = org;
-        const int end = sn;
+        // ---- pack derivation: the 2^p workers' seeds along one GRC path (a5)
+        const int o = org, s = sn, end = sn;
         if (p == 2) {
-            snapshot(P, ws, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
-            for (int j = 1; j <= k; ++j) grc_square(ws.A, SA, o + j, end, lane);
-            snapshot(P, ws, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
-            for (int j = 0; j < k; ++j) grc_square(ws.A, SA, o + j, end, lane);
-            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
-            for (int j = k; j >= 0; --j) grc_square(ws.A, SA, o + j, end, lane);
-            snapshot(P, ws, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
+            snapshot<WORLD1>(P, st, ws, s, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
+            for (int j = 1; j <= k; ++j) grc_packed(ws.A, s, o + j, end, lane);
+            snapshot<WORLD1>(P, st, ws, s, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_packed(ws.A, s, o + j, end, lane);
+            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
+            for (int j = k; j >= 0; --j) grc_packed(ws.A, s, o + j, end, lane);
+            snapshot<WORLD1>(P, st, ws, s, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
         } else if (p == 1) {
-            snapshot(P, ws, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
-            for (int j = 0; j < k; ++j) grc_square(ws.A, SA, o + j, end, lane);
-            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1>(P, st, ws, s, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_packed(ws.A, s, o + j, end, lane);
+            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
         } else {
-            snapshot(P, ws, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
         }
-        // slots beyond this pack's back set are never in the walk list
-        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << p) : 0u;
-        __syncwarp();
 
         // ---- the walk: d + Upsilon(k) in lockstep (a6-a11)
-        uint64_t perm = 0;
-        for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
         const uint32_t Fw = Fhi | (uint32_t)w;          // pack var j = user id j
         const int dw = dh + __popc((uint32_t)w);
-        const bool wvalid = w < P.nw;
         const int NBp = NCSp - k;
+        double* const Ww = ws.W + w;
         for (int t = 0; t < P.sched_len; ++t) {
             const int i = (int)__ldg(P.sched + t) - 1;
-            const int X = (int)((perm >> (4 * i)) & 15u);
-            const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
-            double c, s, h;
-            {
-                double a = ws.W[Ridx(i, Y, w, NCS)];
-                double b = ws.W[Ridx(i + 1, Y, w, NCS)];
-                givens(a, b, c, s, h);
-            }
+            const int X = ws.posmap[i];
+            const int Y = ws.posmap[i + 1];
+            double* const R0 = Ww + i * RS;            // row i
+            double* const R1 = R0 + RS;                // row i+1
+            double* const U2 = Ww + (k + i) * RS;      // U row i+2
+            double* const U1 = U2 - RS;                // U row i+1 (valid when i >= 1)
+            double c, sn, h;
+            givens(R0[Y << 2], R1[Y << 2], c, sn, h);
             const uint32_t T = ws.pm[i] | (1u << (p + Y));
+            const double Kw = P.Kc[dw + i + 1];
             __syncwarp();
             const uint32_t S = Fw | T;
-            const int size = dw + i + 1;
             const int nf = k - 1 - i;
             const int L = nf + NBp;
             for (int e = cl; e < L; e += 8) {
-                int slot = (e == 0) ? X : (e < nf ? (int)((perm >> (4 * (i + 1 + e))) & 15u) : k + (e - nf));
-                int r0 = Ridx(i, slot, w, NCS), r1 = Ridx(i + 1, slot, w, NCS);
-                double x = ws.W[r0], y = ws.W[r1];
-                double u2 = ws.W[Ridx(k + i, slot, w, NCS)];        // U[i+2]
-                double xn = fma(c, x, s * y);
-                double yn = fma(c, y, -s * x);
-                ws.W[r0] = xn;
-                ws.W[r1] = yn;
-                double rss = fma(yn, yn, u2);
-                if (i >= 1) ws.W[Ridx(k + i - 1, slot, w, NCS)] = rss;   // U[i+1]
-                bool present = wvalid && (slot < k || slot >= k + p || !((w >> (slot - k)) & 1));
-                if (present) harvest(P, ws.slotvar[slot], S, size, rss, w, ws);
+                const int slot = (e == 0) ? X : (e < nf ? (int)ws.posmap[i + 1 + e] : k + (e - nf));
+                const int so = slot << 2;
+                const double x = R0[so], y = R1[so], u2 = U2[so];
+                const double xn = fma(c, x, sn * y);
+                const double yn = fma(c, y, -sn * x);
+                R0[so] = xn;
+                R1[so] = yn;
+                const double rss = fma(yn, yn, u2);
+                if (i >= 1) U1[so] = rss;
+                if (!((absent >> slot) & 1u)) harvest<WORLD1>(P, st, ws.slotvar[slot], S, Kw, rss, w, ws);
             }
             if (cl == 0) {
-                ws.W[Ridx(i, Y, w, NCS)] = h;
-                ws.W[Ridx(i + 1, Y, w, NCS)] = 0.0;
-                if (i >= 1) ws.W[Ridx(k + i - 1, Y, w, NCS)] = 0.0;
+                R0[Y << 2] = h;
+                R1[Y << 2] = 0.0;
+                if (i >= 1) U1[Y << 2] = 0.0;
             }
-            {
-                uint64_t d = ((perm >> (4 * i)) ^ (perm >> (4 * (i + 1)))) & 15u;
-                perm ^= (d << (4 * i)) | (d << (4 * (i + 1)));
+            if (lane == 0) {
+                ws.posmap[i] = (uint8_t)Y;
+                ws.posmap[i + 1] = (uint8_t)X;
+                ws.pm[i + 1] = T;
             }
-            if (lane == 0) ws.pm[i + 1] = T;
             __syncwarp();
         }
-        (void)NB;
     }
     // ---- per-warp best over its 4 workers -> global partials (a11)
     __syncwarp();
     if (lane < m) {
         double bb = -__longlong_as_double(0x7ff0000000000000LL);
-        uint32_t bm = 0xffffffffu, bs = 0xffffffffu;
+        uint32_t bm = 0xffffffffu;
+        int bs = 1 << 30;
         for (int ww = 0; ww < 4; ++ww) {
             double b = ws.bb[(ww << 5) + lane];
-            uint32_t s2 = ws.bs[(ww << 5) + lane], m2 = ws.bm[(ww << 5) + lane];
+            uint32_t m2 = ws.bm[(ww << 5) + lane];
+            if (m2 == 0xffffffffu) continue;
+            int s2 = __popc(m2);
             if (b > bb || (b == bb && (s2 < bs || (s2 == bs && m2 < bm)))) { bb = b; bs = s2; bm = m2; }
         }
         P.part_bic[(size_t)gwarp * m + lane] = bb;
@@ -529,24 +606,59 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
     }
 }
 
-// ---------------------------------------------------------------- a11 best reduce
-__global__ void best_reduce_kernel(const double* __restrict__ part_bic, const uint32_t* __restrict__ part_mask,
-                                   int nparts, int m, double* best_bic, uint32_t* best_mask)
+__global__ void debug_ln_kernel(const double* x, double* y, int64_t n, const double2* tab)
 {
-    int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= m) return;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = fast_ln(x[i], tab);
+}
+
+cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2* tab, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    debug_ln_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, y, n, tab);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- a11 best reduce
+// One CTA per child: strided scan over the per-warp partials, then a fixed
+// tree reduction -> deterministic.
+__device__ __forceinline__ bool better(double b1, uint32_t m1, double b2, uint32_t m2)
+{
+    if (m1 == 0xffffffffu) return false;
+    if (m2 == 0xffffffffu) return true;
+    if (b1 != b2) return b1 > b2;
+    int s1 = __popc(m1), s2 = __popc(m2);
+    return s1 != s2 ? s1 < s2 : m1 < m2;
+}
+
+__global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restrict__ part_bic,
+                                                          const uint32_t* __restrict__ part_mask, int nparts, int m,
+                                                          double* best_bic, uint32_t* best_mask)
+{
+    __shared__ double sb[256];
+    __shared__ uint32_t sm[256];
+    const int v = blockIdx.x;
     double bb = -__longlong_as_double(0x7ff0000000000000LL);
     uint32_t bm = 0xffffffffu;
-    int bs = 1 << 30;
-    for (int q = 0; q < nparts; ++q) {
+    for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
         double b = part_bic[(size_t)q * m + v];
         uint32_t mk = part_mask[(size_t)q * m + v];
-        int s = __popc(mk);
-        if (mk == 0xffffffffu) continue;
-        if (b > bb || (b == bb && (s < bs || (s == bs && mk < bm)))) { bb = b; bm = mk; bs = s; }
+        if (better(b, mk, bb, bm)) { bb = b; bm = mk; }
     }
-    best_bic[v] = bb;
-    best_mask[v] = bm;
+    sb[threadIdx.x] = bb;
+    sm[threadIdx.x] = bm;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o && better(sb[threadIdx.x + o], sm[threadIdx.x + o], sb[threadIdx.x], sm[threadIdx.x])) {
+            sb[threadIdx.x] = sb[threadIdx.x + o];
+            sm[threadIdx.x] = sm[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        best_bic[v] = sb[0];
+        best_mask[v] = sm[0];
+    }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -582,29 +694,42 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
     return cudaGetLastError();
 }
 
+static size_t traverse_smem(int m, int k, int wpc, int world1)
+{
+    return warp_smem_bytes(m, k) * wpc + cta_smem_extra(world1);
+}
+
 int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta)
 {
-    size_t smem = warp_smem_bytes(m, k) * warps_per_cta;
-    cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t smem = traverse_smem(m, k, warps_per_cta, 1);
+    cudaFuncSetAttribute(traverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, traverse_kernel, warps_per_cta * 32, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, traverse_kernel<true>, warps_per_cta * 32, smem) !=
+        cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
 
 cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st)
 {
-    size_t smem = warp_smem_bytes(P.m, P.k) * warps_per_cta;
-    cudaError_t e = cudaFuncSetAttribute(traverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    traverse_kernel<<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
+    const bool w1 = P.world1 != 0;
+    size_t smem = traverse_smem(P.m, P.k, warps_per_cta, w1);
+    if (w1) {
+        cudaError_t e = cudaFuncSetAttribute(traverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        traverse_kernel<true><<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
+    } else {
+        cudaError_t e = cudaFuncSetAttribute(traverse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        traverse_kernel<false><<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st)
 {
-    best_reduce_kernel<<<1, 32, 0, st>>>(part_bic, part_mask, nparts, m, best_bic, best_mask);
+    best_reduce_kernel<<<m, 256, 0, st>>>(part_bic, part_mask, nparts, m, best_bic, best_mask);
     return cudaGetLastError();
 }
 

@@ -12,7 +12,7 @@ struct TravParams {
     int m, k, p, bh, L1, nw, NCS, SA;
     int sched_len;
     int npacks;
-    int n_int;                  // unused padding / reserved
+    int world1;                 // 1: single rank, identity table layout
     const int8_t* sched;        // Upsilon(k), 1-based swap positions
     const double* nodes;        // seed-tree nodes at depth L1, m*m doubles each
     const uint32_t* packs;      // this rank's pack ids (costliest first)
@@ -22,6 +22,7 @@ struct TravParams {
     double* part_bic;           // [grid warps][m] per-warp best BIC
     uint32_t* part_mask;        // [grid warps][m] per-warp best mask
     double mhalf_n;             // -n/2
+    const double2* lntab;       // fast-log table (128 x (r_j, -ln r_j))
     double Kc[33];              // BIC constant per parent-set size
     long long child_base[32];   // rank-local layout (plan.h)
     int sh[32];
@@ -41,5 +42,7 @@ cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_ct
 int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st);
+
+cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2* tab, cudaStream_t st);
 
 }  // namespace bnr

@@ -210,3 +210,22 @@ def test_logical_ranks_union(world):
     assert (seen == 1).all()
     mm, mb = bn.bnreg_best_merge(m, np.array(masks), np.array(bics))
     assert np.array_equal(mm, fbm)
+
+
+def test_fast_ln_accuracy():
+    """The BIC epilogue's table+polynomial log against numpy's log (libm) over
+    the whole normal range used by RSS values: |err| <= 4e-15 * max(1, |ln x|)."""
+    import torch
+    bn = _bn()
+    rng = np.random.default_rng(0)
+    x = np.concatenate([10.0 ** rng.uniform(-299, 300, 200000), rng.uniform(0.5, 2.0, 100000),
+                        np.nextafter(1.0, 2.0) ** np.arange(1, 1000), [1.0, 2.0, 0.5, 1e-300 * 1.0001]])
+    h = bn.Bnreg(10, 3)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    h.debug_ln(xd, yd, len(x))
+    y = yd.cpu().numpy()
+    ref = np.log(x)
+    err = np.abs(y - ref) / np.maximum(1.0, np.abs(ref))
+    assert err.max() <= 4e-15, err.max()
+    h.close()
