@@ -42,13 +42,19 @@ __device__ __forceinline__ double warp_sum(double v)
 // happen on rank-deficient data (rejected at create); identity then.
 __device__ __forceinline__ void givens(double a, double b, double& c, double& s, double& h)
 {
-    double h2 = fma(a, a, b * b);
-    if (h2 > 0.0) {
-        double rh = rsqrt(h2);
-        c = a * rh; s = b * rh; h = h2 * rh;
-    } else {
-        c = 1.0; s = 0.0; h = 0.0;
-    }
+    const double h2 = fma(a, a, b * b);
+    // 1/sqrt(h2): hardware approximation + two Newton steps (no special-case
+    // branches: h2 is a positive normal number unless the data is rank deficient)
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+    double e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    const bool ok = h2 > 0.0;
+    c = ok ? a * y : 1.0;
+    s = ok ? b * y : 0.0;
+    h = ok ? h2 * y : 0.0;
 }
 
 // ---------------------------------------------------------------- a1 centre
@@ -279,15 +285,18 @@ __device__ __forceinline__ double fast_ln(double x, const double2* __restrict__ 
     const int e = (hi >> 20) - 1023;
     const int j = (hi >> 13) & 127;
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 t = __ldg(tab + j);
-    const double u = fma(f, t.x, -1.0);
-    double q = fma(u, -1.0 / 6.0, 0.2);
-    q = fma(u, q, -0.25);
-    q = fma(u, q, 1.0 / 3.0);
-    q = fma(u, q, -0.5);
-    q = fma(u, q, 1.0);
+    const double2 t = tab[j];
     const double ed = (double)e;
-    return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, fma(u, q, t.y)));
+    // base = e ln2 + (-ln r_j), independent of the polynomial (ILP)
+    const double base = fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, t.y));
+    const double u = fma(f, t.x, -1.0);
+    // log1p(u) = u q(u), q = 1 - u/2 + u^2/3 - u^3/4 + u^4/5 - u^5/6 (Estrin)
+    const double u2 = u * u;
+    const double a = fma(u, -0.5, 1.0);
+    const double b = fma(u, -0.25, 1.0 / 3.0);
+    const double c = fma(u, -1.0 / 6.0, 0.2);
+    const double q = fma(u2, fma(u2, c, b), a);
+    return fma(u, q, base);
 }
 
 __device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((r * NCS + slot) << 2) + w; }
@@ -326,8 +335,8 @@ __device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int
 struct WarpSmem {
     double* A;        // packed triangle, side <= m (seed derivation)
     double* W;        // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k)
-    double* bb;       // [4][32] best BIC
-    uint32_t* bm;     // [4][32] best mask
+    double* bb;       // [32] best BIC over the warp's workers, per child
+    uint32_t* bm;     // [32] its parent mask
     uint32_t* pm;     // [17] free-prefix masks (user ids) by prefix length
     uint8_t* posmap;  // [16] free position -> free slot
     uint8_t* slotvar; // [32] slot -> user id
@@ -337,16 +346,17 @@ __host__ __device__ inline size_t warp_smem_bytes(int m, int k)
 {
     size_t a = (size_t)(m * (m + 1) / 2) * 8;
     size_t w = (size_t)(2 * k - 1) * m * 4 * 8;
-    size_t best = 4 * 32 * (8 + 4);
+    size_t best = 32 * (8 + 4);
     size_t misc = 17 * 4 + 16 + 32;
     size_t tot = a + w + best + misc;
     return (tot + 15) & ~(size_t)15;
 }
-__host__ __device__ inline size_t cta_smem_extra(int world1) { return world1 ? 0 : 32 * (8 + 4 + 4); }
+__host__ __device__ inline size_t cta_smem_extra(int world1) { return 128 * 16 + (world1 ? 0 : 32 * (8 + 4 + 4)); }
 
 size_t traverse_smem_per_warp(int m, int k) { return warp_smem_bytes(m, k); }
 
 struct ShardTabs {
+    const double2* lntab;   // fast-log table (shared memory)
     const long long* cb;
     const int* sh;
     const uint32_t* pl;
@@ -356,7 +366,7 @@ struct ShardTabs {
 // running best of worker w for child v.
 template <bool WORLD1>
 __device__ __forceinline__ void harvest(const TravParams& P, const ShardTabs& st, int v, uint32_t S, double Kw,
-                                        double rss, int w, const WarpSmem& ws)
+                                        double rss, const WarpSmem& ws)
 {
     const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
     long long idx;
@@ -366,18 +376,18 @@ __device__ __forceinline__ void harvest(const TravParams& P, const ShardTabs& st
         const int sh = st.sh[v];
         idx = st.cb[v] + (long long)(cpr & ((1u << sh) - 1u)) + (((cpr >> sh) != st.pl[v]) ? (1LL << sh) : 0LL);
     }
-    const double bic = (rss > 1e-300) ? fma(P.mhalf_n, fast_ln(rss, P.lntab), Kw)
+    const double bic = (rss > 1e-300) ? fma(P.mhalf_n, fast_ln(rss, st.lntab), Kw)
                                       : __longlong_as_double(0x7ff0000000000000LL);
     if (P.out_rss) __stcs(P.out_rss + idx, rss);
     if (P.out_bic) __stcs(P.out_bic + idx, bic);
-    const int bi = (w << 5) + v;
-    const double cur = ws.bb[bi];
+    // the caller guarantees that no other lane updates child v concurrently
+    const double cur = ws.bb[v];
     if (bic >= cur) {
-        const uint32_t cm = ws.bm[bi];
-        const int cs = __popc(cm), s = __popc(S);
-        if (bic > cur || s < cs || (s == cs && S < cm)) {
-            ws.bb[bi] = bic;
-            ws.bm[bi] = S;
+        const uint32_t cm = ws.bm[v];
+        const int cs = __popc(cm), sz = __popc(S);
+        if (bic > cur || sz < cs || (sz == cs && S < cm)) {
+            ws.bb[v] = bic;
+            ws.bm[v] = S;
         }
     }
 }
@@ -422,7 +432,7 @@ __device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSme
                 if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
                 if (r <= k) {
                     uint32_t S = Fmask | (((1u << r) - 1u) << P.p);
-                    harvest<WORLD1>(P, st, v, S, P.Kc[d + r], acc, w, ws);
+                    harvest<WORLD1>(P, st, v, S, P.Kc[d + r], acc, ws);
                 }
             }
             for (int r = pos + 1; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
@@ -432,6 +442,101 @@ __device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSme
     __syncwarp();
 }
 
+struct StepCtx {
+    double* R0;       // this worker's row i     (interleaved: slot s at [s << 2])
+    double* R1;       // row i+1
+    double* U2;       // suffix-sum row i+2
+    double* U1;       // suffix-sum row i+1 (written when i >= 1)
+    double c, sn;     // the GRC's rotation
+    uint32_t S;       // the new prefix set (user ids) for this worker
+    double Kw;        // BIC constant for |S|
+    int X, i, nf, L, cl, w;
+    uint32_t absent;  // slots whose variable is in this worker's front set
+};
+
+// One GRC step over NCH chunks of 8 list entries per worker, written so that
+// the NCH families a lane owns run as independent dependency chains (ILP):
+// gather -> rotate + suffix sums -> index + log + BIC -> stores + best.
+template <bool WORLD1, int NCH>
+__device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs& st, const WarpSmem& ws,
+                                            const StepCtx& s)
+{
+    int slot[NCH];
+    bool act[NCH];
+    double x[NCH], y[NCH], u2[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        const int e = s.cl + 8 * q;
+        act[q] = e < s.L;
+        int sl = (e == 0) ? s.X : (e < s.nf ? (int)ws.posmap[s.i + 1 + e] : P.k + (e - s.nf));
+        slot[q] = act[q] ? sl : s.X;
+        const int so = slot[q] << 2;
+        x[q] = s.R0[so];
+        y[q] = s.R1[so];
+        u2[q] = s.U2[so];
+    }
+    double rss[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        const double xn = fma(s.c, x[q], s.sn * y[q]);
+        const double yn = fma(s.c, y[q], -s.sn * x[q]);
+        rss[q] = fma(yn, yn, u2[q]);
+        if (act[q]) {
+            const int so = slot[q] << 2;
+            s.R0[so] = xn;
+            s.R1[so] = yn;
+            if (s.i >= 1) s.U1[so] = rss[q];
+        }
+    }
+    bool hv[NCH];
+    int vv[NCH];
+    long long idx[NCH];
+    double bic[NCH], cur[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        hv[q] = act[q] && !((s.absent >> slot[q]) & 1u);
+        const int v = ws.slotvar[slot[q]];
+        vv[q] = v;
+        const uint32_t S = s.S;
+        const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
+        if (WORLD1) {
+            idx[q] = ((long long)v << (P.m - 1)) + cpr;
+        } else {
+            const int sh = st.sh[v];
+            idx[q] = st.cb[v] + (long long)(cpr & ((1u << sh) - 1u)) +
+                     (((cpr >> sh) != st.pl[v]) ? (1LL << sh) : 0LL);
+        }
+        bic[q] = (rss[q] > 1e-300) ? fma(P.mhalf_n, fast_ln(rss[q], st.lntab), s.Kw)
+                                   : __longlong_as_double(0x7ff0000000000000LL);
+        cur[q] = ws.bb[v];
+    }
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        if (hv[q]) {
+            if (P.out_rss) __stcs(P.out_rss + idx[q], rss[q]);
+            if (P.out_bic) __stcs(P.out_bic + idx[q], bic[q]);
+        }
+        // running best (a11): the 4 lanes of a column group share child vv[q];
+        // improvements are rare, so resolve them lane by lane (ascending lane id)
+        unsigned bal = __ballot_sync(FULLMASK, hv[q] && bic[q] >= cur[q]);
+        while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            if ((int)(threadIdx.x & 31) == l) {
+                const int v = vv[q];
+                const double cb = ws.bb[v];
+                const uint32_t cm = ws.bm[v];
+                const int cs = __popc(cm), sz = __popc(s.S);
+                if (bic[q] > cb || (bic[q] == cb && (sz < cs || (sz == cs && s.S < cm)))) {
+                    ws.bb[v] = bic[q];
+                    ws.bm[v] = s.S;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 template <bool WORLD1>
 __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ TravParams P)
 {
@@ -439,33 +544,36 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int m = P.m, k = P.k, p = P.p, bh = P.bh, NCS = P.NCS;
     ShardTabs st{};
-    unsigned char* wbase = smem_raw;
+    {
+        double2* lt = (double2*)smem_raw;
+        for (int j = threadIdx.x; j < 128; j += blockDim.x) lt[j] = P.lntab[j];
+        st.lntab = lt;
+    }
+    unsigned char* wbase = smem_raw + 128 * 16;
     if (!WORLD1) {
-        long long* cb = (long long*)smem_raw;
+        long long* cb = (long long*)wbase;
         int* sh = (int*)(cb + 32);
         uint32_t* pl = (uint32_t*)(sh + 32);
         for (int v = threadIdx.x; v < 32; v += blockDim.x) {
             cb[v] = P.child_base[v]; sh[v] = P.sh[v]; pl[v] = P.pat_lo[v];
         }
         st.cb = cb; st.sh = sh; st.pl = pl;
-        wbase += cta_smem_extra(0);
-        __syncthreads();
+        wbase += 32 * (8 + 4 + 4);
     }
+    __syncthreads();
     const size_t per = warp_smem_bytes(m, k);
     unsigned char* base = wbase + (size_t)wib * per;
     WarpSmem ws;
     ws.A = (double*)base;
     ws.W = ws.A + (m * (m + 1) / 2);
     ws.bb = ws.W + (size_t)(2 * k - 1) * NCS * 4;
-    ws.bm = (uint32_t*)(ws.bb + 4 * 32);
-    ws.pm = ws.bm + 4 * 32;
+    ws.bm = (uint32_t*)(ws.bb + 32);
+    ws.pm = ws.bm + 32;
     ws.posmap = (uint8_t*)(ws.pm + 17);
     ws.slotvar = ws.posmap + 16;
 
-    for (int e = lane; e < 4 * 32; e += 32) {
-        ws.bb[e] = -__longlong_as_double(0x7ff0000000000000LL);
-        ws.bm[e] = 0xffffffffu;
-    }
+    ws.bb[lane] = -__longlong_as_double(0x7ff0000000000000LL);
+    ws.bm[lane] = 0xffffffffu;
     for (int e = lane; e < (2 * k - 1) * NCS * 4; e += 32) ws.W[e] = 0.0;
     __syncwarp();
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -547,10 +655,18 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
         const int dw = dh + __popc((uint32_t)w);
         const int NBp = NCSp - k;
         double* const Ww = ws.W + w;
+        uint64_t perm = 0;                                   // free position -> slot (nibbles)
+        for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
+        int inext = (int)__ldg(P.sched) - 1;
         for (int t = 0; t < P.sched_len; ++t) {
-            const int i = (int)__ldg(P.sched + t) - 1;
-            const int X = ws.posmap[i];
-            const int Y = ws.posmap[i + 1];
+            const int i = inext;
+            if (t + 1 < P.sched_len) inext = (int)__ldg(P.sched + t + 1) - 1;   // prefetch
+            const int X = (int)((perm >> (4 * i)) & 15u);
+            const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
+            {
+                const uint64_t d = (uint64_t)(X ^ Y);
+                perm ^= (d << (4 * i)) | (d << (4 * (i + 1)));
+            }
             double* const R0 = Ww + i * RS;            // row i
             double* const R1 = R0 + RS;                // row i+1
             double* const U2 = Ww + (k + i) * RS;      // U row i+2
@@ -563,17 +679,13 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             const uint32_t S = Fw | T;
             const int nf = k - 1 - i;
             const int L = nf + NBp;
-            for (int e = cl; e < L; e += 8) {
-                const int slot = (e == 0) ? X : (e < nf ? (int)ws.posmap[i + 1 + e] : k + (e - nf));
-                const int so = slot << 2;
-                const double x = R0[so], y = R1[so], u2 = U2[so];
-                const double xn = fma(c, x, sn * y);
-                const double yn = fma(c, y, -sn * x);
-                R0[so] = xn;
-                R1[so] = yn;
-                const double rss = fma(yn, yn, u2);
-                if (i >= 1) U1[so] = rss;
-                if (!((absent >> slot) & 1u)) harvest<WORLD1>(P, st, ws.slotvar[slot], S, Kw, rss, w, ws);
+            const int nch = (L + 7) >> 3;
+            StepCtx sc{R0, R1, U2, U1, c, sn, S, Kw, X, i, nf, L, cl, w, absent};
+            switch (nch) {
+                case 1: walk_chunks<WORLD1, 1>(P, st, ws, sc); break;
+                case 2: walk_chunks<WORLD1, 2>(P, st, ws, sc); break;
+                case 3: walk_chunks<WORLD1, 3>(P, st, ws, sc); break;
+                default: walk_chunks<WORLD1, 4>(P, st, ws, sc); break;
             }
             if (cl == 0) {
                 R0[Y << 2] = h;
@@ -588,21 +700,11 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             __syncwarp();
         }
     }
-    // ---- per-warp best over its 4 workers -> global partials (a11)
+    // ---- per-warp best -> global partials (a11)
     __syncwarp();
     if (lane < m) {
-        double bb = -__longlong_as_double(0x7ff0000000000000LL);
-        uint32_t bm = 0xffffffffu;
-        int bs = 1 << 30;
-        for (int ww = 0; ww < 4; ++ww) {
-            double b = ws.bb[(ww << 5) + lane];
-            uint32_t m2 = ws.bm[(ww << 5) + lane];
-            if (m2 == 0xffffffffu) continue;
-            int s2 = __popc(m2);
-            if (b > bb || (b == bb && (s2 < bs || (s2 == bs && m2 < bm)))) { bb = b; bs = s2; bm = m2; }
-        }
-        P.part_bic[(size_t)gwarp * m + lane] = bb;
-        P.part_mask[(size_t)gwarp * m + lane] = bm;
+        P.part_bic[(size_t)gwarp * m + lane] = ws.bb[lane];
+        P.part_mask[(size_t)gwarp * m + lane] = ws.bm[lane];
     }
 }
 
