@@ -353,6 +353,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p;
     T.NCS = P.m; T.SA = P.m | 1;
     T.sched_len = (int)P.sched.size();
+    if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) T.sched_len = std::min(T.sched_len, atoi(dbg));  // profiling aid
     T.npacks = (int)P.packs.size();
     T.sched = h->d_sched; T.nodes = nodes; T.packs = h->d_packs; T.counter = h->d_counter;
     T.out_rss = out_rss; T.out_bic = out_bic;
@@ -361,12 +362,8 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.lntab = h->d_lntab;
     T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
-    for (int v = 0; v < 32; ++v) {
-        T.child_base[v] = v < P.m ? P.child_base[v] : 0;
-        bool sel = (P.world > 1) && v >= P.m - P.r;
-        T.sh[v] = (P.world == 1) ? P.m - 1 : (sel ? P.m - P.r : P.shard_shift);
-        T.pat_lo[v] = v < P.m ? P.pat_lo[v] : 0;
-    }
+    T.r = P.r;
+    T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
     CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
     CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));

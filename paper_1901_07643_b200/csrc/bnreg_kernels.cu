@@ -273,13 +273,18 @@ __global__ void __launch_bounds__(128) tree_level_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------- a5-a11 traversal
+// Constants of the fast log (constant bank: usable as DFMA operands directly).
+__constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, -1.0 / 6.0, 0.2,
+                               6.93147180369123816490e-01,   // ln2 hi (exact products e * hi for |e| < 2^11)
+                               1.90821492927058770002e-10,   // ln2 lo
+                               0.0};
+
 // Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 7 bits of
 // f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/128) (host,
 // long double); u = f r_j - 1 (|u| <= 3.9e-3);  ln x = e ln2 + (-ln r_j) + log1p(u),
-// log1p by its degree-6 Taylor polynomial (truncation u^7/7 < 2e-18).
-// Absolute error ~1e-15 for the RSS range of the table (|e| < 1024), i.e. a
-// BIC error < 1e-11 at n = 1e4.
-__device__ __forceinline__ double fast_ln(double x, const double2* __restrict__ tab)
+// log1p(u) = u q(u) with q the degree-5 Taylor polynomial (Estrin form;
+// truncation u^7/7 < 2e-18).  Absolute error ~1e-15 for normal x.
+__device__ __forceinline__ double fast_ln(double x, const double2* tab)
 {
     const int hi = __double2hiint(x), lo = __double2loint(x);
     const int e = (hi >> 20) - 1023;
@@ -287,14 +292,12 @@ __device__ __forceinline__ double fast_ln(double x, const double2* __restrict__ 
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double2 t = tab[j];
     const double ed = (double)e;
-    // base = e ln2 + (-ln r_j), independent of the polynomial (ILP)
-    const double base = fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, t.y));
+    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], t.y));
     const double u = fma(f, t.x, -1.0);
-    // log1p(u) = u q(u), q = 1 - u/2 + u^2/3 - u^3/4 + u^4/5 - u^5/6 (Estrin)
     const double u2 = u * u;
-    const double a = fma(u, -0.5, 1.0);
-    const double b = fma(u, -0.25, 1.0 / 3.0);
-    const double c = fma(u, -1.0 / 6.0, 0.2);
+    const double a = fma(u, c_ln[0], 1.0);
+    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double c = fma(u, c_ln[3], c_ln[4]);
     const double q = fma(u2, fma(u2, c, b), a);
     return fma(u, q, base);
 }
@@ -304,7 +307,7 @@ __device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((
 // Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
 __device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
 
-// GRC on the packed triangle (same operation as grc_square).
+// GRC on the packed triangle (the same operation as grc_square).
 __device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int lane)
 {
     const int oJ = poff(J, s), oJ1 = poff(J + 1, s);
@@ -334,7 +337,8 @@ __device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int
 
 struct WarpSmem {
     double* A;        // packed triangle, side <= m (seed derivation)
-    double* W;        // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k)
+    double* W;        // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k);
+                      // slot m is a scratch column for idle lanes
     double* bb;       // [32] best BIC over the warp's workers, per child
     uint32_t* bm;     // [32] its parent mask
     uint32_t* pm;     // [17] free-prefix masks (user ids) by prefix length
@@ -345,50 +349,62 @@ struct WarpSmem {
 __host__ __device__ inline size_t warp_smem_bytes(int m, int k)
 {
     size_t a = (size_t)(m * (m + 1) / 2) * 8;
-    size_t w = (size_t)(2 * k - 1) * m * 4 * 8;
+    size_t w = (size_t)(2 * k - 1) * (m + 1) * 4 * 8;
     size_t best = 32 * (8 + 4);
     size_t misc = 17 * 4 + 16 + 32;
     size_t tot = a + w + best + misc;
     return (tot + 15) & ~(size_t)15;
 }
-__host__ __device__ inline size_t cta_smem_extra(int world1) { return 128 * 16 + (world1 ? 0 : 32 * (8 + 4 + 4)); }
 
 size_t traverse_smem_per_warp(int m, int k) { return warp_smem_bytes(m, k); }
 
-struct ShardTabs {
+struct Ctx {
     const double2* lntab;   // fast-log table (shared memory)
-    const long long* cb;
-    const int* sh;
-    const uint32_t* pl;
+    const double* Kc;       // BIC constants by |S| (shared memory)
 };
 
-// One family (a8-a11): table index (rank-local), BIC, the two 8 B stores,
-// running best of worker w for child v.
+// Rank-local table index of (v, S) (plan.h layout): world 1 = the global
+// index; otherwise child v owns 2^(m-r) entries at v 2^(m-r), holding the
+// compressed masks whose top selector bits match this rank's pattern(s).
 template <bool WORLD1>
-__device__ __forceinline__ void harvest(const TravParams& P, const ShardTabs& st, int v, uint32_t S, double Kw,
-                                        double rss, const WarpSmem& ws)
+__device__ __forceinline__ long long table_index(const TravParams& P, int v, uint32_t S)
 {
     const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
-    long long idx;
-    if (WORLD1) {
-        idx = ((long long)v << (P.m - 1)) + cpr;
-    } else {
-        const int sh = st.sh[v];
-        idx = st.cb[v] + (long long)(cpr & ((1u << sh) - 1u)) + (((cpr >> sh) != st.pl[v]) ? (1LL << sh) : 0LL);
-    }
-    const double bic = (rss > 1e-300) ? fma(P.mhalf_n, fast_ln(rss, st.lntab), Kw)
-                                      : __longlong_as_double(0x7ff0000000000000LL);
-    if (P.out_rss) __stcs(P.out_rss + idx, rss);
-    if (P.out_bic) __stcs(P.out_bic + idx, bic);
-    // the caller guarantees that no other lane updates child v concurrently
+    if (WORLD1) return ((long long)v << (P.m - 1)) + cpr;
+    const bool sel = v >= P.m - P.r;
+    const int sh = sel ? P.m - P.r : P.m - 1 - P.r;
+    const uint32_t low = (cpr & ((1u << sh) - 1u)) + ((!sel && (cpr >> sh) != P.patlo) ? (1u << sh) : 0u);
+    return ((long long)v << (P.m - P.r)) + low;
+}
+
+__device__ __forceinline__ double bic_of(const TravParams& P, const Ctx& cx, double rss, double Kw)
+{
+    const double lnr = fast_ln(fmax(rss, 1e-300), cx.lntab);
+    const double bic = fma(P.mhalf_n, lnr, Kw);
+    return rss > 1e-300 ? bic : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+__device__ __forceinline__ bool tie_better(double b, uint32_t S, double cb, uint32_t cm)
+{
+    if (b != cb) return b > cb;
+    const int s1 = __popc(S), s2 = __popc(cm);
+    return s1 != s2 ? s1 < s2 : S < cm;
+}
+
+// One family outside the lockstep walk (seed prefixes): index, BIC, stores,
+// running best.  The caller guarantees no other lane touches child v meanwhile.
+template <bool WORLD1, bool HR, bool HB>
+__device__ __forceinline__ void harvest(const TravParams& P, const Ctx& cx, int v, uint32_t S, double Kw,
+                                        double rss, const WarpSmem& ws)
+{
+    const long long idx = table_index<WORLD1>(P, v, S);
+    const double bic = bic_of(P, cx, rss, Kw);
+    if (HR) __stcs(P.out_rss + idx, rss);
+    if (HB) __stcs(P.out_bic + idx, bic);
     const double cur = ws.bb[v];
-    if (bic >= cur) {
-        const uint32_t cm = ws.bm[v];
-        const int cs = __popc(cm), sz = __popc(S);
-        if (bic > cur || sz < cs || (sz == cs && S < cm)) {
-            ws.bb[v] = bic;
-            ws.bm[v] = S;
-        }
+    if (bic >= cur && tie_better(bic, S, cur, ws.bm[v])) {
+        ws.bb[v] = bic;
+        ws.bm[v] = S;
     }
 }
 
@@ -410,8 +426,8 @@ __device__ __forceinline__ int slot_pos(int slot, int w, int k, int p, int nw)
 // Snapshot: convert the sub-triangle of A starting at physical origin `org` into
 // worker w's walk state (free rows of R, suffix sums U) and harvest the seed
 // prefixes of sizes d..d+k (reading G11).  Lanes = walk slots.
-template <bool WORLD1>
-__device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSmem& ws, int s, int org, int w,
+template <bool WORLD1, bool HR, bool HB>
+__device__ void snapshot(const TravParams& P, const Ctx& cx, const WarpSmem& ws, int s, int org, int w,
                          uint32_t Fmask, int d, int lane, int NCS, int ncsp)
 {
     const int k = P.k;
@@ -432,7 +448,7 @@ __device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSme
                 if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
                 if (r <= k) {
                     uint32_t S = Fmask | (((1u << r) - 1u) << P.p);
-                    harvest<WORLD1>(P, st, v, S, P.Kc[d + r], acc, ws);
+                    harvest<WORLD1, HR, HB>(P, cx, v, S, cx.Kc[d + r], acc, ws);
                 }
             }
             for (int r = pos + 1; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
@@ -443,24 +459,26 @@ __device__ void snapshot(const TravParams& P, const ShardTabs& st, const WarpSme
 }
 
 struct StepCtx {
-    double* R0;       // this worker's row i     (interleaved: slot s at [s << 2])
-    double* R1;       // row i+1
-    double* U2;       // suffix-sum row i+2
-    double* U1;       // suffix-sum row i+1 (written when i >= 1)
+    int r0;           // W offset of (row i, slot 0, this worker); row stride RS
+    int RS;
     double c, sn;     // the GRC's rotation
     uint32_t S;       // the new prefix set (user ids) for this worker
     double Kw;        // BIC constant for |S|
-    int X, i, nf, L, cl, w;
+    int X, i, nf, L, cl, dummy;
     uint32_t absent;  // slots whose variable is in this worker's front set
 };
 
-// One GRC step over NCH chunks of 8 list entries per worker, written so that
-// the NCH families a lane owns run as independent dependency chains (ILP):
-// gather -> rotate + suffix sums -> index + log + BIC -> stores + best.
-template <bool WORLD1, int NCH>
-__device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs& st, const WarpSmem& ws,
+// One GRC step over NCH chunks of 8 list entries per worker.  The NCH families
+// of a lane are independent dependency chains (ILP): gather -> rotate + suffix
+// sums -> index + log + BIC -> stores + best.  Idle lanes work on the scratch
+// column, so no stores need branches.
+template <bool WORLD1, bool HR, bool HB, int NCH>
+__device__ __forceinline__ void walk_chunks(const TravParams& P, const Ctx& cx, const WarpSmem& ws,
                                             const StepCtx& s)
 {
+    double* const W = ws.W;
+    const int RS = s.RS;
+    const int rU2 = s.r0 + (P.k) * RS;          // U row i+2 lives at W row k+i
     int slot[NCH];
     bool act[NCH];
     double x[NCH], y[NCH], u2[NCH];
@@ -468,12 +486,12 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs
     for (int q = 0; q < NCH; ++q) {
         const int e = s.cl + 8 * q;
         act[q] = e < s.L;
-        int sl = (e == 0) ? s.X : (e < s.nf ? (int)ws.posmap[s.i + 1 + e] : P.k + (e - s.nf));
-        slot[q] = act[q] ? sl : s.X;
+        const int sl = (e == 0) ? s.X : (e < s.nf ? (int)ws.posmap[s.i + 1 + e] : P.k + (e - s.nf));
+        slot[q] = act[q] ? sl : s.dummy;
         const int so = slot[q] << 2;
-        x[q] = s.R0[so];
-        y[q] = s.R1[so];
-        u2[q] = s.U2[so];
+        x[q] = W[s.r0 + so];
+        y[q] = W[s.r0 + RS + so];
+        u2[q] = W[rU2 + so];
     }
     double rss[NCH];
 #pragma unroll
@@ -481,12 +499,10 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs
         const double xn = fma(s.c, x[q], s.sn * y[q]);
         const double yn = fma(s.c, y[q], -s.sn * x[q]);
         rss[q] = fma(yn, yn, u2[q]);
-        if (act[q]) {
-            const int so = slot[q] << 2;
-            s.R0[so] = xn;
-            s.R1[so] = yn;
-            if (s.i >= 1) s.U1[so] = rss[q];
-        }
+        const int so = slot[q] << 2;
+        W[s.r0 + so] = xn;
+        W[s.r0 + RS + so] = yn;
+        if (s.i >= 1) W[rU2 - RS + so] = rss[q];    // U row i+1 (uniform predicate)
     }
     bool hv[NCH];
     int vv[NCH];
@@ -497,24 +513,15 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs
         hv[q] = act[q] && !((s.absent >> slot[q]) & 1u);
         const int v = ws.slotvar[slot[q]];
         vv[q] = v;
-        const uint32_t S = s.S;
-        const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
-        if (WORLD1) {
-            idx[q] = ((long long)v << (P.m - 1)) + cpr;
-        } else {
-            const int sh = st.sh[v];
-            idx[q] = st.cb[v] + (long long)(cpr & ((1u << sh) - 1u)) +
-                     (((cpr >> sh) != st.pl[v]) ? (1LL << sh) : 0LL);
-        }
-        bic[q] = (rss[q] > 1e-300) ? fma(P.mhalf_n, fast_ln(rss[q], st.lntab), s.Kw)
-                                   : __longlong_as_double(0x7ff0000000000000LL);
+        idx[q] = table_index<WORLD1>(P, v, s.S);
+        bic[q] = bic_of(P, cx, rss[q], s.Kw);
         cur[q] = ws.bb[v];
     }
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
         if (hv[q]) {
-            if (P.out_rss) __stcs(P.out_rss + idx[q], rss[q]);
-            if (P.out_bic) __stcs(P.out_bic + idx[q], bic[q]);
+            if (HR) __stcs(P.out_rss + idx[q], rss[q]);
+            if (HB) __stcs(P.out_bic + idx[q], bic[q]);
         }
         // running best (a11): the 4 lanes of a column group share child vv[q];
         // improvements are rare, so resolve them lane by lane (ascending lane id)
@@ -524,10 +531,7 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs
             bal &= bal - 1;
             if ((int)(threadIdx.x & 31) == l) {
                 const int v = vv[q];
-                const double cb = ws.bb[v];
-                const uint32_t cm = ws.bm[v];
-                const int cs = __popc(cm), sz = __popc(s.S);
-                if (bic[q] > cb || (bic[q] == cb && (sz < cs || (sz == cs && s.S < cm)))) {
+                if (tie_better(bic[q], s.S, ws.bb[v], ws.bm[v])) {
                     ws.bb[v] = bic[q];
                     ws.bm[v] = s.S;
                 }
@@ -537,32 +541,21 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const ShardTabs
     }
 }
 
-template <bool WORLD1>
+template <bool WORLD1, bool HR, bool HB>
 __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ TravParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double2 s_lntab[128];
+    __shared__ double s_Kc[33];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int m = P.m, k = P.k, p = P.p, bh = P.bh, NCS = P.NCS;
-    ShardTabs st{};
-    {
-        double2* lt = (double2*)smem_raw;
-        for (int j = threadIdx.x; j < 128; j += blockDim.x) lt[j] = P.lntab[j];
-        st.lntab = lt;
-    }
-    unsigned char* wbase = smem_raw + 128 * 16;
-    if (!WORLD1) {
-        long long* cb = (long long*)wbase;
-        int* sh = (int*)(cb + 32);
-        uint32_t* pl = (uint32_t*)(sh + 32);
-        for (int v = threadIdx.x; v < 32; v += blockDim.x) {
-            cb[v] = P.child_base[v]; sh[v] = P.sh[v]; pl[v] = P.pat_lo[v];
-        }
-        st.cb = cb; st.sh = sh; st.pl = pl;
-        wbase += 32 * (8 + 4 + 4);
-    }
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh;
+    const int NCS = m + 1;                      // slot stride; slot m = scratch column
+    for (int j = threadIdx.x; j < 128; j += blockDim.x) s_lntab[j] = P.lntab[j];
+    for (int j = threadIdx.x; j < 33; j += blockDim.x) s_Kc[j] = P.Kc[j];
     __syncthreads();
+    Ctx cx{s_lntab, s_Kc};
     const size_t per = warp_smem_bytes(m, k);
-    unsigned char* base = wbase + (size_t)wib * per;
+    unsigned char* base = smem_raw + (size_t)wib * per;
     WarpSmem ws;
     ws.A = (double*)base;
     ws.W = ws.A + (m * (m + 1) / 2);
@@ -574,6 +567,7 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
 
     ws.bb[lane] = -__longlong_as_double(0x7ff0000000000000LL);
     ws.bm[lane] = 0xffffffffu;
+    ws.slotvar[lane] = 0;
     for (int e = lane; e < (2 * k - 1) * NCS * 4; e += 32) ws.W[e] = 0.0;
     __syncwarp();
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -614,7 +608,7 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
         uint32_t Fhi = 0;
         for (int l = 0; l < bh; ++l)
             if ((pack >> l) & 1u) Fhi |= 1u << (m - 1 - l);
-        if (lane < NCS) {
+        if (lane < m) {
             int v;
             if (lane < k) v = p + lane;
             else if (lane < k + p) v = lane - k;
@@ -633,64 +627,58 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
         __syncwarp();
 
         // ---- pack derivation: the 2^p workers' seeds along one GRC path (a5)
-        const int o = org, s = sn, end = sn;
+        const int o = org, sz = sn, end = sn;
         if (p == 2) {
-            snapshot<WORLD1>(P, st, ws, s, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
-            for (int j = 1; j <= k; ++j) grc_packed(ws.A, s, o + j, end, lane);
-            snapshot<WORLD1>(P, st, ws, s, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
-            for (int j = 0; j < k; ++j) grc_packed(ws.A, s, o + j, end, lane);
-            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
-            for (int j = k; j >= 0; --j) grc_packed(ws.A, s, o + j, end, lane);
-            snapshot<WORLD1>(P, st, ws, s, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
+            for (int j = 1; j <= k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
+            for (int j = k; j >= 0; --j) grc_packed(ws.A, sz, o + j, end, lane);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
         } else if (p == 1) {
-            snapshot<WORLD1>(P, st, ws, s, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
-            for (int j = 0; j < k; ++j) grc_packed(ws.A, s, o + j, end, lane);
-            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
         } else {
-            snapshot<WORLD1>(P, st, ws, s, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
         }
 
         // ---- the walk: d + Upsilon(k) in lockstep (a6-a11)
         const uint32_t Fw = Fhi | (uint32_t)w;          // pack var j = user id j
         const int dw = dh + __popc((uint32_t)w);
         const int NBp = NCSp - k;
-        double* const Ww = ws.W + w;
-        uint64_t perm = 0;                                   // free position -> slot (nibbles)
+        uint64_t perm = 0;                              // free position -> slot (nibbles)
         for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
-        int inext = (int)__ldg(P.sched) - 1;
+        int iraw = (int)__ldg(P.sched);
         for (int t = 0; t < P.sched_len; ++t) {
-            const int i = inext;
-            if (t + 1 < P.sched_len) inext = (int)__ldg(P.sched + t + 1) - 1;   // prefetch
+            const int i = iraw - 1;
+            if (t + 1 < P.sched_len) iraw = (int)__ldg(P.sched + t + 1);   // prefetch next
             const int X = (int)((perm >> (4 * i)) & 15u);
             const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
             {
                 const uint64_t d = (uint64_t)(X ^ Y);
                 perm ^= (d << (4 * i)) | (d << (4 * (i + 1)));
             }
-            double* const R0 = Ww + i * RS;            // row i
-            double* const R1 = R0 + RS;                // row i+1
-            double* const U2 = Ww + (k + i) * RS;      // U row i+2
-            double* const U1 = U2 - RS;                // U row i+1 (valid when i >= 1)
+            const int r0 = i * RS + w;
             double c, sn, h;
-            givens(R0[Y << 2], R1[Y << 2], c, sn, h);
+            givens(ws.W[r0 + (Y << 2)], ws.W[r0 + RS + (Y << 2)], c, sn, h);
             const uint32_t T = ws.pm[i] | (1u << (p + Y));
-            const double Kw = P.Kc[dw + i + 1];
+            const double Kw = cx.Kc[dw + i + 1];
             __syncwarp();
-            const uint32_t S = Fw | T;
             const int nf = k - 1 - i;
             const int L = nf + NBp;
-            const int nch = (L + 7) >> 3;
-            StepCtx sc{R0, R1, U2, U1, c, sn, S, Kw, X, i, nf, L, cl, w, absent};
-            switch (nch) {
-                case 1: walk_chunks<WORLD1, 1>(P, st, ws, sc); break;
-                case 2: walk_chunks<WORLD1, 2>(P, st, ws, sc); break;
-                case 3: walk_chunks<WORLD1, 3>(P, st, ws, sc); break;
-                default: walk_chunks<WORLD1, 4>(P, st, ws, sc); break;
+            StepCtx sc{r0, RS, c, sn, Fw | T, Kw, X, i, nf, L, cl, m, absent};
+            switch ((L + 7) >> 3) {
+                case 1: walk_chunks<WORLD1, HR, HB, 1>(P, cx, ws, sc); break;
+                case 2: walk_chunks<WORLD1, HR, HB, 2>(P, cx, ws, sc); break;
+                case 3: walk_chunks<WORLD1, HR, HB, 3>(P, cx, ws, sc); break;
+                default: walk_chunks<WORLD1, HR, HB, 4>(P, cx, ws, sc); break;
             }
             if (cl == 0) {
-                R0[Y << 2] = h;
-                R1[Y << 2] = 0.0;
-                if (i >= 1) U1[Y << 2] = 0.0;
+                ws.W[r0 + (Y << 2)] = h;
+                ws.W[r0 + RS + (Y << 2)] = 0.0;
+                if (i >= 1) ws.W[r0 + (k - 1) * RS + (Y << 2)] = 0.0;     // U row i+1
             }
             if (lane == 0) {
                 ws.posmap[i] = (uint8_t)Y;
@@ -796,36 +784,43 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
     return cudaGetLastError();
 }
 
-static size_t traverse_smem(int m, int k, int wpc, int world1)
+static size_t traverse_smem(int m, int k, int wpc) { return warp_smem_bytes(m, k) * wpc; }
+
+template <bool W1, bool HR, bool HB>
+static cudaError_t launch_tv(const TravParams& P, int grid, int wpc, cudaStream_t st)
 {
-    return warp_smem_bytes(m, k) * wpc + cta_smem_extra(world1);
+    size_t smem = traverse_smem(P.m, P.k, wpc);
+    cudaError_t e = cudaFuncSetAttribute(traverse_kernel<W1, HR, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    traverse_kernel<W1, HR, HB><<<grid, wpc * 32, smem, st>>>(P);
+    return cudaGetLastError();
 }
 
 int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta)
 {
-    size_t smem = traverse_smem(m, k, warps_per_cta, 1);
-    cudaFuncSetAttribute(traverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t smem = traverse_smem(m, k, warps_per_cta);
+    cudaFuncSetAttribute(traverse_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, traverse_kernel<true>, warps_per_cta * 32, smem) !=
-        cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, traverse_kernel<true, true, true>, warps_per_cta * 32,
+                                                      smem) != cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
 
-cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st)
+cudaError_t launch_traverse(const TravParams& P, int grid, int wpc, cudaStream_t st)
 {
-    const bool w1 = P.world1 != 0;
-    size_t smem = traverse_smem(P.m, P.k, warps_per_cta, w1);
-    if (w1) {
-        cudaError_t e = cudaFuncSetAttribute(traverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        traverse_kernel<true><<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
-    } else {
-        cudaError_t e = cudaFuncSetAttribute(traverse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        traverse_kernel<false><<<grid_ctas, warps_per_cta * 32, smem, st>>>(P);
+    const int key = (P.world1 ? 4 : 0) | (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
+    switch (key) {
+        case 7: return launch_tv<true, true, true>(P, grid, wpc, st);
+        case 6: return launch_tv<true, true, false>(P, grid, wpc, st);
+        case 5: return launch_tv<true, false, true>(P, grid, wpc, st);
+        case 4: return launch_tv<true, false, false>(P, grid, wpc, st);
+        case 3: return launch_tv<false, true, true>(P, grid, wpc, st);
+        case 2: return launch_tv<false, true, false>(P, grid, wpc, st);
+        case 1: return launch_tv<false, false, true>(P, grid, wpc, st);
+        default: return launch_tv<false, false, false>(P, grid, wpc, st);
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,

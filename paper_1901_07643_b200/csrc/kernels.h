@@ -24,9 +24,8 @@ struct TravParams {
     double mhalf_n;             // -n/2
     const double2* lntab;       // fast-log table (128 x (r_j, -ln r_j))
     double Kc[33];              // BIC constant per parent-set size
-    long long child_base[32];   // rank-local layout (plan.h)
-    int sh[32];
-    unsigned pat_lo[32];
+    int r;                      // rank-selector bits (world > 1)
+    unsigned patlo;             // smaller selector pattern of this rank (non-selector children)
 };
 
 // smem bytes per warp of the traversal kernel
