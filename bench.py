@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--wpc", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--outputs", default="both", choices=["both", "rss", "bic", "none"],
+                    help="diagnostic: which tables the timed run writes (the metric needs both)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -232,11 +234,14 @@ def bench_ours(args):
         B = torch.stack(gb).cpu().numpy()
         bn.bnreg_best_merge(m, M, B)
 
+    out_r = rss if args.outputs in ("both", "rss") else None
+    out_b = bic if args.outputs in ("both", "bic") else None
+
     def step_device():
         if rank == 0:
             h.load(Xd)
         broadcast_root()
-        h.run_async(rss, bic, bm_d, bb_d)
+        h.run_async(out_r, out_b, bm_d, bb_d)
         gather_best()
 
     def step_e2e():

@@ -129,7 +129,7 @@ def bnreg_plan_query(m: int, n: int, opt: Options | None = None) -> dict:
     info = np.zeros(16, dtype=np.int64)
     _check(lib().bnreg_plan_query(m, n, ctypes.byref(opt) if opt else None, _hptr(info)))
     keys = ["k", "b", "p", "bh", "L1", "LW", "npacks", "sched_len", "local_families", "total_families",
-            "smem_per_warp", "r"]
+            "smem_per_warp", "r", "g"]
     return {k: int(v) for k, v in zip(keys, info)}
 
 

@@ -120,6 +120,7 @@ bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* o, int6
         info[0] = P.k; info[1] = P.b; info[2] = P.p; info[3] = P.bh; info[4] = P.L1; info[5] = P.LW;
         info[6] = (int64_t)P.packs.size(); info[7] = (int64_t)P.sched.size(); info[8] = P.local_families;
         info[9] = P.total_families; info[10] = (int64_t)traverse_smem_per_warp(P.m, P.k); info[11] = P.r;
+        info[12] = P.g;
     } catch (std::exception& e) {
         return fail(BNREG_E_INVAL, e.what());
     }
@@ -193,10 +194,11 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_sched, std::max<size_t>(1, P.sched.size())));
     if (!P.sched.empty()) CKH(cudaMemcpy(h->d_sched, P.sched.data(), P.sched.size(), cudaMemcpyHostToDevice));
     CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
-    h->wpc = d.warps_per_cta > 0 ? d.warps_per_cta : 2;
+    h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
+    (void)d.warps_per_cta;
     int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
     int64_t want = (int64_t)h->num_sms * per_sm;
-    int64_t need = ((int64_t)P.packs.size() + h->wpc - 1) / h->wpc;
+    int64_t need = (int64_t)P.packs.size();
     h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
     size_t gw = (size_t)h->grid_ctas * h->wpc;
     CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
@@ -350,7 +352,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     }
     if (h->timing) CK(cudaEventRecord(h->ev[1], st));
     TravParams T{};
-    T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p;
+    T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p; T.g = P.g;
     T.NCS = P.m; T.SA = P.m | 1;
     T.sched_len = (int)P.sched.size();
     if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) T.sched_len = std::min(T.sched_len, atoi(dbg));  // profiling aid

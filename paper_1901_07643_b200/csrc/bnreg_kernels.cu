@@ -447,7 +447,7 @@ __device__ void snapshot(const TravParams& P, const Ctx& cx, const WarpSmem& ws,
                 if (r < k) ws.W[Ridx(r, slot, w, NCS)] = x;
                 if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
                 if (r <= k) {
-                    uint32_t S = Fmask | (((1u << r) - 1u) << P.p);
+                    uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
                     harvest<WORLD1, HR, HB>(P, cx, v, S, cx.Kc[d + r], acc, ws);
                 }
             }
@@ -542,14 +542,16 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const Ctx& cx, 
 }
 
 template <bool WORLD1, bool HR, bool HB>
-__global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ TravParams P)
+__global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ TravParams P)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 s_lntab[128];
     __shared__ double s_Kc[33];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int m = P.m, k = P.k, p = P.p, bh = P.bh;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
+    const int fv0 = p + g;                      // user id of free slot 0
     const int NCS = m + 1;                      // slot stride; slot m = scratch column
+    __shared__ uint32_t s_item;
     for (int j = threadIdx.x; j < 128; j += blockDim.x) s_lntab[j] = P.lntab[j];
     for (int j = threadIdx.x; j < 33; j += blockDim.x) s_Kc[j] = P.Kc[j];
     __syncthreads();
@@ -582,11 +584,14 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             if ((w >> j) & 1) absent |= 1u << (k + j);
 
     for (;;) {
-        uint32_t item = 0;
-        if (lane == 0) item = atomicAdd(P.counter, 1u);
-        item = __shfl_sync(FULLMASK, item, 0);
+        // one work item = one gang: the CTA's 2^g warps take the 2^g packs that
+        // differ in the gang variables and walk them in lockstep
+        if (threadIdx.x == 0) s_item = atomicAdd(P.counter, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        __syncthreads();
         if ((int)item >= P.npacks) break;
-        const uint32_t pack = P.packs[item];
+        const uint32_t pack = P.packs[item] | ((uint32_t)wib << (bh - g));
 
         // ---- seed: load the depth-L1 node, derive the remaining hi levels (a5)
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
@@ -605,23 +610,26 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             }
         }
         // slot -> user id: free, pack, then hi vars in B (ascending id = latest deferred first)
-        uint32_t Fhi = 0;
+        uint32_t Fhi = 0;                                   // tree-level vars in F (user ids)
         for (int l = 0; l < bh; ++l)
-            if ((pack >> l) & 1u) Fhi |= 1u << (m - 1 - l);
+            if ((pack >> l) & 1u) Fhi |= 1u << (l < bh - g ? m - 1 - l : fv0 - 1 - (l - (bh - g)));
         if (lane < m) {
             int v;
-            if (lane < k) v = p + lane;
+            if (lane < k) v = fv0 + lane;
             else if (lane < k + p) v = lane - k;
             else {
+                // back set: tree-level vars not in F, ascending id (= latest deferred first)
                 int q = lane - k - p, cnt = 0;
                 v = 0;
-                for (int id = p + k; id < m; ++id)
+                for (int id = p; id < m; ++id) {
+                    if (id >= fv0 && id < fv0 + k) continue;
                     if (!((Fhi >> id) & 1u)) { if (cnt == q) { v = id; break; } ++cnt; }
+                }
             }
             ws.slotvar[lane] = (uint8_t)v;
         }
         if (lane < 16) ws.posmap[lane] = (uint8_t)lane;
-        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << p) : 0u;
+        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << fv0) : 0u;
         const int dh = __popc(pack);
         const int NCSp = k + p + (bh - dh);   // slots in use for this pack
         __syncwarp();
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
             const int r0 = i * RS + w;
             double c, sn, h;
             givens(ws.W[r0 + (Y << 2)], ws.W[r0 + RS + (Y << 2)], c, sn, h);
-            const uint32_t T = ws.pm[i] | (1u << (p + Y));
+            const uint32_t T = ws.pm[i] | (1u << (fv0 + Y));
             const double Kw = cx.Kc[dw + i + 1];
             __syncwarp();
             const int nf = k - 1 - i;
@@ -685,7 +693,8 @@ __global__ void __launch_bounds__(64) traverse_kernel(const __grid_constant__ Tr
                 ws.posmap[i + 1] = (uint8_t)X;
                 ws.pm[i + 1] = T;
             }
-            __syncwarp();
+            if (g) __syncthreads();      // the gang's warps write one 128 B line per (child, T)
+            else __syncwarp();
         }
     }
     // ---- per-warp best -> global partials (a11)

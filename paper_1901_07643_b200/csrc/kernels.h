@@ -10,12 +10,13 @@ namespace bnr {
 // a8 harvest + a9 BIC + a10 store + a11 per-child running best).
 struct TravParams {
     int m, k, p, bh, L1, nw, NCS, SA;
+    int g;                      // gang bits: 2^g lockstep warps per CTA
     int sched_len;
     int npacks;
     int world1;                 // 1: single rank, identity table layout
     const int8_t* sched;        // Upsilon(k), 1-based swap positions
     const double* nodes;        // seed-tree nodes at depth L1, m*m doubles each
-    const uint32_t* packs;      // this rank's pack ids (costliest first)
+    const uint32_t* packs;      // this rank's work items = gang base pack ids (costliest first)
     unsigned int* counter;      // work-queue counter (zeroed before launch)
     double* out_rss;            // rank-local RSS table (device) or nullptr
     double* out_bic;            // rank-local BIC table (device) or nullptr

@@ -13,12 +13,18 @@
 // Variable roles (reading G27: any relabelling is valid; the table stays keyed
 // by user ids):
 //   pack vars  ids 0..p-1            (p = min(2, b)); lowest ids so the 2^p
-//                                     workers of a pack write adjacent entries
-//   free vars  ids p..p+k-1           the k variables Upsilon(k) permutes
-//   hi vars    ids p+k..m-1           processed in DEScending id order by the
-//                                     seed tree: hv[l] = m-1-l is bit l of the
-//                                     pack id P (1 = in front set F)
-// A worker = (pack P, w) with w bit j = 1 iff pack var j is in F.
+//                                     workers of a pack (one warp) write
+//                                     adjacent entries (a 32 B sector)
+//   gang vars  ids p..p+g-1           (g <= 2) the 2^g warps of a CTA differ in
+//                                     these and step in lockstep, so one step
+//                                     writes 2^(p+g) adjacent entries (128 B)
+//   free vars  ids p+g..p+g+k-1       the k variables Upsilon(k) permutes
+//   hi vars    ids p+g+k..m-1         with the gang vars, the "pinned" levels of
+//                                     the seed tree: hv[l] = m-1-l for the top
+//                                     ids, then the gang ids p+g-1..p last;
+//                                     bit l of the pack id P is hv[l] in F
+// A worker = (pack P, w) with w bit j = 1 iff pack var j is in F.  A work item
+// = a gang: the 2^g packs whose ids differ only in the top g bits.
 #pragma once
 #include <cstdint>
 #include <cmath>
@@ -32,6 +38,7 @@ namespace bnr {
 constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
 constexpr int kPackBits = 2;     // 4 lockstep workers per warp
+constexpr int kGangBits = 2;     // 4 lockstep warps per CTA
 
 // Alg.1 GreedySwaps(m) with Eq.10's +1.
 // Returns 1-based swap positions, length 2^m - m - 1 (Eq.9).
@@ -49,14 +56,15 @@ inline std::vector<int8_t> greedy_swaps(int m)
 }
 
 struct Plan {
-    int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh hi bits
+    int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
+    int g = 0;                                // gang bits (the top g of the bh tree bits)
     int L1 = 0, LW = 0;                       // tree depth in global memory / levels derived in-warp
     int world = 1, rank = 0, r = 0;           // rank selector bits r (0 when world == 1)
     int64_t n = 0;
     int64_t total_families = 0;               // m 2^(m-1)
     int64_t local_families = 0;               // this rank's share
     std::vector<int8_t> sched;                // Upsilon(k), 1-based
-    std::vector<uint32_t> packs;              // this rank's pack ids, costliest first
+    std::vector<uint32_t> packs;              // this rank's work items (gang base pack ids), costliest first
     std::vector<int> root_order;              // position -> user id of the root R
     // rank-local layout: per child, up to 2 ranges of the child's 2^(m-1) block
     int64_t child_base[32] = {0};             // local offset of child v's first range
@@ -68,6 +76,12 @@ struct Plan {
 };
 
 inline int popc(uint32_t x) { return __builtin_popcount(x); }
+
+// user id of tree level l (bit l of a pack id)
+inline int hv_id(const Plan& P, int l)
+{
+    return l < P.bh - P.g ? P.m - 1 - l : P.p + P.g - 1 - (l - (P.bh - P.g));
+}
 
 // Cost of a pack in families (sum over its 2^p workers of 2^(k-1)(2(m-d)-k)).
 inline int64_t pack_cost(const Plan& P, uint32_t pack)
@@ -94,31 +108,38 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.p = std::min(kPackBits, P.b);
     P.bh = P.b - P.p;
+    P.g = std::min(kGangBits, P.bh);
     if (lw < 0) lw = 4;
-    P.LW = std::min(lw, P.bh);
+    P.LW = std::min(std::max(lw, P.g), P.bh);
     P.L1 = P.bh - P.LW;
     P.world = world; P.rank = rank;
     P.total_families = (int64_t)m << (m - 1);
     P.sched = greedy_swaps(k);
-    // root order: [hv[0..bh-1], pack 0..p-1, free p..p+k-1]
-    for (int l = 0; l < P.bh; ++l) P.root_order.push_back(m - 1 - l);
+    // root order: [hv[0..bh-1], pack 0..p-1, free p+g..p+g+k-1]
+    for (int l = 0; l < P.bh; ++l) P.root_order.push_back(hv_id(P, l));
     for (int j = 0; j < P.p; ++j) P.root_order.push_back(j);
-    for (int f = 0; f < k; ++f) P.root_order.push_back(P.p + f);
+    for (int f = 0; f < k; ++f) P.root_order.push_back(P.p + P.g + f);
 
     // rank selector: top r hi bits (hv[0..r-1] = ids m-1..m-r), complementary patterns
     if (world > 1) {
         int r = 0;
         while ((1 << r) < 2 * world) ++r;
-        if (r > P.bh) throw std::invalid_argument("too few pinned variables for this world size (lower k)");
+        if (r > P.bh - P.g) throw std::invalid_argument("too few pinned variables for this world size (lower k)");
         P.r = r;
     }
     uint32_t tmask = (1u << P.r) - 1u;
     uint32_t t0 = (uint32_t)rank, t1 = tmask ^ (uint32_t)rank;
     std::vector<uint32_t> all;
-    for (uint32_t q = 0; q < (1u << P.bh); ++q)
+    const int gs = P.bh - P.g;                    // gang bits are the top g tree bits
+    auto item_cost = [&](uint32_t q) {
+        int64_t c = 0;
+        for (uint32_t j = 0; j < (1u << P.g); ++j) c += pack_cost(P, q | (j << gs));
+        return c;
+    };
+    for (uint32_t q = 0; q < (1u << gs); ++q)
         if (world == 1 || (q & tmask) == t0 || (q & tmask) == t1) all.push_back(q);
     std::stable_sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) {
-        int64_t ca = pack_cost(P, a), cb = pack_cost(P, b);
+        int64_t ca = item_cost(a), cb = item_cost(b);
         return ca != cb ? ca > cb : a < b;
     });
     P.packs = all;

@@ -58,15 +58,19 @@ def test_plan_partition(bn, m, k):
     q = bn.bnreg_plan_query(m, n, bn.options(free_vars=k))
     assert q["sched_len"] == 2 ** k - k - 1
     assert q["b"] == m - k and q["p"] == min(2, m - k)
-    packs = bn.bnreg_plan_packs(m, n, bn.options(free_vars=k))
-    assert sorted(packs.tolist()) == list(range(1 << q["bh"]))
+    def expand(items):
+        gs = q["bh"] - q["g"]
+        return [it | (j << gs) for it in items for j in range(1 << q["g"])]
+
+    packs = expand(bn.bnreg_plan_packs(m, n, bn.options(free_vars=k)).tolist())
+    assert sorted(packs) == list(range(1 << q["bh"]))
     for world in [2, 4, 8]:
-        if (1 << q["bh"]) < 2 * world:
+        if (1 << (q["bh"] - q["g"])) < 2 * world:
             continue
         allp, costs, fams = [], [], 0
         for rank in range(world):
             o = bn.options(free_vars=k, world=world, rank=rank)
-            pr = bn.bnreg_plan_packs(m, n, o).tolist()
+            pr = expand(bn.bnreg_plan_packs(m, n, o).tolist())
             allp += pr
             # family count of a pack = sum over its workers of 2^(k-1)(2(m-d)-k) (V11)
             c = sum(sum(2 ** (k - 1) * (2 * (m - (bin(P).count("1") + bin(w).count("1"))) - k)
