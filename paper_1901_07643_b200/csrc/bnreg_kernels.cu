@@ -335,52 +335,64 @@ __device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- walk state layout
+// Per warp (one pack = 4 workers w):
+//   W[w]  column-contiguous walk state, for every slot s (a column of the
+//         worker's R restricted to its k free rows) the k pairs
+//           E_l = (R_l, U_{l+1}),  l = 0..k-1,
+//         U_l = sum_{r >= l} R_r^2 (+ the tail below the free rows for back
+//         columns): a GRC at free position i reads E_i, E_{i+1} and writes
+//         E_i = (R'_i, U'_{i+1}), E_{i+1}.x = R'_{i+1}  (a8: suffix sums by
+//         addition only).  Column stride CS = 16 (k|1) bytes (odd number of
+//         16 B units), worker stride WS = 16 ws16 with ws16 = 2 (mod 8): the 8
+//         lanes of an LDS.128 phase hit distinct bank groups.
+//   A     the packed seed triangle of the derivation; it overlaps the region
+//         of the worker snapshotted last (placed last in memory).
+//   rec   per slot: row pointers (this child's block of the RSS / BIC table)
+//   bb,bm per child: the warp's running best (a11)
 struct WarpSmem {
-    double* A;        // packed triangle, side <= m (seed derivation)
-    double* W;        // (2k-1) rows x NCS slots x 4 workers  (R rows 0..k-1, U rows 2..k);
-                      // slot m is a scratch column for idle lanes
-    double* bb;       // [32] best BIC over the warp's workers, per child
-    uint32_t* bm;     // [32] its parent mask
-    uint32_t* pm;     // [17] free-prefix masks (user ids) by prefix length
-    uint8_t* posmap;  // [16] free position -> free slot
-    uint8_t* slotvar; // [32] slot -> user id
+    unsigned char* Wb;      // worker regions
+    double* A;              // packed derivation triangle
+    ulonglong2* rec;        // [32] (rss row ptr, bic row ptr)
+    double* bb;             // [32]
+    uint32_t* bm;           // [32]
+    uint32_t* pm;           // [17] free-prefix masks by prefix length (user ids)
+    uint8_t* posmap;        // [48] walk position -> slot (positions >= NCSp -> 0)
+    uint8_t* slotvar;       // [32] slot -> user id
 };
+
+__host__ __device__ inline void walk_geometry(int m, int k, int& CS, int& WS)
+{
+    const int cs16 = k | 1;
+    int ws16 = m * cs16;
+    ws16 += (2 - (ws16 & 7) + 8) & 7;
+    CS = cs16 * 16;
+    WS = ws16 * 16;
+}
 
 __host__ __device__ inline size_t warp_smem_bytes(int m, int k)
 {
-    size_t a = (size_t)(m * (m + 1) / 2) * 8;
-    size_t w = (size_t)(2 * k - 1) * (m + 1) * 4 * 8;
-    size_t best = 32 * (8 + 4);
-    size_t misc = 17 * 4 + 16 + 32;
-    size_t tot = a + w + best + misc;
+    int CS, WS;
+    walk_geometry(m, k, CS, WS);
+    size_t asz = (size_t)(m * (m + 1) / 2) * 8;
+    size_t w = (size_t)4 * WS;
+    if ((size_t)3 * WS + asz > w) w = (size_t)3 * WS + asz;
+    size_t tot = w + 32 * 16 + 32 * 8 + 32 * 4 + 17 * 4 + 48 + 32;
     return (tot + 15) & ~(size_t)15;
 }
 
 size_t traverse_smem_per_warp(int m, int k) { return warp_smem_bytes(m, k); }
 
-struct Ctx {
-    const double2* lntab;   // fast-log table (shared memory)
-    const double* Kc;       // BIC constants by |S| (shared memory)
-};
-
-// Rank-local table index of (v, S) (plan.h layout): world 1 = the global
-// index; otherwise child v owns 2^(m-r) entries at v 2^(m-r), holding the
-// compressed masks whose top selector bits match this rank's pattern(s).
-template <bool WORLD1>
-__device__ __forceinline__ long long table_index(const TravParams& P, int v, uint32_t S)
+// region index of worker w: the worker snapshotted last owns the last region
+__device__ __forceinline__ int region_of(int w, int p)
 {
-    const uint32_t cpr = (S & ((1u << v) - 1u)) | ((S >> (v + 1)) << v);
-    if (WORLD1) return ((long long)v << (P.m - 1)) + cpr;
-    const bool sel = v >= P.m - P.r;
-    const int sh = sel ? P.m - P.r : P.m - 1 - P.r;
-    const uint32_t low = (cpr & ((1u << sh) - 1u)) + ((!sel && (cpr >> sh) != P.patlo) ? (1u << sh) : 0u);
-    return ((long long)v << (P.m - P.r)) + low;
+    const int last = (p == 2) ? 2 : 0;
+    return w == last ? 3 : (w < last ? w : w - 1);
 }
 
-__device__ __forceinline__ double bic_of(const TravParams& P, const Ctx& cx, double rss, double Kw)
+__device__ __forceinline__ double bic_of(double rss, double lnr, double mhalf_n, double Kw)
 {
-    const double lnr = fast_ln(fmax(rss, 1e-300), cx.lntab);
-    const double bic = fma(P.mhalf_n, lnr, Kw);
+    const double bic = fma(mhalf_n, lnr, Kw);
     return rss > 1e-300 ? bic : __longlong_as_double(0x7ff0000000000000LL);
 }
 
@@ -391,21 +403,20 @@ __device__ __forceinline__ bool tie_better(double b, uint32_t S, double cb, uint
     return s1 != s2 ? s1 < s2 : S < cm;
 }
 
-// One family outside the lockstep walk (seed prefixes): index, BIC, stores,
-// running best.  The caller guarantees no other lane touches child v meanwhile.
-template <bool WORLD1, bool HR, bool HB>
-__device__ __forceinline__ void harvest(const TravParams& P, const Ctx& cx, int v, uint32_t S, double Kw,
-                                        double rss, const WarpSmem& ws)
+// Offset (in entries) of family (v, S) inside child v's block of this rank's
+// table, given lm = (1 << v) - 1: compress(S, v) is the bitwise select
+// lm ? S : S >> 1 (bit v of S is 0).  World 1: the block is v 2^(m-1).. and
+// the offset is the compressed mask; otherwise (plan.h) child v's 2^(m-r)
+// entries hold the masks whose top selector bits match this rank's patterns.
+template <bool WORLD1>
+__device__ __forceinline__ uint32_t block_offset(const TravParams& P, uint32_t S, uint32_t S1, uint32_t lm)
 {
-    const long long idx = table_index<WORLD1>(P, v, S);
-    const double bic = bic_of(P, cx, rss, Kw);
-    if (HR) __stcs(P.out_rss + idx, rss);
-    if (HB) __stcs(P.out_bic + idx, bic);
-    const double cur = ws.bb[v];
-    if (bic >= cur && tie_better(bic, S, cur, ws.bm[v])) {
-        ws.bb[v] = bic;
-        ws.bm[v] = S;
-    }
+    const uint32_t cpr = (S & lm) | (S1 & ~lm);
+    if (WORLD1) return cpr;
+    const int v = __popc(lm);
+    const bool sel = v >= P.m - P.r;
+    const int sh = sel ? P.m - P.r : P.m - 1 - P.r;
+    return (cpr & ((1u << sh) - 1u)) + ((!sel && (cpr >> sh) != P.patlo) ? (1u << sh) : 0u);
 }
 
 // Logical position (relative to the snapshot origin) of a walk slot for worker
@@ -423,121 +434,160 @@ __device__ __forceinline__ int slot_pos(int slot, int w, int k, int p, int nw)
     return k + present + (slot - k - p);
 }
 
-// Snapshot: convert the sub-triangle of A starting at physical origin `org` into
-// worker w's walk state (free rows of R, suffix sums U) and harvest the seed
-// prefixes of sizes d..d+k (reading G11).  Lanes = walk slots.
+// One family outside the lockstep walk (seed prefixes): stores + running best.
+// The caller guarantees that no other lane touches child v meanwhile.
 template <bool WORLD1, bool HR, bool HB>
-__device__ void snapshot(const TravParams& P, const Ctx& cx, const WarpSmem& ws, int s, int org, int w,
-                         uint32_t Fmask, int d, int lane, int NCS, int ncsp)
+__device__ __forceinline__ void harvest_one(const TravParams& P, const double2* lntab, const WarpSmem& ws,
+                                            int slot, uint32_t S, double Kw, double rss)
+{
+    const int v = ws.slotvar[slot];
+    const uint32_t lm = (1u << v) - 1u;
+    const uint32_t off = block_offset<WORLD1>(P, S, S >> 1, lm);
+    const ulonglong2 rp = ws.rec[slot];
+    const double bic = bic_of(rss, fast_ln(fmax(rss, 1e-300), lntab), P.mhalf_n, Kw);
+    if (HR) __stcs((double*)rp.x + off, rss);
+    if (HB) __stcs((double*)rp.y + off, bic);
+    const double cur = ws.bb[v];
+    if (bic >= cur && tie_better(bic, S, cur, ws.bm[v])) {
+        ws.bb[v] = bic;
+        ws.bm[v] = S;
+    }
+}
+
+// Snapshot: convert the sub-triangle of A starting at physical origin `org`
+// (side s) into worker w's walk state and harvest its seed prefixes of sizes
+// d..d+k (reading G11).  Lanes = walk slots.  STAGE: A overlaps this worker's
+// region, so each lane first reads its whole column into registers.
+template <bool WORLD1, bool HR, bool HB, bool STAGE>
+__device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSmem& ws, int s, int org, int w,
+                         uint32_t Fmask, int d, int lane, int CS, int WS, int ncsp, double K0, double mhlnn)
 {
     const int k = P.k;
     if (w >= P.nw) return;
     const int slot = lane;
-    if (slot < ncsp) {
-        const int pos = slot_pos(slot, w, k, P.p, P.nw);
-        if (pos < 0) {
-            for (int r = 0; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
-            for (int u = 2; u <= k; ++u) ws.W[Ridx(k + u - 2, slot, w, NCS)] = 0.0;
-        } else {
-            const int v = ws.slotvar[slot];
-            double acc = 0.0;
-            for (int r = pos; r >= 0; --r) {
-                double x = ws.A[poff(org + r, s) + pos - r];
-                acc = fma(x, x, acc);
-                if (r < k) ws.W[Ridx(r, slot, w, NCS)] = x;
-                if (r >= 2 && r <= k) ws.W[Ridx(k + r - 2, slot, w, NCS)] = acc;
-                if (r <= k) {
-                    uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
-                    harvest<WORLD1, HR, HB>(P, cx, v, S, cx.Kc[d + r], acc, ws);
+    const int pos = (slot < ncsp) ? slot_pos(slot, w, k, P.p, P.nw) : -1;
+    double col[STAGE ? 32 : 1];
+    if (STAGE) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+            col[r] = (r <= pos) ? ws.A[poff(org + r, s) + pos - r] : 0.0;
+        __syncwarp();
+    }
+    double* E = (double*)(ws.Wb + region_of(w, P.p) * WS + slot * CS);
+    if (slot < P.m) {
+        for (int l = 0; l < k; ++l) { E[2 * l] = 0.0; E[2 * l + 1] = 0.0; }
+        double acc = 0.0;
+        if (STAGE) {
+#pragma unroll
+            for (int r = 31; r >= 0; --r) {
+                if (r <= pos) {
+                    const double x = col[r];
+                    acc = fma(x, x, acc);
+                    if (r < k) E[2 * r] = x;
+                    if (r >= 1 && r <= k) E[2 * (r - 1) + 1] = acc;       // U_r
+                    if (r <= k) {
+                        const uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
+                        harvest_one<WORLD1, HR, HB>(P, lntab, ws, slot, S, fma((double)(d + r), mhlnn, K0), acc);
+                    }
                 }
             }
-            for (int r = pos + 1; r < k; ++r) ws.W[Ridx(r, slot, w, NCS)] = 0.0;
-            for (int u = (pos + 1 > 2 ? pos + 1 : 2); u <= k; ++u) ws.W[Ridx(k + u - 2, slot, w, NCS)] = 0.0;
+        } else {
+            for (int r = pos; r >= 0; --r) {
+                const double x = ws.A[poff(org + r, s) + pos - r];
+                acc = fma(x, x, acc);
+                if (r < k) E[2 * r] = x;
+                if (r >= 1 && r <= k) E[2 * (r - 1) + 1] = acc;           // U_r
+                if (r <= k) {
+                    const uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
+                    harvest_one<WORLD1, HR, HB>(P, lntab, ws, slot, S, fma((double)(d + r), mhlnn, K0), acc);
+                }
+            }
         }
     }
     __syncwarp();
 }
 
 struct StepCtx {
-    int r0;           // W offset of (row i, slot 0, this worker); row stride RS
-    int RS;
-    double c, sn;     // the GRC's rotation
-    uint32_t S;       // the new prefix set (user ids) for this worker
-    double Kw;        // BIC constant for |S|
-    int X, i, nf, L, cl, dummy;
-    uint32_t absent;  // slots whose variable is in this worker's front set
+    unsigned char* base;   // this lane's worker region + 16 i (E_i of slot 0)
+    int CS;
+    double c, sn;          // the GRC's rotation
+    uint32_t S, S1;        // new prefix set of this worker (user ids), S >> 1
+    double Kw;             // BIC constant for |S|
+    int X, i, L, cl;
+    uint32_t absent;       // slots whose variable is in this worker's front set
 };
 
-// One GRC step over NCH chunks of 8 list entries per worker.  The NCH families
-// of a lane are independent dependency chains (ILP): gather -> rotate + suffix
-// sums -> index + log + BIC -> stores + best.  Idle lanes work on the scratch
-// column, so no stores need branches.
+// One GRC step over NCH chunks of 8 list entries per worker (list = positions
+// i+1.. of the walk order: the free columns after the swap, then the back
+// columns).  The NCH families of a lane are independent chains (ILP).
 template <bool WORLD1, bool HR, bool HB, int NCH>
-__device__ __forceinline__ void walk_chunks(const TravParams& P, const Ctx& cx, const WarpSmem& ws,
+__device__ __forceinline__ void walk_chunks(const TravParams& P, const double2* lntab, const WarpSmem& ws,
                                             const StepCtx& s)
 {
-    double* const W = ws.W;
-    const int RS = s.RS;
-    const int rU2 = s.r0 + (P.k) * RS;          // U row i+2 lives at W row k+i
     int slot[NCH];
     bool act[NCH];
-    double x[NCH], y[NCH], u2[NCH];
+    double2 e0[NCH], e1[NCH];
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
         const int e = s.cl + 8 * q;
         act[q] = e < s.L;
-        const int sl = (e == 0) ? s.X : (e < s.nf ? (int)ws.posmap[s.i + 1 + e] : P.k + (e - s.nf));
-        slot[q] = act[q] ? sl : s.dummy;
-        const int so = slot[q] << 2;
-        x[q] = W[s.r0 + so];
-        y[q] = W[s.r0 + RS + so];
-        u2[q] = W[rU2 + so];
+        slot[q] = (q == 0 && s.cl == 0) ? s.X : (int)ws.posmap[s.i + 1 + e];
+        const unsigned char* col = s.base + slot[q] * s.CS;
+        e0[q] = *(const double2*)col;
+        e1[q] = *(const double2*)(col + 16);
     }
     double rss[NCH];
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
-        const double xn = fma(s.c, x[q], s.sn * y[q]);
-        const double yn = fma(s.c, y[q], -s.sn * x[q]);
-        rss[q] = fma(yn, yn, u2[q]);
-        const int so = slot[q] << 2;
-        W[s.r0 + so] = xn;
-        W[s.r0 + RS + so] = yn;
-        if (s.i >= 1) W[rU2 - RS + so] = rss[q];    // U row i+1 (uniform predicate)
+        const double xn = fma(s.c, e0[q].x, s.sn * e1[q].x);
+        const double yn = fma(s.c, e1[q].x, -s.sn * e0[q].x);
+        rss[q] = fma(yn, yn, e1[q].y);
+        if (act[q]) {
+            unsigned char* col = s.base + slot[q] * s.CS;
+            *(double2*)col = make_double2(xn, rss[q]);
+            *(double*)(col + 16) = yn;
+        }
     }
     bool hv[NCH];
+    double bic[NCH];
+    ulonglong2 rp[NCH];
+    uint32_t off[NCH];
     int vv[NCH];
-    long long idx[NCH];
-    double bic[NCH], cur[NCH];
+    bool up = false;
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
         hv[q] = act[q] && !((s.absent >> slot[q]) & 1u);
         const int v = ws.slotvar[slot[q]];
         vv[q] = v;
-        idx[q] = table_index<WORLD1>(P, v, s.S);
-        bic[q] = bic_of(P, cx, rss[q], s.Kw);
-        cur[q] = ws.bb[v];
+        off[q] = block_offset<WORLD1>(P, s.S, s.S1, (1u << v) - 1u);
+        rp[q] = ws.rec[slot[q]];
+        bic[q] = bic_of(rss[q], fast_ln(fmax(rss[q], 1e-300), lntab), P.mhalf_n, s.Kw);
+        up |= hv[q] && bic[q] >= ws.bb[v];
     }
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
         if (hv[q]) {
-            if (HR) __stcs(P.out_rss + idx[q], rss[q]);
-            if (HB) __stcs(P.out_bic + idx[q], bic[q]);
+            if (HR) __stcs((double*)rp[q].x + off[q], rss[q]);
+            if (HB) __stcs((double*)rp[q].y + off[q], bic[q]);
         }
-        // running best (a11): the 4 lanes of a column group share child vv[q];
-        // improvements are rare, so resolve them lane by lane (ascending lane id)
-        unsigned bal = __ballot_sync(FULLMASK, hv[q] && bic[q] >= cur[q]);
-        while (bal) {
-            const int l = __ffs(bal) - 1;
-            bal &= bal - 1;
-            if ((int)(threadIdx.x & 31) == l) {
+    }
+    // running best (a11): the 4 lanes of a column group share a child; record
+    // improvements are rare, so they are resolved lane by lane (ascending id)
+    unsigned bal = __ballot_sync(FULLMASK, up);
+    while (bal) {
+        const int l = __ffs(bal) - 1;
+        bal &= bal - 1;
+        if ((int)(threadIdx.x & 31) == l) {
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) {
                 const int v = vv[q];
-                if (tie_better(bic[q], s.S, ws.bb[v], ws.bm[v])) {
+                if (hv[q] && tie_better(bic[q], s.S, ws.bb[v], ws.bm[v])) {
                     ws.bb[v] = bic[q];
                     ws.bm[v] = s.S;
                 }
             }
-            __syncwarp();
         }
+        __syncwarp();
     }
 }
 
@@ -546,42 +596,47 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double2 s_lntab[128];
-    __shared__ double s_Kc[33];
+    __shared__ uint32_t s_item;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
     const int fv0 = p + g;                      // user id of free slot 0
-    const int NCS = m + 1;                      // slot stride; slot m = scratch column
-    __shared__ uint32_t s_item;
     for (int j = threadIdx.x; j < 128; j += blockDim.x) s_lntab[j] = P.lntab[j];
-    for (int j = threadIdx.x; j < 33; j += blockDim.x) s_Kc[j] = P.Kc[j];
     __syncthreads();
-    Ctx cx{s_lntab, s_Kc};
+    int CS, WS;
+    walk_geometry(m, k, CS, WS);
+    const double K0 = P.Kc[0];
+    const double mhlnn = P.Kc[1] - P.Kc[0];     // -(1/2) ln n
     const size_t per = warp_smem_bytes(m, k);
     unsigned char* base = smem_raw + (size_t)wib * per;
+    size_t wbytes = (size_t)4 * WS;
+    {
+        size_t asz = (size_t)(m * (m + 1) / 2) * 8;
+        if ((size_t)3 * WS + asz > wbytes) wbytes = (size_t)3 * WS + asz;
+    }
     WarpSmem ws;
-    ws.A = (double*)base;
-    ws.W = ws.A + (m * (m + 1) / 2);
-    ws.bb = ws.W + (size_t)(2 * k - 1) * NCS * 4;
+    ws.Wb = base;
+    ws.A = (double*)(base + 3 * WS);
+    ws.rec = (ulonglong2*)(base + wbytes);
+    ws.bb = (double*)(ws.rec + 32);
     ws.bm = (uint32_t*)(ws.bb + 32);
     ws.pm = ws.bm + 32;
     ws.posmap = (uint8_t*)(ws.pm + 17);
-    ws.slotvar = ws.posmap + 16;
+    ws.slotvar = ws.posmap + 48;
 
     ws.bb[lane] = -__longlong_as_double(0x7ff0000000000000LL);
     ws.bm[lane] = 0xffffffffu;
-    ws.slotvar[lane] = 0;
-    for (int e = lane; e < (2 * k - 1) * NCS * 4; e += 32) ws.W[e] = 0.0;
     __syncwarp();
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
     const int w = lane & 3;           // worker of this lane within the pack
     const int cl = lane >> 2;         // lane's column group (0..7)
-    const int RS = NCS << 2;          // W row stride (doubles)
     // slots of pack variables in a worker's front set are never harvested
     uint32_t absent = 0;
     if (w >= P.nw) absent = 0xffffffffu;
     else
         for (int j = 0; j < p; ++j)
             if ((w >> j) & 1) absent |= 1u << (k + j);
+    unsigned char* const Wlane = ws.Wb + region_of(w, p) * WS;
+    const int shb = WORLD1 ? m - 1 : m - P.r;   // child block = v << shb entries
 
     for (;;) {
         // one work item = one gang: the CTA's 2^g warps take the 2^g packs that
@@ -593,7 +648,7 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
         if ((int)item >= P.npacks) break;
         const uint32_t pack = P.packs[item] | ((uint32_t)wib << (bh - g));
 
-        // ---- seed: load the depth-L1 node, derive the remaining hi levels (a5)
+        // ---- seed: load the depth-L1 node, derive the remaining tree levels (a5)
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
         const int sn = m - __popc(nid);
         const double* src = P.nodes + (size_t)nid * m * m;
@@ -609,47 +664,48 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
                 for (int j = 0; j < T; ++j) grc_packed(ws.A, sn, org + j, sn, lane);
             }
         }
-        // slot -> user id: free, pack, then hi vars in B (ascending id = latest deferred first)
         uint32_t Fhi = 0;                                   // tree-level vars in F (user ids)
         for (int l = 0; l < bh; ++l)
             if ((pack >> l) & 1u) Fhi |= 1u << (l < bh - g ? m - 1 - l : fv0 - 1 - (l - (bh - g)));
-        if (lane < m) {
-            int v;
+        const int dh = __popc(pack);
+        const int NCSp = k + p + (bh - dh);                 // slots in use for this pack
+        {
+            int v = 0;
             if (lane < k) v = fv0 + lane;
             else if (lane < k + p) v = lane - k;
-            else {
+            else if (lane < NCSp) {
                 // back set: tree-level vars not in F, ascending id (= latest deferred first)
                 int q = lane - k - p, cnt = 0;
-                v = 0;
                 for (int id = p; id < m; ++id) {
                     if (id >= fv0 && id < fv0 + k) continue;
                     if (!((Fhi >> id) & 1u)) { if (cnt == q) { v = id; break; } ++cnt; }
                 }
             }
             ws.slotvar[lane] = (uint8_t)v;
+            ws.rec[lane] = make_ulonglong2(
+                HR ? (unsigned long long)(P.out_rss + ((long long)v << shb)) : 0ull,
+                HB ? (unsigned long long)(P.out_bic + ((long long)v << shb)) : 0ull);
         }
-        if (lane < 16) ws.posmap[lane] = (uint8_t)lane;
+        for (int q = lane; q < 48; q += 32) ws.posmap[q] = (uint8_t)(q < NCSp ? q : 0);
         if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << fv0) : 0u;
-        const int dh = __popc(pack);
-        const int NCSp = k + p + (bh - dh);   // slots in use for this pack
         __syncwarp();
 
         // ---- pack derivation: the 2^p workers' seeds along one GRC path (a5)
         const int o = org, sz = sn, end = sn;
         if (p == 2) {
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 2, 3, Fhi | 3u, dh + 2, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 2, 3, Fhi | 3u, dh + 2, lane, CS, WS, NCSp, K0, mhlnn);
             for (int j = 1; j <= k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
             for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
             for (int j = k; j >= 0; --j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 2, Fhi | 2u, dh + 1, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o + 1, 2, Fhi | 2u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
         } else if (p == 1) {
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
             for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
         } else {
-            snapshot<WORLD1, HR, HB>(P, cx, ws, sz, o, 0, Fhi, dh, lane, NCS, NCSp);
+            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
         }
 
         // ---- the walk: d + Upsilon(k) in lockstep (a6-a11)
@@ -665,28 +721,27 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
             const int X = (int)((perm >> (4 * i)) & 15u);
             const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
             {
-                const uint64_t d = (uint64_t)(X ^ Y);
-                perm ^= (d << (4 * i)) | (d << (4 * (i + 1)));
+                const uint64_t dd = (uint64_t)(X ^ Y);
+                perm ^= (dd << (4 * i)) | (dd << (4 * (i + 1)));
             }
-            const int r0 = i * RS + w;
+            unsigned char* const bi = Wlane + 16 * i;
             double c, sn, h;
-            givens(ws.W[r0 + (Y << 2)], ws.W[r0 + RS + (Y << 2)], c, sn, h);
+            givens(*(const double*)(bi + Y * CS), *(const double*)(bi + Y * CS + 16), c, sn, h);
             const uint32_t T = ws.pm[i] | (1u << (fv0 + Y));
-            const double Kw = cx.Kc[dw + i + 1];
+            const uint32_t S = Fw | T;
+            const double Kw = fma((double)(dw + i + 1), mhlnn, K0);
             __syncwarp();
-            const int nf = k - 1 - i;
-            const int L = nf + NBp;
-            StepCtx sc{r0, RS, c, sn, Fw | T, Kw, X, i, nf, L, cl, m, absent};
+            const int L = (k - 1 - i) + NBp;
+            StepCtx sc{bi, CS, c, sn, S, S >> 1, Kw, X, i, L, cl, absent};
             switch ((L + 7) >> 3) {
-                case 1: walk_chunks<WORLD1, HR, HB, 1>(P, cx, ws, sc); break;
-                case 2: walk_chunks<WORLD1, HR, HB, 2>(P, cx, ws, sc); break;
-                case 3: walk_chunks<WORLD1, HR, HB, 3>(P, cx, ws, sc); break;
-                default: walk_chunks<WORLD1, HR, HB, 4>(P, cx, ws, sc); break;
+                case 1: walk_chunks<WORLD1, HR, HB, 1>(P, s_lntab, ws, sc); break;
+                case 2: walk_chunks<WORLD1, HR, HB, 2>(P, s_lntab, ws, sc); break;
+                case 3: walk_chunks<WORLD1, HR, HB, 3>(P, s_lntab, ws, sc); break;
+                default: walk_chunks<WORLD1, HR, HB, 4>(P, s_lntab, ws, sc); break;
             }
             if (cl == 0) {
-                ws.W[r0 + (Y << 2)] = h;
-                ws.W[r0 + RS + (Y << 2)] = 0.0;
-                if (i >= 1) ws.W[r0 + (k - 1) * RS + (Y << 2)] = 0.0;     // U row i+1
+                *(double2*)(bi + Y * CS) = make_double2(h, 0.0);   // Y now at position i: (h, U_{i+1} = 0)
+                *(double*)(bi + Y * CS + 16) = 0.0;                // R_{i+1} = 0
             }
             if (lane == 0) {
                 ws.posmap[i] = (uint8_t)Y;
