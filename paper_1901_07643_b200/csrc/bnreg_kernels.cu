@@ -444,7 +444,7 @@ __device__ __forceinline__ void harvest_one(const TravParams& P, const double2* 
     const uint32_t lm = (1u << v) - 1u;
     const uint32_t off = block_offset<WORLD1>(P, S, S >> 1, lm);
     const ulonglong2 rp = ws.rec[slot];
-    const double bic = bic_of(rss, fast_ln(fmax(rss, 1e-300), lntab), P.mhalf_n, Kw);
+    const double bic = bic_of(rss, fast_ln(rss, lntab), P.mhalf_n, Kw);
     if (HR) __stcs((double*)rp.x + off, rss);
     if (HB) __stcs((double*)rp.y + off, bic);
     const double cur = ws.bb[v];
@@ -509,45 +509,73 @@ __device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSm
 
 struct StepCtx {
     unsigned char* base;   // this lane's worker region + 16 i (E_i of slot 0)
+    unsigned char* wl;     // this lane's worker region
     int CS;
-    double c, sn;          // the GRC's rotation
+    double c, sn, h;       // the GRC's rotation and the new diagonal
     uint32_t S, S1;        // new prefix set of this worker (user ids), S >> 1
     double Kw;             // BIC constant for |S|
-    int X, i, L, cl;
+    int X, Y, i, L, cl, lane;
     uint32_t absent;       // slots whose variable is in this worker's front set
+    uint32_t T;            // new free prefix mask (for pm)
+    // the next step (software pipelining of the Givens chain)
+    int in, Yn;            // next position / pivot slot (in < 0: none)
 };
 
 // One GRC step over NCH chunks of 8 list entries per worker (list = positions
 // i+1.. of the walk order: the free columns after the swap, then the back
-// columns).  The NCH families of a lane are independent chains (ILP).
+// columns).  Phases: (A) rotate + suffix sums + stores of the state, (B) the
+// NEXT step's Givens coefficients (they only need values (A) just stored),
+// (C) this step's harvest: index, log, BIC, table stores, running best.
+// (B) and (C) are independent, so their dependency chains overlap; within (A)
+// and (C) the NCH families of a lane are independent chains too.
 template <bool WORLD1, bool HR, bool HB, int NCH>
-__device__ __forceinline__ void walk_chunks(const TravParams& P, const double2* lntab, const WarpSmem& ws,
-                                            const StepCtx& s)
+__device__ __forceinline__ void walk_step(const TravParams& P, const double2* lntab, const WarpSmem& ws,
+                                          const StepCtx& s, double& cn, double& snn, double& hn)
 {
     int slot[NCH];
     bool act[NCH];
-    double2 e0[NCH], e1[NCH];
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-        const int e = s.cl + 8 * q;
-        act[q] = e < s.L;
-        slot[q] = (q == 0 && s.cl == 0) ? s.X : (int)ws.posmap[s.i + 1 + e];
-        const unsigned char* col = s.base + slot[q] * s.CS;
-        e0[q] = *(const double2*)col;
-        e1[q] = *(const double2*)(col + 16);
-    }
     double rss[NCH];
+    // ---- (A)
+    {
+        double2 e0[NCH], e1[NCH];
 #pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-        const double xn = fma(s.c, e0[q].x, s.sn * e1[q].x);
-        const double yn = fma(s.c, e1[q].x, -s.sn * e0[q].x);
-        rss[q] = fma(yn, yn, e1[q].y);
-        if (act[q]) {
-            unsigned char* col = s.base + slot[q] * s.CS;
-            *(double2*)col = make_double2(xn, rss[q]);
-            *(double*)(col + 16) = yn;
+        for (int q = 0; q < NCH; ++q) {
+            const int e = s.cl + 8 * q;
+            act[q] = e < s.L;
+            slot[q] = (q == 0 && s.cl == 0) ? s.X : (int)ws.posmap[s.i + 1 + e];
+            const unsigned char* col = s.base + slot[q] * s.CS;
+            e0[q] = *(const double2*)col;
+            e1[q] = *(const double2*)(col + 16);
         }
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) {
+            const double xn = fma(s.c, e0[q].x, s.sn * e1[q].x);
+            const double yn = fma(s.c, e1[q].x, -s.sn * e0[q].x);
+            rss[q] = fma(yn, yn, e1[q].y);
+            if (act[q]) {
+                unsigned char* col = s.base + slot[q] * s.CS;
+                *(double2*)col = make_double2(xn, rss[q]);
+                *(double*)(col + 16) = yn;
+            }
+        }
+        if (s.cl == 0) {
+            unsigned char* col = s.base + s.Y * s.CS;
+            *(double2*)col = make_double2(s.h, 0.0);   // Y now at position i: (h, U_{i+1} = 0)
+            *(double*)(col + 16) = 0.0;                // R_{i+1} = 0
+        }
+        if (s.lane == 0) {
+            ws.posmap[s.i] = (uint8_t)s.Y;
+            ws.posmap[s.i + 1] = (uint8_t)s.X;
+            ws.pm[s.i + 1] = s.T;
+        }
+        __syncwarp();
     }
+    // ---- (B) next step's rotation
+    if (s.in >= 0) {
+        const unsigned char* col = s.wl + 16 * s.in + s.Yn * s.CS;
+        givens(*(const double*)col, *(const double*)(col + 16), cn, snn, hn);
+    }
+    // ---- (C)
     bool hv[NCH];
     double bic[NCH];
     ulonglong2 rp[NCH];
@@ -561,7 +589,7 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const double2* 
         vv[q] = v;
         off[q] = block_offset<WORLD1>(P, s.S, s.S1, (1u << v) - 1u);
         rp[q] = ws.rec[slot[q]];
-        bic[q] = bic_of(rss[q], fast_ln(fmax(rss[q], 1e-300), lntab), P.mhalf_n, s.Kw);
+        bic[q] = bic_of(rss[q], fast_ln(rss[q], lntab), P.mhalf_n, s.Kw);   // rss <= 1e-300: value replaced by +inf
         up |= hv[q] && bic[q] >= ws.bb[v];
     }
 #pragma unroll
@@ -577,7 +605,7 @@ __device__ __forceinline__ void walk_chunks(const TravParams& P, const double2* 
     while (bal) {
         const int l = __ffs(bal) - 1;
         bal &= bal - 1;
-        if ((int)(threadIdx.x & 31) == l) {
+        if (s.lane == l) {
 #pragma unroll
             for (int q = 0; q < NCH; ++q) {
                 const int v = vv[q];
@@ -714,41 +742,44 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
         const int NBp = NCSp - k;
         uint64_t perm = 0;                              // free position -> slot (nibbles)
         for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
-        int iraw = (int)__ldg(P.sched);
+        // step 0's Givens (afterwards each step computes the next one's)
+        int i = (int)__ldg(P.sched) - 1;
+        int X = (int)((perm >> (4 * i)) & 15u);
+        int Y = (int)((perm >> (4 * (i + 1))) & 15u);
+        double c, sg, h;
+        {
+            const unsigned char* col = Wlane + 16 * i + Y * CS;
+            givens(*(const double*)col, *(const double*)(col + 16), c, sg, h);
+        }
         for (int t = 0; t < P.sched_len; ++t) {
-            const int i = iraw - 1;
-            if (t + 1 < P.sched_len) iraw = (int)__ldg(P.sched + t + 1);   // prefetch next
-            const int X = (int)((perm >> (4 * i)) & 15u);
-            const int Y = (int)((perm >> (4 * (i + 1))) & 15u);
             {
                 const uint64_t dd = (uint64_t)(X ^ Y);
                 perm ^= (dd << (4 * i)) | (dd << (4 * (i + 1)));
             }
-            unsigned char* const bi = Wlane + 16 * i;
-            double c, sn, h;
-            givens(*(const double*)(bi + Y * CS), *(const double*)(bi + Y * CS + 16), c, sn, h);
+            int in = -1, Xn = 0, Yn = 0;
+            if (t + 1 < P.sched_len) {
+                in = (int)__ldg(P.sched + t + 1) - 1;
+                Xn = (int)((perm >> (4 * in)) & 15u);
+                Yn = (int)((perm >> (4 * (in + 1))) & 15u);
+            }
             const uint32_t T = ws.pm[i] | (1u << (fv0 + Y));
             const uint32_t S = Fw | T;
             const double Kw = fma((double)(dw + i + 1), mhlnn, K0);
-            __syncwarp();
             const int L = (k - 1 - i) + NBp;
-            StepCtx sc{bi, CS, c, sn, S, S >> 1, Kw, X, i, L, cl, absent};
+            StepCtx sc{Wlane + 16 * i, Wlane, CS, c, sg, h, S, S >> 1, Kw, X, Y, i, L, cl, lane, absent, T, in, Yn};
+            double cn = 1.0, snn = 0.0, hn = 0.0;
             switch ((L + 7) >> 3) {
-                case 1: walk_chunks<WORLD1, HR, HB, 1>(P, s_lntab, ws, sc); break;
-                case 2: walk_chunks<WORLD1, HR, HB, 2>(P, s_lntab, ws, sc); break;
-                case 3: walk_chunks<WORLD1, HR, HB, 3>(P, s_lntab, ws, sc); break;
-                default: walk_chunks<WORLD1, HR, HB, 4>(P, s_lntab, ws, sc); break;
+                case 1: walk_step<WORLD1, HR, HB, 1>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                case 2: walk_step<WORLD1, HR, HB, 2>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                case 3: walk_step<WORLD1, HR, HB, 3>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                default: walk_step<WORLD1, HR, HB, 4>(P, s_lntab, ws, sc, cn, snn, hn); break;
             }
-            if (cl == 0) {
-                *(double2*)(bi + Y * CS) = make_double2(h, 0.0);   // Y now at position i: (h, U_{i+1} = 0)
-                *(double*)(bi + Y * CS + 16) = 0.0;                // R_{i+1} = 0
-            }
-            if (lane == 0) {
-                ws.posmap[i] = (uint8_t)Y;
-                ws.posmap[i + 1] = (uint8_t)X;
-                ws.pm[i + 1] = T;
-            }
-            if (g) __syncthreads();      // the gang's warps write one 128 B line per (child, T)
+            c = cn; sg = snn; h = hn;
+            i = in; X = Xn; Y = Yn;
+            // the gang's warps write one 128 B line per (child, T): keep them
+            // within a few steps of each other (lines complete in L2 long
+            // before eviction) without paying a barrier every step
+            if (g && ((t & 3) == 3 || t + 1 == P.sched_len)) __syncthreads();
             else __syncwarp();
         }
     }
