@@ -51,7 +51,7 @@ struct bnreg {
     double* d_root = nullptr;      // root R (m*m)
     double* d_nodes[2] = {nullptr, nullptr};
     uint32_t* d_packs = nullptr;
-    int8_t* d_sched = nullptr;
+    uint4* d_steps = nullptr;
     unsigned* d_counter = nullptr;
     double* d_part_bic = nullptr;
     uint32_t* d_part_mask = nullptr;
@@ -66,6 +66,7 @@ struct bnreg {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double acc_ms[4] = {0, 0, 0, 0};
     int64_t runs = 0;
+    unsigned long long* dbg = nullptr;
 };
 
 static bnreg_options defaults(const bnreg_options* o)
@@ -83,7 +84,7 @@ static void free_all(bnreg* h)
 {
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
-                    h->d_packs, h->d_sched, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
+                    h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
                     h->d_best_mask, h->d_status, h->d_lntab};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -191,8 +192,11 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_packs, std::max<size_t>(1, P.packs.size()) * sizeof(uint32_t)));
     if (!P.packs.empty())
         CKH(cudaMemcpy(h->d_packs, P.packs.data(), P.packs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CKH(cudaMalloc(&h->d_sched, std::max<size_t>(1, P.sched.size())));
-    if (!P.sched.empty()) CKH(cudaMemcpy(h->d_sched, P.sched.data(), P.sched.size(), cudaMemcpyHostToDevice));
+    {
+        auto recs = step_records(P.k, P.sched);
+        CKH(cudaMalloc(&h->d_steps, recs.size() * sizeof(uint4)));
+        CKH(cudaMemcpy(h->d_steps, recs.data(), recs.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+    }
     CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
     h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
     (void)d.warps_per_cta;
@@ -356,8 +360,17 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.NCS = P.m; T.SA = P.m | 1;
     T.sched_len = (int)P.sched.size();
     if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) T.sched_len = std::min(T.sched_len, atoi(dbg));  // profiling aid
+    T.nsteps = P.k + 1 + T.sched_len;
+    T.dbg = nullptr;
+    if (getenv("BNREG_DEBUG_STEP_CLOCKS")) {   // profiling aid: step phase clocks of warp 0
+        static unsigned long long* dd = nullptr;
+        if (!dd) cudaMalloc(&dd, (1 + 3 * 4000) * sizeof(unsigned long long));
+        cudaMemsetAsync(dd, 0, 8, st);
+        T.dbg = dd;
+        h->dbg = dd;
+    }
     T.npacks = (int)P.packs.size();
-    T.sched = h->d_sched; T.nodes = nodes; T.packs = h->d_packs; T.counter = h->d_counter;
+    T.steps = h->d_steps; T.nodes = nodes; T.packs = h->d_packs; T.counter = h->d_counter;
     T.out_rss = out_rss; T.out_bic = out_bic;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
@@ -393,6 +406,17 @@ bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* b
 {
     bnreg_status s = run_impl(h, out_rss, out_bic, nullptr, nullptr);
     if (s != BNREG_OK) return s;
+    if (h->dbg) {
+        std::vector<unsigned long long> v(1 + 3 * 4000);
+        cudaMemcpy(v.data(), h->dbg, v.size() * 8, cudaMemcpyDeviceToHost);
+        double a = 0, b = 0, n = 0;
+        for (unsigned long long q = 20; q < v[0]; ++q) {
+            a += (double)(v[2 + 3 * q] - v[1 + 3 * q]);
+            b += (double)(v[3 + 3 * q] - v[2 + 3 * q]);
+            n += 1;
+        }
+        fprintf(stderr, "step clocks (warp 0, %g steps): start->A-done %.0f, A-done->end %.0f\n", n, a / n, b / n);
+    }
     const int m = h->plan.m;
     if (best_mask)
         CK(cudaMemcpyAsync(best_mask, h->d_best_mask, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));

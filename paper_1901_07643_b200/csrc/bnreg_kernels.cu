@@ -356,8 +356,6 @@ struct WarpSmem {
     ulonglong2* rec;        // [32] (rss row ptr, bic row ptr)
     double* bb;             // [32]
     uint32_t* bm;           // [32]
-    uint32_t* pm;           // [17] free-prefix masks by prefix length (user ids)
-    uint8_t* posmap;        // [48] walk position -> slot (positions >= NCSp -> 0)
     uint8_t* slotvar;       // [32] slot -> user id
 };
 
@@ -377,7 +375,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int m, int k)
     size_t asz = (size_t)(m * (m + 1) / 2) * 8;
     size_t w = (size_t)4 * WS;
     if ((size_t)3 * WS + asz > w) w = (size_t)3 * WS + asz;
-    size_t tot = w + 32 * 16 + 32 * 8 + 32 * 4 + 17 * 4 + 48 + 32;
+    size_t tot = w + 32 * 16 + 32 * 8 + 32 * 4 + 32;
     return (tot + 15) & ~(size_t)15;
 }
 
@@ -434,33 +432,14 @@ __device__ __forceinline__ int slot_pos(int slot, int w, int k, int p, int nw)
     return k + present + (slot - k - p);
 }
 
-// One family outside the lockstep walk (seed prefixes): stores + running best.
-// The caller guarantees that no other lane touches child v meanwhile.
-template <bool WORLD1, bool HR, bool HB>
-__device__ __forceinline__ void harvest_one(const TravParams& P, const double2* lntab, const WarpSmem& ws,
-                                            int slot, uint32_t S, double Kw, double rss)
-{
-    const int v = ws.slotvar[slot];
-    const uint32_t lm = (1u << v) - 1u;
-    const uint32_t off = block_offset<WORLD1>(P, S, S >> 1, lm);
-    const ulonglong2 rp = ws.rec[slot];
-    const double bic = bic_of(rss, fast_ln(rss, lntab), P.mhalf_n, Kw);
-    if (HR) __stcs((double*)rp.x + off, rss);
-    if (HB) __stcs((double*)rp.y + off, bic);
-    const double cur = ws.bb[v];
-    if (bic >= cur && tie_better(bic, S, cur, ws.bm[v])) {
-        ws.bb[v] = bic;
-        ws.bm[v] = S;
-    }
-}
-
 // Snapshot: convert the sub-triangle of A starting at physical origin `org`
-// (side s) into worker w's walk state and harvest its seed prefixes of sizes
-// d..d+k (reading G11).  Lanes = walk slots.  STAGE: A overlaps this worker's
-// region, so each lane first reads its whole column into registers.
-template <bool WORLD1, bool HR, bool HB, bool STAGE>
-__device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSmem& ws, int s, int org, int w,
-                         uint32_t Fmask, int d, int lane, int CS, int WS, int ncsp, double K0, double mhlnn)
+// (side s) into worker w's walk state (E pairs of its slots).  The seed
+// prefixes are harvested afterwards by the walk's seed pseudo-steps.  Lanes =
+// walk slots.  STAGE: A overlaps this worker's region, so each lane first
+// reads its whole column into registers.
+template <bool STAGE>
+__device__ void snapshot(const TravParams& P, const WarpSmem& ws, int s, int org, int w, int lane, int CS, int WS,
+                         int ncsp)
 {
     const int k = P.k;
     if (w >= P.nw) return;
@@ -485,10 +464,6 @@ __device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSm
                     acc = fma(x, x, acc);
                     if (r < k) E[2 * r] = x;
                     if (r >= 1 && r <= k) E[2 * (r - 1) + 1] = acc;       // U_r
-                    if (r <= k) {
-                        const uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
-                        harvest_one<WORLD1, HR, HB>(P, lntab, ws, slot, S, fma((double)(d + r), mhlnn, K0), acc);
-                    }
                 }
             }
         } else {
@@ -497,10 +472,6 @@ __device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSm
                 acc = fma(x, x, acc);
                 if (r < k) E[2 * r] = x;
                 if (r >= 1 && r <= k) E[2 * (r - 1) + 1] = acc;           // U_r
-                if (r <= k) {
-                    const uint32_t S = Fmask | (((1u << r) - 1u) << (P.p + P.g));
-                    harvest_one<WORLD1, HR, HB>(P, lntab, ws, slot, S, fma((double)(d + r), mhlnn, K0), acc);
-                }
             }
         }
     }
@@ -508,42 +479,56 @@ __device__ void snapshot(const TravParams& P, const double2* lntab, const WarpSm
 }
 
 struct StepCtx {
-    unsigned char* base;   // this lane's worker region + 16 i (E_i of slot 0)
     unsigned char* wl;     // this lane's worker region
     int CS;
     double c, sn, h;       // the GRC's rotation and the new diagonal
     uint32_t S, S1;        // new prefix set of this worker (user ids), S >> 1
     double Kw;             // BIC constant for |S|
-    int X, Y, i, L, cl, lane;
+    int X, Y, i, nf, L, cl, k;
+    uint32_t lo, hi;       // free slots at positions i+1.. (nibbles)
     uint32_t absent;       // slots whose variable is in this worker's front set
-    uint32_t T;            // new free prefix mask (for pm)
-    // the next step (software pipelining of the Givens chain)
-    int in, Yn;            // next position / pivot slot (in < 0: none)
+    int in, Yn;            // next step's position / pivot (in < 0: no Givens needed)
 };
 
-// One GRC step over NCH chunks of 8 list entries per worker (list = positions
-// i+1.. of the walk order: the free columns after the swap, then the back
-// columns).  Phases: (A) rotate + suffix sums + stores of the state, (B) the
-// NEXT step's Givens coefficients (they only need values (A) just stored),
-// (C) this step's harvest: index, log, BIC, table stores, running best.
-// (B) and (C) are independent, so their dependency chains overlap; within (A)
-// and (C) the NCH families of a lane are independent chains too.
-template <bool WORLD1, bool HR, bool HB, int NCH>
+// One lockstep step over NCH chunks of 8 list entries per worker (list = the
+// free slots at positions i+1.., then the back slots).
+//   SEED: a seed pseudo-step harvests prefix j = i+1 of the seed order:
+//         RSS = U_j = E_i.y (U_0 = E_0.x^2 + E_0.y).
+//   else: (A) the GRC at i: rotate rows i, i+1, new suffix sums, store state;
+//   (B) the NEXT step's Givens coefficients (only needs values (A) stored);
+//   (C) this step's harvest: index, log, BIC, table stores, running best.
+//   (B) and (C) are independent chains; so are the NCH families of a lane.
+template <bool WORLD1, bool HR, bool HB, bool SEED, int NCH>
 __device__ __forceinline__ void walk_step(const TravParams& P, const double2* lntab, const WarpSmem& ws,
                                           const StepCtx& s, double& cn, double& snn, double& hn)
 {
     int slot[NCH];
     bool act[NCH];
     double rss[NCH];
-    // ---- (A)
-    {
+    const int sh = 4 * s.cl;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        const int e = s.cl + 8 * q;
+        act[q] = e < s.L;
+        int sl;
+        if (q == 0) sl = (e < s.nf) ? (int)((s.lo >> sh) & 15u) : s.k + e - s.nf;
+        else if (q == 1) sl = (e < s.nf) ? (int)((s.hi >> sh) & 15u) : s.k + e - s.nf;
+        else sl = s.k + e - s.nf;
+        slot[q] = act[q] ? sl : 0;
+    }
+    if (SEED) {
+        const int i0 = s.i < 0 ? 0 : s.i;
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) {
+            const double2 e0 = *(const double2*)(s.wl + slot[q] * s.CS + 16 * i0);
+            rss[q] = (s.i < 0) ? fma(e0.x, e0.x, e0.y) : e0.y;
+        }
+    } else {
+        unsigned char* const base = s.wl + 16 * s.i;
         double2 e0[NCH], e1[NCH];
 #pragma unroll
         for (int q = 0; q < NCH; ++q) {
-            const int e = s.cl + 8 * q;
-            act[q] = e < s.L;
-            slot[q] = (q == 0 && s.cl == 0) ? s.X : (int)ws.posmap[s.i + 1 + e];
-            const unsigned char* col = s.base + slot[q] * s.CS;
+            const unsigned char* col = base + slot[q] * s.CS;
             e0[q] = *(const double2*)col;
             e1[q] = *(const double2*)(col + 16);
         }
@@ -553,23 +538,19 @@ __device__ __forceinline__ void walk_step(const TravParams& P, const double2* ln
             const double yn = fma(s.c, e1[q].x, -s.sn * e0[q].x);
             rss[q] = fma(yn, yn, e1[q].y);
             if (act[q]) {
-                unsigned char* col = s.base + slot[q] * s.CS;
+                unsigned char* col = base + slot[q] * s.CS;
                 *(double2*)col = make_double2(xn, rss[q]);
                 *(double*)(col + 16) = yn;
             }
         }
         if (s.cl == 0) {
-            unsigned char* col = s.base + s.Y * s.CS;
+            unsigned char* col = base + s.Y * s.CS;
             *(double2*)col = make_double2(s.h, 0.0);   // Y now at position i: (h, U_{i+1} = 0)
             *(double*)(col + 16) = 0.0;                // R_{i+1} = 0
         }
-        if (s.lane == 0) {
-            ws.posmap[s.i] = (uint8_t)s.Y;
-            ws.posmap[s.i + 1] = (uint8_t)s.X;
-            ws.pm[s.i + 1] = s.T;
-        }
-        __syncwarp();
     }
+    __syncwarp();
+    if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) P.dbg[2 + 3 * P.dbg[0]] = clock64();
     // ---- (B) next step's rotation
     if (s.in >= 0) {
         const unsigned char* col = s.wl + 16 * s.in + s.Yn * s.CS;
@@ -589,7 +570,7 @@ __device__ __forceinline__ void walk_step(const TravParams& P, const double2* ln
         vv[q] = v;
         off[q] = block_offset<WORLD1>(P, s.S, s.S1, (1u << v) - 1u);
         rp[q] = ws.rec[slot[q]];
-        bic[q] = bic_of(rss[q], fast_ln(rss[q], lntab), P.mhalf_n, s.Kw);   // rss <= 1e-300: value replaced by +inf
+        bic[q] = bic_of(rss[q], fast_ln(rss[q], lntab), P.mhalf_n, s.Kw);   // rss <= 1e-300 -> +inf
         up |= hv[q] && bic[q] >= ws.bb[v];
     }
 #pragma unroll
@@ -605,7 +586,7 @@ __device__ __forceinline__ void walk_step(const TravParams& P, const double2* ln
     while (bal) {
         const int l = __ffs(bal) - 1;
         bal &= bal - 1;
-        if (s.lane == l) {
+        if ((int)(threadIdx.x & 31) == l) {
 #pragma unroll
             for (int q = 0; q < NCH; ++q) {
                 const int v = vv[q];
@@ -647,9 +628,7 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
     ws.rec = (ulonglong2*)(base + wbytes);
     ws.bb = (double*)(ws.rec + 32);
     ws.bm = (uint32_t*)(ws.bb + 32);
-    ws.pm = ws.bm + 32;
-    ws.posmap = (uint8_t*)(ws.pm + 17);
-    ws.slotvar = ws.posmap + 48;
+    ws.slotvar = (uint8_t*)(ws.bm + 32);
 
     ws.bb[lane] = -__longlong_as_double(0x7ff0000000000000LL);
     ws.bm[lane] = 0xffffffffu;
@@ -714,72 +693,71 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
                 HR ? (unsigned long long)(P.out_rss + ((long long)v << shb)) : 0ull,
                 HB ? (unsigned long long)(P.out_bic + ((long long)v << shb)) : 0ull);
         }
-        for (int q = lane; q < 48; q += 32) ws.posmap[q] = (uint8_t)(q < NCSp ? q : 0);
-        if (lane < 17) ws.pm[lane] = (lane <= k) ? (((1u << lane) - 1u) << fv0) : 0u;
         __syncwarp();
 
         // ---- pack derivation: the 2^p workers' seeds along one GRC path (a5)
         const int o = org, sz = sn, end = sn;
         if (p == 2) {
-            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 2, 3, Fhi | 3u, dh + 2, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<false>(P, ws, sz, o + 2, 3, lane, CS, WS, NCSp);
             for (int j = 1; j <= k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<false>(P, ws, sz, o + 1, 1, lane, CS, WS, NCSp);
             for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<false>(P, ws, sz, o, 0, lane, CS, WS, NCSp);
             for (int j = k; j >= 0; --j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o + 1, 2, Fhi | 2u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<true>(P, ws, sz, o + 1, 2, lane, CS, WS, NCSp);
         } else if (p == 1) {
-            snapshot<WORLD1, HR, HB, false>(P, s_lntab, ws, sz, o + 1, 1, Fhi | 1u, dh + 1, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<false>(P, ws, sz, o + 1, 1, lane, CS, WS, NCSp);
             for (int j = 0; j < k; ++j) grc_packed(ws.A, sz, o + j, end, lane);
-            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<true>(P, ws, sz, o, 0, lane, CS, WS, NCSp);
         } else {
-            snapshot<WORLD1, HR, HB, true>(P, s_lntab, ws, sz, o, 0, Fhi, dh, lane, CS, WS, NCSp, K0, mhlnn);
+            snapshot<true>(P, ws, sz, o, 0, lane, CS, WS, NCSp);
         }
 
-        // ---- the walk: d + Upsilon(k) in lockstep (a6-a11)
+        // ---- the walk: k+1 seed pseudo-steps, then d + Upsilon(k), in lockstep (a6-a11)
         const uint32_t Fw = Fhi | (uint32_t)w;          // pack var j = user id j
         const int dw = dh + __popc((uint32_t)w);
         const int NBp = NCSp - k;
-        uint64_t perm = 0;                              // free position -> slot (nibbles)
-        for (int f = 0; f < k; ++f) perm |= (uint64_t)f << (4 * f);
-        // step 0's Givens (afterwards each step computes the next one's)
-        int i = (int)__ldg(P.sched) - 1;
-        int X = (int)((perm >> (4 * i)) & 15u);
-        int Y = (int)((perm >> (4 * (i + 1))) & 15u);
-        double c, sg, h;
-        {
-            const unsigned char* col = Wlane + 16 * i + Y * CS;
-            givens(*(const double*)col, *(const double*)(col + 16), c, sg, h);
-        }
-        for (int t = 0; t < P.sched_len; ++t) {
-            {
-                const uint64_t dd = (uint64_t)(X ^ Y);
-                perm ^= (dd << (4 * i)) | (dd << (4 * (i + 1)));
-            }
-            int in = -1, Xn = 0, Yn = 0;
-            if (t + 1 < P.sched_len) {
-                in = (int)__ldg(P.sched + t + 1) - 1;
-                Xn = (int)((perm >> (4 * in)) & 15u);
-                Yn = (int)((perm >> (4 * (in + 1))) & 15u);
-            }
-            const uint32_t T = ws.pm[i] | (1u << (fv0 + Y));
-            const uint32_t S = Fw | T;
-            const double Kw = fma((double)(dw + i + 1), mhlnn, K0);
-            const int L = (k - 1 - i) + NBp;
-            StepCtx sc{Wlane + 16 * i, Wlane, CS, c, sg, h, S, S >> 1, Kw, X, Y, i, L, cl, lane, absent, T, in, Yn};
+        double c = 1.0, sg = 0.0, h = 0.0;
+        uint4 rec = __ldg(P.steps);
+        for (int t = 0; t < P.nsteps; ++t) {
+            const uint4 nrec = (t + 1 < P.nsteps) ? __ldg(P.steps + t + 1) : make_uint4(1u << 18, 0, 0, 0);
+            const int i = (int)(rec.x & 31u) - 1;
+            const bool seed = (rec.x >> 18) & 1u;
+            const int nf = (int)((rec.x >> 13) & 31u);
+            const int L = nf + NBp;
+            const uint32_t S = Fw | (rec.y << fv0);
+            const bool nreal = !((nrec.x >> 18) & 1u);
+            StepCtx sc{Wlane, CS, c, sg, h, S, S >> 1, fma((double)(dw + i + 1), mhlnn, K0),
+                       (int)((rec.x >> 5) & 15u), (int)((rec.x >> 9) & 15u), i, nf, L, cl, k, rec.z, rec.w, absent,
+                       nreal ? (int)(nrec.x & 31u) - 1 : -1, (int)((nrec.x >> 9) & 15u)};
             double cn = 1.0, snn = 0.0, hn = 0.0;
-            switch ((L + 7) >> 3) {
-                case 1: walk_step<WORLD1, HR, HB, 1>(P, s_lntab, ws, sc, cn, snn, hn); break;
-                case 2: walk_step<WORLD1, HR, HB, 2>(P, s_lntab, ws, sc, cn, snn, hn); break;
-                case 3: walk_step<WORLD1, HR, HB, 3>(P, s_lntab, ws, sc, cn, snn, hn); break;
-                default: walk_step<WORLD1, HR, HB, 4>(P, s_lntab, ws, sc, cn, snn, hn); break;
+            const int nch = (L + 7) >> 3;
+            if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) P.dbg[1 + 3 * P.dbg[0]] = clock64();
+            if (seed) {
+                switch (nch) {
+                    case 1: walk_step<WORLD1, HR, HB, true, 1>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    case 2: walk_step<WORLD1, HR, HB, true, 2>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    case 3: walk_step<WORLD1, HR, HB, true, 3>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    default: walk_step<WORLD1, HR, HB, true, 4>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                }
+            } else {
+                switch (nch) {
+                    case 1: walk_step<WORLD1, HR, HB, false, 1>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    case 2: walk_step<WORLD1, HR, HB, false, 2>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    case 3: walk_step<WORLD1, HR, HB, false, 3>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                    default: walk_step<WORLD1, HR, HB, false, 4>(P, s_lntab, ws, sc, cn, snn, hn); break;
+                }
+            }
+            if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) {
+                P.dbg[3 + 3 * P.dbg[0]] = clock64();
+                P.dbg[0] += 1;
             }
             c = cn; sg = snn; h = hn;
-            i = in; X = Xn; Y = Yn;
+            rec = nrec;
             // the gang's warps write one 128 B line per (child, T): keep them
             // within a few steps of each other (lines complete in L2 long
             // before eviction) without paying a barrier every step
-            if (g && ((t & 3) == 3 || t + 1 == P.sched_len)) __syncthreads();
+            if (g && ((t & 3) == 3 || t + 1 == P.nsteps)) __syncthreads();
             else __syncwarp();
         }
     }

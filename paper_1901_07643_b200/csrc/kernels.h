@@ -14,7 +14,8 @@ struct TravParams {
     int sched_len;
     int npacks;
     int world1;                 // 1: single rank, identity table layout
-    const int8_t* sched;        // Upsilon(k), 1-based swap positions
+    const uint4* steps;         // step records (plan.h StepRec): k+1 seed steps, then Upsilon(k)
+    int nsteps;
     const double* nodes;        // seed-tree nodes at depth L1, m*m doubles each
     const uint32_t* packs;      // this rank's work items = gang base pack ids (costliest first)
     unsigned int* counter;      // work-queue counter (zeroed before launch)
@@ -27,6 +28,7 @@ struct TravParams {
     double Kc[33];              // BIC constant per parent-set size
     int r;                      // rank-selector bits (world > 1)
     unsigned patlo;             // smaller selector pattern of this rank (non-selector children)
+    unsigned long long* dbg;    // profiling aid (BNREG_DEBUG_STEP_CLOCKS): per-step clock64 stamps, or nullptr
 };
 
 // smem bytes per warp of the traversal kernel

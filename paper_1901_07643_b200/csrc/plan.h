@@ -55,6 +55,54 @@ inline std::vector<int8_t> greedy_swaps(int m)
     return s;
 }
 
+// One record per lockstep step of a worker's walk (host-built, identical for
+// every worker since all of them run Upsilon(k) on their free block):
+//   seed pseudo-steps j = 0..k: harvest the seed prefix {free 0..j-1}
+//     (reading G11: prefixes of sizes d..d+k), no rotation;
+//   real steps t: the GRC at free position i = Upsilon(k)[t] - 1, which swaps
+//     free slots X (position i) and Y (position i+1).
+// meta: bits 0-4 = i + 1 (seed j: i = j - 1), 5-8 = X, 9-12 = Y, 13-17 = nf
+// (free children after the prefix), bit 18 = seed.  T = free-slot mask of the
+// new prefix set.  (lo, hi) = nibbles of the free slots at positions i+1.. .
+struct StepRec {
+    uint32_t meta, T, lo, hi;
+};
+
+inline std::vector<StepRec> step_records(int k, const std::vector<int8_t>& sched)
+{
+    std::vector<StepRec> out;
+    std::vector<int> perm(k);
+    for (int f = 0; f < k; ++f) perm[f] = f;
+    auto list_of = [&](int from, StepRec& r) {
+        uint64_t nib = 0;
+        for (int pos = from, e = 0; pos < k; ++pos, ++e) nib |= (uint64_t)perm[pos] << (4 * e);
+        r.lo = (uint32_t)nib;
+        r.hi = (uint32_t)(nib >> 32);
+    };
+    for (int j = 0; j <= k; ++j) {
+        StepRec r{};
+        const int i = j - 1, nf = k - j;
+        r.meta = (uint32_t)(i + 1) | ((uint32_t)nf << 13) | (1u << 18);
+        r.T = (uint32_t)((1u << j) - 1u);
+        list_of(j, r);
+        out.push_back(r);
+    }
+    for (int8_t s1 : sched) {
+        const int i = s1 - 1;
+        const int X = perm[i], Y = perm[i + 1];
+        std::swap(perm[i], perm[i + 1]);
+        StepRec r{};
+        const int nf = k - 1 - i;
+        r.meta = (uint32_t)(i + 1) | ((uint32_t)X << 5) | ((uint32_t)Y << 9) | ((uint32_t)nf << 13);
+        uint32_t T = 0;
+        for (int q = 0; q <= i; ++q) T |= 1u << perm[q];
+        r.T = T;
+        list_of(i + 1, r);
+        out.push_back(r);
+    }
+    return out;
+}
+
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
     int g = 0;                                // gang bits (the top g of the bh tree bits)
