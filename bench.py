@@ -139,7 +139,8 @@ def oracle_rate(X, seconds, seed=1234, batch=256):
     import oracle
     n, m = X.shape
     Xc = oracle.centre(X)
-    idx = datagen.sample_indices(m, 200000, seed)
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.integers(0, m << (m - 1), size=2_000_000)).astype(np.int64)
     done, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds and done < len(idx):
         oracle.rss_indices(Xc, idx[done:done + batch])
