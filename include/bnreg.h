@@ -123,6 +123,12 @@ bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev);
  * number of ranges (<= 2m); starts/lens (capacity 2m) receive them in order. */
 bnreg_status bnreg_shard_ranges(const bnreg_t* h, int64_t* count, int64_t* starts, int64_t* lens);
 
+/* Host-only equivalents for a plan (no GPU, no handle): the shard ranges and
+ * the rank-local offset of a global index (-1 if another rank owns it). */
+bnreg_status bnreg_plan_shard_ranges(int32_t m, int64_t n, const bnreg_options* opt, int64_t* count, int64_t* starts,
+                                     int64_t* lens);
+int64_t bnreg_plan_local_index(int32_t m, int64_t n, const bnreg_options* opt, int64_t global_index);
+
 /* Deterministic merge of per-rank bests (step a11 after the all-gather):
  * masks/bics are nparts x m row-major HOST arrays. */
 bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, const double* bics,

@@ -26,7 +26,7 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
            "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
-           "bnreg_shard_ranges", "bnreg_best_merge", "bnreg_timing", "bnreg_plan_query",
+           "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_plan_query",
            "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_last_error", "bnreg_destroy"]
 
 
@@ -77,6 +77,8 @@ def lib():
         "bnreg_get_root_device": ([H, P], i32),
         "bnreg_set_root_device": ([H, P], i32),
         "bnreg_shard_ranges": ([H, P, P, P], i32),
+        "bnreg_plan_shard_ranges": ([i32, i64, POPT, P, P, P], i32),
+        "bnreg_plan_local_index": ([i32, i64, POPT, i64], i64),
         "bnreg_best_merge": ([i32, i32, P, P, P, P], i32),
         "bnreg_timing": ([H, i32, P, P], i32),
         "bnreg_plan_query": ([i32, i64, POPT, P], i32),
@@ -141,6 +143,19 @@ def bnreg_plan_packs(m: int, n: int, opt: Options | None = None) -> np.ndarray:
     out = np.zeros(cnt, dtype=np.uint32)
     lib().bnreg_plan_packs(m, n, o, _hptr(out), cnt)
     return out
+
+
+def bnreg_plan_shard_ranges(m: int, n: int, opt: Options | None = None):
+    cnt = ctypes.c_int64(0)
+    starts = np.zeros(2 * m, dtype=np.int64)
+    lens = np.zeros(2 * m, dtype=np.int64)
+    _check(lib().bnreg_plan_shard_ranges(m, n, ctypes.byref(opt) if opt else None, ctypes.byref(cnt),
+                                         _hptr(starts), _hptr(lens)))
+    return starts[:cnt.value].copy(), lens[:cnt.value].copy()
+
+
+def bnreg_plan_local_index(m: int, n: int, opt: Options | None, g: int) -> int:
+    return lib().bnreg_plan_local_index(m, n, ctypes.byref(opt) if opt else None, g)
 
 
 def bnreg_best_merge(m: int, masks: np.ndarray, bics: np.ndarray):

@@ -315,10 +315,44 @@ int64_t bnreg_local_index(const bnreg_t* h, int64_t g)
     return local_index(h->plan, g);
 }
 
+static void shard_ranges_of(const Plan& P, int64_t* count, int64_t* starts, int64_t* lens);
+
 bnreg_status bnreg_shard_ranges(const bnreg_t* h, int64_t* count, int64_t* starts, int64_t* lens)
 {
     if (!h || !count) return fail(BNREG_E_INVAL, "NULL argument");
-    const Plan& P = h->plan;
+    shard_ranges_of(h->plan, count, starts, lens);
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_plan_shard_ranges(int32_t m, int64_t n, const bnreg_options* o, int64_t* count, int64_t* starts,
+                                     int64_t* lens)
+{
+    if (!count) return fail(BNREG_E_INVAL, "NULL argument");
+    bnreg_options d = defaults(o);
+    try {
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        shard_ranges_of(P, count, starts, lens);
+    } catch (std::exception& e) {
+        return fail(BNREG_E_INVAL, e.what());
+    }
+    return BNREG_OK;
+}
+
+int64_t bnreg_plan_local_index(int32_t m, int64_t n, const bnreg_options* o, int64_t g)
+{
+    bnreg_options d = defaults(o);
+    try {
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        if (g < 0 || g >= P.total_families) return -1;
+        return local_index(P, g);
+    } catch (std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+static void shard_ranges_of(const Plan& P, int64_t* count, int64_t* starts, int64_t* lens)
+{
     std::vector<std::pair<int64_t, int64_t>> r;
     for (int v = 0; v < P.m; ++v) {
         int64_t cb = (int64_t)v << (P.m - 1);
@@ -336,7 +370,6 @@ bnreg_status bnreg_shard_ranges(const bnreg_t* h, int64_t* count, int64_t* start
         if (starts) starts[i] = r[i].first;
         if (lens) lens[i] = r[i].second;
     }
-    return BNREG_OK;
 }
 
 static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev)
