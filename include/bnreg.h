@@ -53,7 +53,7 @@ typedef enum {
 
 typedef struct {
     int32_t free_vars;        /* k, the free block each worker permutes with Upsilon(k);
-                                 0 = auto (min(m, 8)); 2 <= k <= min(m, 16)              */
+                                 0 = auto (min(m, 9)); 2 <= k <= min(m, 16)              */
     int32_t levels_in_warp;   /* seed-tree levels each warp derives itself; -1 = auto (4) */
     int32_t world;            /* ranks sharing the walk (power of two); 0 or 1 = single */
     int32_t rank;             /* this rank, 0 <= rank < world                             */

@@ -550,7 +550,9 @@ __device__ __forceinline__ void walk_step(const TravParams& P, const double2* ln
         }
     }
     __syncwarp();
+#ifdef BNREG_STEP_CLOCKS
     if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) P.dbg[2 + 3 * P.dbg[0]] = clock64();
+#endif
     // ---- (B) next step's rotation
     if (s.in >= 0) {
         const unsigned char* col = s.wl + 16 * s.in + s.Yn * s.CS;
@@ -659,9 +661,22 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
         const int sn = m - __popc(nid);
         const double* src = P.nodes + (size_t)nid * m * m;
-        for (int r = 0; r < sn; ++r)
-            for (int c = r + lane; c < sn; c += 32) ws.A[poff(r, sn) + c - r] = src[r * m + c];
-        __syncwarp();
+        {
+            // all loads in flight at once (the node comes from HBM/L2): cp.async 8 B per entry
+            const int tot = sn * (sn + 1) / 2;
+            for (int e = lane; e < tot; e += 32) {
+                // packed index e -> (r, c): row r starts at poff(r, sn)
+                int r = (int)((2.0f * sn + 1.0f - sqrtf((2.0f * sn + 1.0f) * (2.0f * sn + 1.0f) - 8.0f * e)) * 0.5f);
+                if (r < 0) r = 0;
+                while (r > 0 && poff(r, sn) > e) --r;
+                while (r + 1 < sn && poff(r + 1, sn) <= e) ++r;
+                const int c = r + (e - poff(r, sn));
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(ws.A + e);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa), "l"(src + r * m + c));
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+        }
         int org = 0;
         for (int l = P.L1; l < bh; ++l) {
             if ((pack >> l) & 1u) {
@@ -732,7 +747,9 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
                        nreal ? (int)(nrec.x & 31u) - 1 : -1, (int)((nrec.x >> 9) & 15u)};
             double cn = 1.0, snn = 0.0, hn = 0.0;
             const int nch = (L + 7) >> 3;
+#ifdef BNREG_STEP_CLOCKS
             if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) P.dbg[1 + 3 * P.dbg[0]] = clock64();
+#endif
             if (seed) {
                 switch (nch) {
                     case 1: walk_step<WORLD1, HR, HB, true, 1>(P, s_lntab, ws, sc, cn, snn, hn); break;
@@ -748,10 +765,12 @@ __global__ void __launch_bounds__(128) traverse_kernel(const __grid_constant__ T
                     default: walk_step<WORLD1, HR, HB, false, 4>(P, s_lntab, ws, sc, cn, snn, hn); break;
                 }
             }
+#ifdef BNREG_STEP_CLOCKS
             if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0 && P.dbg[0] < 4000) {
                 P.dbg[3 + 3 * P.dbg[0]] = clock64();
                 P.dbg[0] += 1;
             }
+#endif
             c = cn; sg = snn; h = hn;
             rec = nrec;
             // the gang's warps write one 128 B line per (child, T): keep them

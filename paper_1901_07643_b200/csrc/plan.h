@@ -151,7 +151,8 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (n < m + 1) throw std::invalid_argument("need n >= m + 1");
     if (world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
         throw std::invalid_argument("world must be a power of two and 0 <= rank < world");
-    if (k <= 0) k = std::min(m, 8);
+    // k = 9: the column stride is (k|1) 16 B, so k = 8 and k = 9 take the same shared memory
+    if (k <= 0) k = std::min(m, 9);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.p = std::min(kPackBits, P.b);
