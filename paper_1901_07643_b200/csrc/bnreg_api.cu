@@ -204,7 +204,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     int64_t want = (int64_t)h->num_sms * per_sm;
     int64_t need = (int64_t)P.packs.size();
     h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
-    size_t gw = (size_t)h->grid_ctas * h->wpc;
+    size_t gw = (size_t)h->grid_ctas * h->wpc * traverse_warps_per_cta_factor();
     CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
     CKH(cudaMalloc(&h->d_part_mask, gw * m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
@@ -415,7 +415,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
     CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
-    CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->grid_ctas * h->wpc, P.m,
+    CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->grid_ctas * h->wpc * traverse_warps_per_cta_factor(), P.m,
                           bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask, st));
     if (h->timing) CK(cudaEventRecord(h->ev[3], st));
     return BNREG_OK;

@@ -42,6 +42,7 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
                               cudaStream_t st);
 cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st);
 int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta);
+int traverse_warps_per_cta_factor();   // warps per gang pack (2 with warp specialisation)
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st);
 
