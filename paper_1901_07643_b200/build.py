@@ -7,8 +7,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu"]
-HEADERS = ["plan.h", "kernels.h"]
+SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu", "walk_kernel.cu"]
+HEADERS = ["plan.h", "kernels.h", "device.cuh"]
 OUT = os.path.join(HERE, "libbnreg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -67,6 +67,14 @@ struct bnreg {
     double acc_ms[4] = {0, 0, 0, 0};
     int64_t runs = 0;
     unsigned long long* dbg = nullptr;
+    // walk kernel: one launch per shared-memory class of work items
+    struct WalkClass {
+        int begin, end, S_alloc, grid, part_base;
+    };
+    std::vector<WalkClass> classes;
+    int nparts = 0;                // rows of d_part_bic / d_part_mask
+    unsigned* d_counters = nullptr;
+    int bar_every = 1;
 };
 
 static bnreg_options defaults(const bnreg_options* o)
@@ -85,7 +93,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab};
+                    h->d_best_mask, h->d_status, h->d_lntab, h->d_counters};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -200,13 +208,53 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
     h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
     (void)d.warps_per_cta;
-    int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
-    int64_t want = (int64_t)h->num_sms * per_sm;
-    int64_t need = (int64_t)P.packs.size();
-    h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
-    size_t gw = (size_t)h->grid_ctas * h->wpc * traverse_warps_per_cta_factor();
+    if (P.variant == 0) {
+        // walk kernel: items are sorted costliest first = most walk slots first
+        // (a gang's slots: m - |F among its tree levels|); consecutive items with
+        // the same occupancy share a launch sized for the first (largest) one
+        const int gs = P.bh - P.g;
+        int64_t i0 = 0;
+        const int64_t ni = (int64_t)P.packs.size();
+        while (i0 < ni) {
+            const int S0 = m - popc(P.packs[i0] & ((1u << gs) - 1u));
+            int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, P.world == 1);
+            if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory"));
+            int64_t i1 = i0 + 1;
+            while (i1 < ni) {
+                const int S1 = m - popc(P.packs[i1] & ((1u << gs) - 1u));
+                const int o1 = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S1, P.g, P.world == 1);
+                if (o1 != occ) break;
+                ++i1;
+            }
+            bnreg::WalkClass c;
+            c.begin = (int)i0; c.end = (int)i1; c.S_alloc = S0;
+            c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * occ, i1 - i0));
+            c.part_base = h->nparts;
+            h->nparts += c.grid * h->wpc;
+            h->classes.push_back(c);
+            i0 = i1;
+        }
+        if (h->classes.empty()) {            // no work items (cannot happen for m >= 2): keep the reduce well-defined
+            h->nparts = 1;
+        }
+        CKH(cudaMalloc(&h->d_counters, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned)));
+        if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(1, atoi(be));
+    } else {
+        int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
+        int64_t want = (int64_t)h->num_sms * per_sm;
+        int64_t need = (int64_t)P.packs.size();
+        h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
+        h->nparts = h->grid_ctas * h->wpc * traverse_warps_per_cta_factor();
+    }
+    size_t gw = (size_t)h->nparts;
     CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
     CKH(cudaMalloc(&h->d_part_mask, gw * m * sizeof(uint32_t)));
+    if (P.variant == 0 && h->classes.empty()) {
+        std::vector<double> nb(m, -INFINITY);
+        std::vector<uint32_t> nm(m, 0xffffffffu);
+        CKH(cudaMemcpy(h->d_part_bic, nb.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+        CKH(cudaMemcpy(h->d_part_mask, nm.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
     CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
     CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
@@ -412,10 +460,25 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
     T.r = P.r;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
-    CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
-    CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
+    if (P.variant == 0) {
+        T.nw = 1 << P.p;
+        T.bar_every = h->bar_every;
+        CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
+        for (size_t c = 0; c < h->classes.size(); ++c) {
+            const auto& C = h->classes[c];
+            T.counter = h->d_counters + c;
+            T.S_alloc = C.S_alloc;
+            T.item_begin = C.begin;
+            T.item_end = C.end;
+            T.part_base = C.part_base;
+            CK(launch_walk(T, C.grid, st));
+        }
+    } else {
+        CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
+        CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
+    }
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
-    CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->grid_ctas * h->wpc * traverse_warps_per_cta_factor(), P.m,
+    CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->nparts, P.m,
                           bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask, st));
     if (h->timing) CK(cudaEventRecord(h->ev[3], st));
     return BNREG_OK;

@@ -27,36 +27,9 @@
 #include <cmath>
 #include <cstdlib>
 #include "kernels.h"
+#include "device.cuh"
 
 namespace bnr {
-
-#define FULLMASK 0xffffffffu
-
-__device__ __forceinline__ double warp_sum(double v)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-    return v;
-}
-
-// Givens coefficients for the GRC (Eq.4 read with G1).  h2 == 0 can only
-// happen on rank-deficient data (rejected at create); identity then.
-__device__ __forceinline__ void givens(double a, double b, double& c, double& s, double& h)
-{
-    const double h2 = fma(a, a, b * b);
-    // 1/sqrt(h2): hardware approximation + two Newton steps (no special-case
-    // branches: h2 is a positive normal number unless the data is rank deficient)
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
-    double e = fma(-h2, y * y, 1.0);
-    y = fma(0.5 * y, e, y);
-    e = fma(-h2, y * y, 1.0);
-    y = fma(0.5 * y, e, y);
-    const bool ok = h2 > 0.0;
-    c = ok ? a * y : 1.0;
-    s = ok ? b * y : 0.0;
-    h = ok ? h2 * y : 0.0;
-}
 
 // ---------------------------------------------------------------- a1 centre
 // grid = m CTAs (root position j), 256 threads.  Xr is column-major n x m in
@@ -273,69 +246,6 @@ __global__ void __launch_bounds__(128) tree_level_kernel(const double* __restric
     }
 }
 
-// ---------------------------------------------------------------- a5-a11 traversal
-// Constants of the fast log (constant bank: usable as DFMA operands directly).
-__constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, -1.0 / 6.0, 0.2,
-                               6.93147180369123816490e-01,   // ln2 hi (exact products e * hi for |e| < 2^11)
-                               1.90821492927058770002e-10,   // ln2 lo
-                               0.0};
-
-// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 7 bits of
-// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/128) (host,
-// long double); u = f r_j - 1 (|u| <= 3.9e-3);  ln x = e ln2 + (-ln r_j) + log1p(u),
-// log1p(u) = u q(u) with q the degree-5 Taylor polynomial (Estrin form;
-// truncation u^7/7 < 2e-18).  Absolute error ~1e-15 for normal x.
-__device__ __forceinline__ double fast_ln(double x, const double2* tab)
-{
-    const int hi = __double2hiint(x), lo = __double2loint(x);
-    const int e = (hi >> 20) - 1023;
-    const int j = (hi >> 13) & 127;
-    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 t = tab[j];
-    const double ed = (double)e;
-    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], t.y));
-    const double u = fma(f, t.x, -1.0);
-    const double u2 = u * u;
-    const double a = fma(u, c_ln[0], 1.0);
-    const double b = fma(u, c_ln[1], c_ln[2]);
-    const double c = fma(u, c_ln[3], c_ln[4]);
-    const double q = fma(u2, fma(u2, c, b), a);
-    return fma(u, q, base);
-}
-
-__device__ __forceinline__ int Ridx(int r, int slot, int w, int NCS) { return ((r * NCS + slot) << 2) + w; }
-
-// Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
-__device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
-
-// GRC on the packed triangle (the same operation as grc_square).
-__device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int lane)
-{
-    const int oJ = poff(J, s), oJ1 = poff(J + 1, s);
-    double a = A[oJ + 1];
-    double b = A[oJ1];
-    double rjj = A[oJ];
-    double c, sn, h;
-    givens(a, b, c, sn, h);
-    __syncwarp();
-    const int q = lane;
-    if (q < J) {
-        const int oq = poff(q, s);
-        double t0 = A[oq + J - q], t1 = A[oq + J + 1 - q];
-        A[oq + J - q] = t1;
-        A[oq + J + 1 - q] = t0;
-    } else if (q == J) {
-        A[oJ] = h;
-        A[oJ + 1] = c * rjj;
-        A[oJ1] = -sn * rjj;
-    } else if (q >= J + 2 && q < end) {
-        double x = A[oJ + q - J], y = A[oJ1 + q - J - 1];
-        A[oJ + q - J] = fma(c, x, sn * y);
-        A[oJ1 + q - J - 1] = fma(c, y, -sn * x);
-    }
-    __syncwarp();
-}
-
 // ---------------------------------------------------------------- walk state layout
 // Per warp (one pack = 4 workers w):
 //   W[w]  column-contiguous walk state, for every slot s (a column of the
@@ -387,35 +297,6 @@ __device__ __forceinline__ int region_of(int w, int p)
 {
     const int last = (p == 2) ? 2 : 0;
     return w == last ? 3 : (w < last ? w : w - 1);
-}
-
-__device__ __forceinline__ double bic_of(double rss, double lnr, double mhalf_n, double Kw)
-{
-    const double bic = fma(mhalf_n, lnr, Kw);
-    return rss > 1e-300 ? bic : __longlong_as_double(0x7ff0000000000000LL);
-}
-
-__device__ __forceinline__ bool tie_better(double b, uint32_t S, double cb, uint32_t cm)
-{
-    if (b != cb) return b > cb;
-    const int s1 = __popc(S), s2 = __popc(cm);
-    return s1 != s2 ? s1 < s2 : S < cm;
-}
-
-// Offset (in entries) of family (v, S) inside child v's block of this rank's
-// table, given lm = (1 << v) - 1: compress(S, v) is the bitwise select
-// lm ? S : S >> 1 (bit v of S is 0).  World 1: the block is v 2^(m-1).. and
-// the offset is the compressed mask; otherwise (plan.h) child v's 2^(m-r)
-// entries hold the masks whose top selector bits match this rank's patterns.
-template <bool WORLD1>
-__device__ __forceinline__ uint32_t block_offset(const TravParams& P, uint32_t S, uint32_t S1, uint32_t lm)
-{
-    const uint32_t cpr = (S & lm) | (S1 & ~lm);
-    if (WORLD1) return cpr;
-    const int v = __popc(lm);
-    const bool sel = v >= P.m - P.r;
-    const int sh = sel ? P.m - P.r : P.m - 1 - P.r;
-    return (cpr & ((1u << sh) - 1u)) + ((!sel && (cpr >> sh) != P.patlo) ? (1u << sh) : 0u);
 }
 
 // Logical position (relative to the snapshot origin) of a walk slot for worker
@@ -1119,15 +1000,6 @@ cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2
 // ---------------------------------------------------------------- a11 best reduce
 // One CTA per child: strided scan over the per-warp partials, then a fixed
 // tree reduction -> deterministic.
-__device__ __forceinline__ bool better(double b1, uint32_t m1, double b2, uint32_t m2)
-{
-    if (m1 == 0xffffffffu) return false;
-    if (m2 == 0xffffffffu) return true;
-    if (b1 != b2) return b1 > b2;
-    int s1 = __popc(m1), s2 = __popc(m2);
-    return s1 != s2 ? s1 < s2 : m1 < m2;
-}
-
 __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restrict__ part_bic,
                                                           const uint32_t* __restrict__ part_mask, int nparts, int m,
                                                           double* best_bic, uint32_t* best_mask)

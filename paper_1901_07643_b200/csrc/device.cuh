@@ -1,0 +1,143 @@
+// device.cuh -- device helpers shared by the sm_100a kernels: the Givens
+// coefficients of a GRC (Eq.4 with reading G1), the fast fp64
+// log of the BIC (a9, reading G5), the packed-triangle GRC used by the seed
+// derivation (a5), the BIC/tie-break rules (G13, G14) and the table index
+// (a10).
+#pragma once
+#include <cstdint>
+#include <cmath>
+#include "kernels.h"
+
+namespace bnr {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+// Givens coefficients for the GRC (Eq.4 read with G1).  h2 == 0 can only
+// happen on rank-deficient data (rejected at create); identity then.
+__device__ __forceinline__ void givens(double a, double b, double& c, double& s, double& h)
+{
+    const double h2 = fma(a, a, b * b);
+    // 1/sqrt(h2): hardware approximation + two Newton steps (no special-case
+    // branches: h2 is a positive normal number unless the data is rank deficient)
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+    double e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    const bool ok = h2 > 0.0;
+    c = ok ? a * y : 1.0;
+    s = ok ? b * y : 0.0;
+    h = ok ? h2 * y : 0.0;
+}
+
+// Constants of the fast log (constant bank: usable as DFMA operands directly).
+static __constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, -1.0 / 6.0, 0.2,
+                               6.93147180369123816490e-01,   // ln2 hi (exact products e * hi for |e| < 2^11)
+                               1.90821492927058770002e-10,   // ln2 lo
+                               0.0};
+
+// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 7 bits of
+// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/128) (host,
+// long double); u = f r_j - 1 (|u| <= 3.9e-3);  ln x = e ln2 + (-ln r_j) + log1p(u),
+// log1p(u) = u q(u) with q the degree-5 Taylor polynomial (Estrin form;
+// truncation u^7/7 < 2e-18).  Absolute error ~1e-15 for normal x.
+__device__ __forceinline__ double fast_ln(double x, const double2* tab)
+{
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) - 1023;
+    const int j = (hi >> 13) & 127;
+    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 t = tab[j];
+    const double ed = (double)e;
+    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], t.y));
+    const double u = fma(f, t.x, -1.0);
+    const double u2 = u * u;
+    const double a = fma(u, c_ln[0], 1.0);
+    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double c = fma(u, c_ln[3], c_ln[4]);
+    const double q = fma(u2, fma(u2, c, b), a);
+    return fma(u, q, base);
+}
+
+// Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
+__device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
+
+// GRC on the packed triangle: swap (physical) columns J, J+1
+// and restore the triangle with one rotation of rows J, J+1.  Warp-collective,
+// lane = column for the rotation (columns J+2..end-1), lane = row for the swap.
+__device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int lane)
+{
+    const int oJ = poff(J, s), oJ1 = poff(J + 1, s);
+    double a = A[oJ + 1];
+    double b = A[oJ1];
+    double rjj = A[oJ];
+    double c, sn, h;
+    givens(a, b, c, sn, h);
+    __syncwarp();
+    const int q = lane;
+    if (q < J) {
+        const int oq = poff(q, s);
+        double t0 = A[oq + J - q], t1 = A[oq + J + 1 - q];
+        A[oq + J - q] = t1;
+        A[oq + J + 1 - q] = t0;
+    } else if (q == J) {
+        A[oJ] = h;
+        A[oJ + 1] = c * rjj;
+        A[oJ1] = -sn * rjj;
+    } else if (q >= J + 2 && q < end) {
+        double x = A[oJ + q - J], y = A[oJ1 + q - J - 1];
+        A[oJ + q - J] = fma(c, x, sn * y);
+        A[oJ1 + q - J - 1] = fma(c, y, -sn * x);
+    }
+    __syncwarp();
+}
+
+// BIC (reading G5): -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi) - (|S|/2) ln n
+//   = mhalf_n * ln RSS + K(|S|);  +inf for RSS <= 1e-300 (G13).
+__device__ __forceinline__ double bic_of(double rss, double lnr, double mhalf_n, double Kw)
+{
+    const double bic = fma(mhalf_n, lnr, Kw);
+    return rss > 1e-300 ? bic : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+// Argmax tie-break (G14): larger BIC, then smaller |S|, then smaller mask.
+__device__ __forceinline__ bool tie_better(double b, uint32_t S, double cb, uint32_t cm)
+{
+    if (b != cb) return b > cb;
+    const int s1 = __popc(S), s2 = __popc(cm);
+    return s1 != s2 ? s1 < s2 : S < cm;
+}
+
+// Same rule for (BIC, mask) candidates where mask 0xffffffff means "none".
+__device__ __forceinline__ bool better(double b1, uint32_t m1, double b2, uint32_t m2)
+{
+    if (m1 == 0xffffffffu) return false;
+    if (m2 == 0xffffffffu) return true;
+    return tie_better(b1, m1, b2, m2);
+}
+
+// Offset (in entries) of family (v, S) inside child v's block of this rank's
+// table, given lm = (1 << v) - 1: compress(S, v) is the bitwise select
+// lm ? S : S >> 1 (bit v of S is 0).  World 1: the block is v 2^(m-1).. and
+// the offset is the compressed mask; otherwise (plan.h) child v's 2^(m-r)
+// entries hold the masks whose top selector bits match this rank's patterns.
+template <bool WORLD1>
+__device__ __forceinline__ uint32_t block_offset(const TravParams& P, uint32_t S, uint32_t S1, uint32_t lm)
+{
+    const uint32_t cpr = (S & lm) | (S1 & ~lm);
+    if (WORLD1) return cpr;
+    const int v = __popc(lm);
+    const bool sel = v >= P.m - P.r;
+    const int sh = sel ? P.m - P.r : P.m - 1 - P.r;
+    return (cpr & ((1u << sh) - 1u)) + ((!sel && (cpr >> sh) != P.patlo) ? (1u << sh) : 0u);
+}
+
+}  // namespace bnr

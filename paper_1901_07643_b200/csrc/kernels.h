@@ -29,7 +29,18 @@ struct TravParams {
     int r;                      // rank-selector bits (world > 1)
     unsigned patlo;             // smaller selector pattern of this rank (non-selector children)
     unsigned long long* dbg;    // profiling aid (BNREG_DEBUG_STEP_CLOCKS): per-step clock64 stamps, or nullptr
+    // walk kernel (walk_kernel.cu): one launch per smem class of work items
+    int S_alloc;                // walk slots allocated per warp (>= every item's slot count)
+    int item_begin, item_end;   // this launch's work items [begin, end) of `packs`
+    int part_base;              // first row of this launch's warps in part_bic / part_mask
+    int bar_every;              // gang barrier every bar_every steps
 };
+
+// walk kernel: 2^lw lockstep workers per warp, gang of 2^g warps per CTA
+constexpr int kWalkLW = 3;
+size_t walk_cta_smem(int m, int k, int S_alloc, int g);
+int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1);
+cudaError_t launch_walk(const TravParams& P, int grid_ctas, cudaStream_t st);
 
 // smem bytes per warp of the traversal kernel
 size_t traverse_smem_per_warp(int m, int k);

@@ -27,6 +27,7 @@
 // = a gang: the 2^g packs whose ids differ only in the top g bits.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -37,7 +38,16 @@ namespace bnr {
 
 constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
-constexpr int kPackBits = 2;     // 4 lockstep workers per warp
+constexpr int kPackBits = 3;     // 8 lockstep workers per warp (walk kernel)
+constexpr int kPackBitsLegacy = 2;  // 4 per warp (legacy traversal kernels, BNREG_LEGACY_TRAVERSE / BNREG_WS_TRAVERSE)
+
+// 0 = walk kernel (default), 1 = legacy traversal, 2 = warp-specialised traversal
+inline int kernel_variant()
+{
+    if (std::getenv("BNREG_LEGACY_TRAVERSE")) return 1;
+    if (std::getenv("BNREG_WS_TRAVERSE")) return 2;
+    return 0;
+}
 constexpr int kGangBits = 2;     // 4 lockstep warps per CTA
 
 // Alg.1 GreedySwaps(m) with Eq.10's +1.
@@ -105,6 +115,7 @@ inline std::vector<StepRec> step_records(int k, const std::vector<int8_t>& sched
 
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
+    int variant = 0;                          // kernel_variant() at plan time
     int g = 0;                                // gang bits (the top g of the bh tree bits)
     int L1 = 0, LW = 0;                       // tree depth in global memory / levels derived in-warp
     int world = 1, rank = 0, r = 0;           // rank selector bits r (0 when world == 1)
@@ -155,7 +166,8 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (k <= 0) k = std::min(m, 9);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
-    P.p = std::min(kPackBits, P.b);
+    P.variant = kernel_variant();
+    P.p = std::min(P.variant == 0 ? kPackBits : kPackBitsLegacy, P.b);
     P.bh = P.b - P.p;
     P.g = std::min(kGangBits, P.bh);
     if (lw < 0) lw = 4;
@@ -164,9 +176,11 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     P.world = world; P.rank = rank;
     P.total_families = (int64_t)m << (m - 1);
     P.sched = greedy_swaps(k);
-    // root order: [hv[0..bh-1], pack 0..p-1, free p+g..p+g+k-1]
+    // root order: [hv[0..bh-1], pack vars, free p+g..p+g+k-1]
     for (int l = 0; l < P.bh; ++l) P.root_order.push_back(hv_id(P, l));
-    for (int j = 0; j < P.p; ++j) P.root_order.push_back(j);
+    // the walk kernel's Gray path wants the warp variables in descending id
+    // next to the free block ([w_{p-1} .. w_0 | free]); the legacy kernels ascending
+    for (int j = 0; j < P.p; ++j) P.root_order.push_back(P.variant == 0 ? P.p - 1 - j : j);
     for (int f = 0; f < k; ++f) P.root_order.push_back(P.p + P.g + f);
 
     // rank selector: top r hi bits (hv[0..r-1] = ids m-1..m-r), complementary patterns

@@ -51,13 +51,13 @@ def test_index_matches_oracle(bn):
 
 @pytest.mark.parametrize("m,k", [(8, 4), (12, 5), (16, 8), (20, 8), (28, 8), (24, 10)])
 def test_plan_partition(bn, m, k):
-    """Packs x 4 workers enumerate every Alg.2 worker (every front set of the
+    """Packs x 2^p workers enumerate every Alg.2 worker (every front set of the
     pinned variables) exactly once; world ranks split packs disjointly with
     equal cost (complementary top-bit patterns)."""
     n = 1000
     q = bn.bnreg_plan_query(m, n, bn.options(free_vars=k))
     assert q["sched_len"] == 2 ** k - k - 1
-    assert q["b"] == m - k and q["p"] == min(2, m - k)
+    assert q["b"] == m - k and q["p"] == min(3, m - k)   # 8 lockstep workers per warp (walk kernel)
     def expand(items):
         gs = q["bh"] - q["g"]
         return [it | (j << gs) for it in items for j in range(1 << q["g"])]

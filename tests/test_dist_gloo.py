@@ -76,7 +76,7 @@ def _worker(rank, world, port, m, n, k, q):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_gloo_shard_protocol(world):
-    m, n, k = 11, 60, 4
+    m, n, k = 11, 60, 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -190,12 +190,12 @@ def test_logical_ranks_union(world):
     bn = _bn()
     X = datagen.dag_data(12, 200, 0.25, 0.5, 2.0, seed=12)
     m = 12
-    full, fullb, fbm, fbb, h0 = run_tables(X, bn.options(free_vars=4))
+    full, fullb, fbm, fbb, h0 = run_tables(X, bn.options(free_vars=3))
     h0.close()
     seen = np.zeros(m << (m - 1), dtype=np.int32)
     masks, bics = [], []
     for rank in range(world):
-        rss, bic, bm, bb, h = run_tables(X, bn.options(free_vars=4, world=world, rank=rank))
+        rss, bic, bm, bb, h = run_tables(X, bn.options(free_vars=3, world=world, rank=rank))
         starts, lens = h.shard_ranges()
         gidx = np.concatenate([np.arange(s, s + l) for s, l in zip(starts, lens)])
         assert len(gidx) == h.num_families() == len(rss)
