@@ -58,7 +58,8 @@ struct bnreg {
     double* d_best_bic = nullptr;
     uint32_t* d_best_mask = nullptr;
     int* d_status = nullptr;
-    double2* d_lntab = nullptr;    // fast-log table (a9)
+    double2* d_lntab = nullptr;    // fast-log table (a9), 128 entries (legacy kernels)
+    double2* d_lntab9 = nullptr;   // fast-log table (a9), 512 entries (walk kernel, debug_ln)
     int grid_ctas = 0, wpc = 2;
     bool loaded = false;
     // timing
@@ -93,7 +94,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab, h->d_counters};
+                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -208,6 +209,8 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
     h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
     (void)d.warps_per_cta;
+    if (P.variant == 0 && P.local_families > (int64_t)0xffffffffLL)
+        return bail(fail(BNREG_E_INVAL, "this rank's table exceeds 2^32 entries (use more ranks)"));
     if (P.variant == 0) {
         // walk kernel: items are sorted costliest first = most walk slots first
         // (a gang's slots: m - |F among its tree levels|); consecutive items with
@@ -234,6 +237,10 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             h->classes.push_back(c);
             i0 = i1;
         }
+        if (getenv("BNREG_VERBOSE"))
+            for (auto& c : h->classes)
+                fprintf(stderr, "walk class: items [%d, %d) S_alloc %d grid %d smem %zu\n", c.begin, c.end, c.S_alloc,
+                        c.grid, walk_cta_smem(m, P.k, c.S_alloc, P.g));
         if (h->classes.empty()) {            // no work items (cannot happen for m >= 2): keep the reduce well-defined
             h->nparts = 1;
         }
@@ -269,6 +276,15 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         }
         CKH(cudaMalloc(&h->d_lntab, 128 * sizeof(double2)));
         CKH(cudaMemcpy(h->d_lntab, tab.data(), 128 * sizeof(double2), cudaMemcpyHostToDevice));
+        std::vector<double2> tab9(512);
+        for (int j = 0; j < 512; ++j) {
+            long double t = 1.0L + ((long double)j + 0.5L) / 512.0L;
+            double r = (double)(1.0L / t);
+            tab9[j].x = r;
+            tab9[j].y = (double)(-logl((long double)r));
+        }
+        CKH(cudaMalloc(&h->d_lntab9, 512 * sizeof(double2)));
+        CKH(cudaMemcpy(h->d_lntab9, tab9.data(), 512 * sizeof(double2), cudaMemcpyHostToDevice));
     }
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
 #undef CKH
@@ -456,6 +472,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
     T.lntab = h->d_lntab;
+    T.lntab9 = h->d_lntab9;
     T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
     T.r = P.r;
@@ -574,7 +591,7 @@ bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* r
 bnreg_status bnreg_debug_ln(bnreg_t* h, const double* x_dev, double* out_dev, int64_t count)
 {
     if (!h || (!x_dev && count > 0) || (!out_dev && count > 0)) return fail(BNREG_E_INVAL, "NULL argument");
-    CK(launch_debug_ln(x_dev, out_dev, count, h->d_lntab, h->stream));
+    CK(launch_debug_ln(x_dev, out_dev, count, h->d_lntab9, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return BNREG_OK;
 }

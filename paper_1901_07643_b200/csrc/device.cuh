@@ -67,6 +67,25 @@ __device__ __forceinline__ double fast_ln(double x, const double2* tab)
     return fma(u, q, base);
 }
 
+// The walk kernel's log: the same reduction with a 512-entry table,
+// r_j ~ 1/(1 + (j+0.5)/512), |u| <= 9.8e-4, so log1p(u) = u q(u) with q the
+// degree-3 Taylor polynomial (truncation u^5/5 < 2e-16).
+__device__ __forceinline__ double fast_ln9(double x, const double2* tab)
+{
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) - 1023;
+    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 t = *(const double2*)((const char*)tab + ((hi >> 7) & 0x1ff0));
+    const double ed = (double)e;
+    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], t.y));
+    const double u = fma(f, t.x, -1.0);
+    const double u2 = u * u;
+    const double a = fma(u, c_ln[0], 1.0);
+    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double q = fma(u2, b, a);
+    return fma(u, q, base);
+}
+
 // Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
 __device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
 

@@ -24,7 +24,8 @@ struct TravParams {
     double* part_bic;           // [grid warps][m] per-warp best BIC
     uint32_t* part_mask;        // [grid warps][m] per-warp best mask
     double mhalf_n;             // -n/2
-    const double2* lntab;       // fast-log table (128 x (r_j, -ln r_j))
+    const double2* lntab;       // fast-log table (128 x (r_j, -ln r_j)), legacy kernels
+    const double2* lntab9;      // fast-log table (512 x (r_j, -ln r_j)), walk kernel
     double Kc[33];              // BIC constant per parent-set size
     int r;                      // rank-selector bits (world > 1)
     unsigned patlo;             // smaller selector pattern of this rank (non-selector children)

@@ -30,15 +30,16 @@
 namespace bnr {
 
 // ---------------------------------------------------------------- shared memory layout
-// Per CTA: [lntab 128 x 16 B][K(s) 33 doubles] then per warp:
+// Per CTA: [log table 512 x 16 B][K(s) 33 doubles] then per warp:
 //   state   k * SA * W * 16 B   E(l, slot, w) at ((l*SA + slot)*W + w)*16
-//   scratch max(tri, SA*W*12)   derivation triangle (packed, side <= m) | per-(slot, worker) best
-//   desc    SA * 16 B           (RSS row ptr, BIC row ptr) of each slot's child
-//   lm      SA * 4 B            (1 << v) - 1 of each slot's child v
+//   scratch                     derivation triangle (packed, side <= m), then
+//                               rec[slot][w] (16 B: running best BIC, table index of
+//                               (child, F_w) with no free variable, lm = (1 << v) - 1)
+//                               and bm[slot][w] (mask of the running best)
 //   wbb/wbm 32 * 12 B           the warp's running best per child (kept across items)
 //   slotof  32 B                variable -> slot
 struct WalkLayout {
-    int state, scratch, bm, desc, lm, wbb, wbm, slotof, per_warp;
+    int state, scratch, bm, wbb, wbm, slotof, per_warp;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -50,13 +51,9 @@ __host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
     L.state = o;
     o += al16(k * SA * W * 16);
     L.scratch = o;
-    L.bm = o + SA * W * 8;
-    const int tri = (m * (m + 1) / 2) * 8, bst = SA * W * 12;
-    o += al16(tri > bst ? tri : bst);
-    L.desc = o;
-    o += al16(SA * 16);
-    L.lm = o;
-    o += al16(SA * 4);
+    L.bm = o + SA * W * 16;
+    const int tri = (m * (m + 1) / 2) * 8, rec = SA * W * 20;
+    o += al16(tri > rec ? tri : rec);
     L.wbb = o;
     o += 32 * 8;
     L.wbm = o;
@@ -67,7 +64,7 @@ __host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
     return L;
 }
 
-constexpr int kWalkHead = 2048 + 272;   // lntab + K(s) table
+constexpr int kWalkHead = 8192 + 272;   // log table + K(s) table
 
 size_t walk_cta_smem(int m, int k, int SA, int g)
 {
@@ -111,34 +108,106 @@ __device__ __forceinline__ void snapshot(const double* A, int sn, int og, int k,
     }
 }
 
-// One family (child of list entry `slot`, prefix set S of this worker):
-// BIC, the two table stores, the running best of (slot, worker).
-template <bool WORLD1, bool HR, bool HB>
-__device__ __forceinline__ void harvest(const TravParams& P, const double2* lntab, const ulonglong2* desc,
-                                        const uint32_t* lmt, double* bb, uint32_t* bm, int W, int w, int slot,
-                                        bool present, double rss, uint32_t S, uint32_t S1, double Kw)
+// Predicated stores that stay predicated (no branch around them, so the
+// entries of a step remain one basic block the scheduler can interleave).
+__device__ __forceinline__ void stg_cs_if(double* p, double v, bool q)
 {
-    const double bic = bic_of(rss, fast_ln(rss, lntab), P.mhalf_n, Kw);   // rss <= 1e-300 -> +inf
-    const ulonglong2 d = desc[slot];
-    const uint32_t off = block_offset<WORLD1>(P, S, S1, lmt[slot]);
-    if (present) {
-        if (HR) __stcs((double*)d.x + off, rss);
-        if (HB) __stcs((double*)d.y + off, bic);
-        double* bp = bb + slot * W + w;
-        if (bic >= *bp) {                      // rare: a new best (or a tie) for this (child, worker)
-            uint32_t* mp = bm + slot * W + w;
-            if (tie_better(bic, S, *bp, *mp)) {
-                *bp = bic;
-                *mp = S;
-            }
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
+                 "r"((unsigned)q));
+}
+__device__ __forceinline__ void sts_pair_if(unsigned a, double x, double u, double y, int rs, bool q)
+{
+    // E_i = (x, u) at a, E_{i+1}.x = y at a + rs
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.shared.v2.f64 [%0], {%1, %2};\n\t"
+                 "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(a), "d"(x), "d"(u), "r"(a + rs), "d"(y), "r"((unsigned)q)
+                 : "memory");
+}
+
+// Per-step values shared by the step bodies.
+struct StepV {
+    unsigned bi;          // shared address of (slot 0, row i, worker w) of the walk state
+    unsigned rw;          // shared address of rec[slot 0][w]
+    int RS;               // bytes between rows i and i+1
+    int h, L, nf, kb;     // part, list length, free entries, back entry e -> slot kb + e
+    uint32_t nl, nh;      // this lane's free-list nibbles
+    uint32_t absent;      // slots whose variable is in this worker's F
+    uint32_t Tsh, Tsh1;   // free part of the prefix set, and >> 1
+    double c, sg;         // rotation
+    double Kw;            // BIC constant of |S|
+    int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
+};
+
+constexpr int kMaxE = 8;   // list entries per lane and step (list length <= 4 * kMaxE = 32 > m - 1)
+
+template <int PP>
+__device__ __forceinline__ int entry_slot(const StepV& v, int j)
+{
+    const int e = v.h + PP * j;
+    int slot = v.kb + e;
+    if (j < 4 && e < v.nf) slot = (int)(((j < 2 ? v.nl : v.nh) >> (16 * (j & 1))) & 15u);
+    return e < v.L ? slot : 0;
+}
+
+// One step of a lane: NE = ceil(L / PP) list entries (e = h + PP j).
+//   phase A: the GRC's rotation of rows i, i+1 of each entry's column and the
+//            new suffix sum U_{i+1} (a7, a8), or the seed pseudo-step's read
+//   phase C: ln RSS, BIC (a9), the two table stores (a10), the running-best
+//            candidates (a11; rare updates resolved by the caller)
+// The caller computes the next step's rotation between the two phases.
+template <bool SEED, int NE, int PP>
+__device__ __forceinline__ void phase_a(const StepV& v, double (&rs)[kMaxE], int (&sl)[kMaxE])
+{
+    double2 a0[NE], a1[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+        sl[j] = entry_slot<PP>(v, j);
+        const unsigned pa = v.bi + sl[j] * (16 * (32 / PP));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0[j].x), "=d"(a0[j].y) : "r"(pa));
+        if (!SEED) asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a1[j].x), "=d"(a1[j].y) : "r"(pa + v.RS));
+    }
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+        if (SEED) {
+            rs[j] = v.seed0 ? fma(a0[j].x, a0[j].x, a0[j].y) : a0[j].y;   // U_0 or U_{i+1}
+        } else {
+            const double xa = fma(v.c, a0[j].x, v.sg * a1[j].x), ya = fma(v.c, a1[j].x, -v.sg * a0[j].x);
+            const double ra = fma(ya, ya, a1[j].y);
+            rs[j] = ra;
+            const int e = v.h + PP * j;
+            sts_pair_if(v.bi + sl[j] * (16 * (32 / PP)), xa, ra, ya, v.RS, e < v.L);
         }
     }
 }
 
-__device__ __forceinline__ int entry_slot(int e, int nf, int k, uint64_t nib)
+template <bool HR, bool HB, int NE, int PP>
+__device__ __forceinline__ uint32_t phase_c(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
+                                            double* out_bic, const double (&rs)[kMaxE], const int (&sl)[kMaxE],
+                                            double (&bics)[kMaxE])
 {
-    return e < nf ? (int)((nib >> (4 * e)) & 15u) : k + e - nf;
+    const double PINF = __longlong_as_double(0x7ff0000000000000LL);
+    uint32_t upd = 0;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+        const int e = v.h + PP * j;
+        const int slot = sl[j];
+        const double rss = rs[j];
+        const double lnr = fast_ln9(rss, lntab);
+        double bic = fma(mhalf_n, lnr, v.Kw);
+        bic = rss > 1e-300 ? bic : PINF;                          // G13
+        bics[j] = bic;
+        double bb, rr;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(bb), "=d"(rr) : "r"(v.rw + slot * (16 * (32 / PP))));
+        const uint32_t idx = (uint32_t)__double2loint(rr);        // table index of (child, F_w)
+        const uint32_t lm = (uint32_t)__double2hiint(rr);         // (1 << child) - 1
+        const uint32_t ix = idx + ((v.Tsh & lm) | (v.Tsh1 & ~lm)); // + compress(T, child)
+        const bool ok = e < v.L && !((v.absent >> slot) & 1u);
+        if (HR) stg_cs_if(out_rss + ix, rss, ok);
+        if (HB) stg_cs_if(out_bic + ix, bic, ok);
+        upd |= (ok && bic >= bb) ? (1u << j) : 0u;
+    }
+    return upd;
 }
+
 
 template <bool WORLD1, bool HR, bool HB>
 __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ TravParams P)
@@ -146,12 +215,13 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     constexpr int LW = kWalkLW;
     constexpr int W = 1 << LW;
     constexpr int PP = 32 / W;                  // lanes (parts) per worker
+    static_assert(PP * kMaxE >= 32, "list entries");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_item;
     double2* const lntab = (double2*)smem;
-    double* const KC = (double*)(smem + 2048);
+    double* const KC = (double*)(smem + 8192);
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-    for (int j = tid; j < 128; j += blockDim.x) lntab[j] = P.lntab[j];
+    for (int j = tid; j < 512; j += blockDim.x) lntab[j] = P.lntab9[j];
     for (int j = tid; j < 33; j += blockDim.x) KC[j] = P.Kc[j];
     const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g, SA = P.S_alloc;
     const int fv0 = p + g;                      // user id of free slot 0
@@ -161,10 +231,8 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     unsigned char* const wb = smem + kWalkHead + wib * Ly.per_warp;
     unsigned char* const st = wb + Ly.state;
     double* const tri = (double*)(wb + Ly.scratch);
-    double* const bb = (double*)(wb + Ly.scratch);
-    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);
-    ulonglong2* const desc = (ulonglong2*)(wb + Ly.desc);
-    uint32_t* const lmt = (uint32_t*)(wb + Ly.lm);
+    unsigned char* const recb = wb + Ly.scratch;            // rec[slot][w], 16 B
+    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);           // bm[slot][w]
     double* const wbb = (double*)(wb + Ly.wbb);
     uint32_t* const wbm = (uint32_t*)(wb + Ly.wbm);
     uint8_t* const slotof = wb + Ly.slotof;
@@ -174,8 +242,11 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     wbm[lane] = 0xffffffffu;
     const int shb = WORLD1 ? m - 1 : m - P.r;   // child block = v << shb entries
     const int RS = SA * W * 16;                 // bytes between free rows l and l+1 of a slot
-    const int CSb = W * 16;                     // bytes between slots
+    constexpr int CSb = W * 16;                 // bytes between slots (state and rec)
     const int nw = P.nw;
+    double* const out_rss = P.out_rss;
+    double* const out_bic = P.out_bic;
+    const double mhalf_n = P.mhalf_n;
     __syncthreads();
 
     for (;;) {
@@ -228,29 +299,21 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                     }
             }
         }
-        // slot tables: slots [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
-        if (lane < SA) {
-            int v = -1;
+        // slot -> variable: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        int slotvar = -1;
+        if (lane < Sw) {
             const int s = lane;
-            if (s < k) v = fv0 + s;
-            else if (s < k + p) v = s - k;
-            else if (s < Sw) {
+            if (s < k) slotvar = fv0 + s;
+            else if (s < k + p) slotvar = s - k;
+            else {
                 int c = s - k - p;
                 for (int l = bh - 1; l >= 0; --l)
                     if (!((pack >> l) & 1u)) {
-                        if (c == 0) { v = hv_of(l, m, gs, fv0); break; }
+                        if (c == 0) { slotvar = hv_of(l, m, gs, fv0); break; }
                         --c;
                     }
             }
-            if (v >= 0) {
-                slotof[v] = (uint8_t)s;
-                desc[s] = make_ulonglong2(HR ? (unsigned long long)(P.out_rss + ((long long)v << shb)) : 0ull,
-                                          HB ? (unsigned long long)(P.out_bic + ((long long)v << shb)) : 0ull);
-                lmt[s] = (1u << v) - 1u;
-            } else {
-                desc[s] = make_ulonglong2(0ull, 0ull);
-                lmt[s] = 0u;
-            }
+            slotof[slotvar] = (uint8_t)s;
         }
         __syncwarp();
         // remaining tree levels in-warp: F -> drop the leading row/column, B -> bubble it behind the free block
@@ -282,9 +345,24 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             snapshot<W>(tri, sn, org + __popc(wcur), k, SA, wcur, lane, myvar, slotof, st);
         }
         __syncwarp();
-        for (int e = lane; e < SA * W; e += 32) {      // the best arrays overlay the triangle
-            bb[e] = NINF;
-            bm[e] = 0xffffffffu;
+        // per (slot, worker) records (they overlay the triangle): running best,
+        // table index of (child v, F_w) -- the free part is added per step -- and lm
+        {
+            // lane = (slot group, worker): 4 slots per pass
+            for (int s0 = 0; s0 < Sw; s0 += PP) {
+                const int s = s0 + h;
+                const int v = __shfl_sync(FULLMASK, slotvar, s & 31);
+                if (s < Sw) {
+                    const uint32_t Fw0 = Fhi | (uint32_t)w;
+                    const uint32_t lm = (1u << v) - 1u;
+                    const uint32_t idx = (uint32_t)((long long)v << shb) + block_offset<WORLD1>(P, Fw0, Fw0 >> 1, lm);
+                    unsigned char* r = recb + (s * W + w) * 16;
+                    *(double*)r = NINF;
+                    *(uint32_t*)(r + 8) = idx;
+                    *(uint32_t*)(r + 12) = lm;
+                    bm[s * W + w] = 0xffffffffu;
+                }
+            }
         }
         __syncwarp();
 
@@ -294,77 +372,94 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         const uint32_t absent = (w < nw) ? ((uint32_t)w << k) : 0xffffffffu;
         const int NB = Sw - k;
         unsigned char* const sw = st + w * 16;
+        unsigned char* const rw = recb + w * 16;
         double c = 1.0, sg = 0.0, hh = 0.0;
+        int bar_left = P.bar_every;
         uint4 rec = __ldg(P.steps);
         for (int t = 0; t < P.nsteps; ++t) {
             const uint4 nrec = (t + 1 < P.nsteps) ? __ldg(P.steps + t + 1) : make_uint4(1u << 18, 0, 0, 0);
             const int i = (int)(rec.x & 31u) - 1;
             const int nf = (int)((rec.x >> 13) & 31u);
             const int L = nf + NB;
-            const uint32_t S = Fw | (rec.y << fv0);
-            const uint32_t S1 = S >> 1;
+            const int kb = k - nf;                               // back entry e -> slot kb + e
+            const uint32_t Tsh = rec.y << fv0;                   // the free part of the prefix set
+            const uint32_t S = Fw | Tsh;
+            const uint32_t Tsh1 = Tsh >> 1;
             const double Kw = KC[dw + i + 1];
-            const uint64_t nib = ((uint64_t)rec.w << 32) | rec.z;
-            if ((rec.x >> 18) & 1u) {
-                // seed pseudo-step: prefix = free positions 0..i, RSS = U_{i+1} = E_i.y (U_0 = E_0.x^2 + E_0.y)
-                const unsigned char* bi = sw + (i < 0 ? 0 : i) * RS;
-                for (int e = h; e < L; e += PP) {
-                    const int slot = entry_slot(e, nf, k, nib);
-                    const double2 e0 = *(const double2*)(bi + slot * CSb);
-                    const double rss = i < 0 ? fma(e0.x, e0.x, e0.y) : e0.y;
-                    harvest<WORLD1, HR, HB>(P, lntab, desc, lmt, bb, bm, W, w, slot, !((absent >> slot) & 1u), rss,
-                                            S, S1, Kw);
-                }
+            // this lane's free-list nibbles: entry h + 4j at bits 16j (j = 0, 1) / 16(j-2) (j = 2, 3)
+            const uint32_t nl = __funnelshift_r(rec.z, rec.w, 4 * h);
+            const uint32_t nh = rec.w >> (4 * h);
+            const bool seed = (rec.x >> 18) & 1u;
+            StepV v;
+            v.bi = (unsigned)__cvta_generic_to_shared(sw + (i < 0 ? 0 : i) * RS);
+            v.rw = (unsigned)__cvta_generic_to_shared(rw);
+            v.RS = RS; v.h = h; v.L = L; v.nf = nf; v.kb = kb; v.nl = nl; v.nh = nh; v.absent = absent;
+            v.Tsh = Tsh; v.Tsh1 = Tsh1; v.c = c; v.sg = sg; v.Kw = Kw; v.seed0 = i < 0;
+            double rs[kMaxE], bics[kMaxE];
+            int sl[kMaxE];
+            const int ne = (L + PP - 1) / PP;
+#define BN_PA(SEEDV)                                                                      \
+    switch (ne) {                                                                         \
+        case 1: phase_a<SEEDV, 1, PP>(v, rs, sl); break;                                  \
+        case 2: phase_a<SEEDV, 2, PP>(v, rs, sl); break;                                  \
+        case 3: phase_a<SEEDV, 3, PP>(v, rs, sl); break;                                  \
+        case 4: phase_a<SEEDV, 4, PP>(v, rs, sl); break;                                  \
+        case 5: phase_a<SEEDV, 5, PP>(v, rs, sl); break;                                  \
+        case 6: phase_a<SEEDV, 6, PP>(v, rs, sl); break;                                  \
+        case 7: phase_a<SEEDV, 7, PP>(v, rs, sl); break;                                  \
+        default: phase_a<SEEDV, 8, PP>(v, rs, sl); break;                                 \
+    }
+            if (seed) {
+                BN_PA(true)
             } else {
-                // GRC at free position i: rotate rows i, i+1 of every column after the prefix
-                unsigned char* const bi = sw + i * RS;
-                int e = h;
-                for (; e + PP < L; e += 2 * PP) {
-                    const int sa = entry_slot(e, nf, k, nib), sb = entry_slot(e + PP, nf, k, nib);
-                    unsigned char* const pa = bi + sa * CSb;
-                    unsigned char* const pb = bi + sb * CSb;
-                    const double2 a0 = *(const double2*)pa, a1 = *(const double2*)(pa + RS);
-                    const double2 b0 = *(const double2*)pb, b1 = *(const double2*)(pb + RS);
-                    const double xa = fma(c, a0.x, sg * a1.x), ya = fma(c, a1.x, -sg * a0.x);
-                    const double xb = fma(c, b0.x, sg * b1.x), yb = fma(c, b1.x, -sg * b0.x);
-                    const double ra = fma(ya, ya, a1.y), rb = fma(yb, yb, b1.y);
-                    *(double2*)pa = make_double2(xa, ra);
-                    *(double*)(pa + RS) = ya;
-                    *(double2*)pb = make_double2(xb, rb);
-                    *(double*)(pb + RS) = yb;
-                    harvest<WORLD1, HR, HB>(P, lntab, desc, lmt, bb, bm, W, w, sa, !((absent >> sa) & 1u), ra, S, S1,
-                                            Kw);
-                    harvest<WORLD1, HR, HB>(P, lntab, desc, lmt, bb, bm, W, w, sb, !((absent >> sb) & 1u), rb, S, S1,
-                                            Kw);
-                }
-                if (e < L) {
-                    const int sa = entry_slot(e, nf, k, nib);
-                    unsigned char* const pa = bi + sa * CSb;
-                    const double2 a0 = *(const double2*)pa, a1 = *(const double2*)(pa + RS);
-                    const double xa = fma(c, a0.x, sg * a1.x), ya = fma(c, a1.x, -sg * a0.x);
-                    const double ra = fma(ya, ya, a1.y);
-                    *(double2*)pa = make_double2(xa, ra);
-                    *(double*)(pa + RS) = ya;
-                    harvest<WORLD1, HR, HB>(P, lntab, desc, lmt, bb, bm, W, w, sa, !((absent >> sa) & 1u), ra, S, S1,
-                                            Kw);
-                }
+                BN_PA(false)
                 if (h == 0) {
                     // the pivot Y (now at position i): R_i = h, U_{i+1} = 0, R_{i+1} = 0
-                    unsigned char* const py = bi + (int)((rec.x >> 9) & 15u) * CSb;
+                    unsigned char* const py = sw + i * RS + (int)((rec.x >> 9) & 15u) * CSb;
                     *(double2*)py = make_double2(hh, 0.0);
                     *(double*)(py + RS) = 0.0;
                 }
             }
+#undef BN_PA
             __syncwarp();
+            // ---- the next step's rotation (entries (in, in+1) of its pivot column); overlaps phase C
             if (!((nrec.x >> 18) & 1u)) {
-                // the next step's rotation: entries (in, in+1) of its pivot column
                 const int in = (int)(nrec.x & 31u) - 1, Yn = (int)((nrec.x >> 9) & 15u);
                 const unsigned char* col = sw + in * RS + Yn * CSb;
                 givens(*(const double*)col, *(const double*)(col + RS), c, sg, hh);
             }
+            // ---- phase C: BIC, table stores, running best (a8-a11)
+            uint32_t upd;
+            switch (ne) {
+                case 1: upd = phase_c<HR, HB, 1, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 2: upd = phase_c<HR, HB, 2, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 3: upd = phase_c<HR, HB, 3, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 4: upd = phase_c<HR, HB, 4, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 5: upd = phase_c<HR, HB, 5, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 6: upd = phase_c<HR, HB, 6, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                case 7: upd = phase_c<HR, HB, 7, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+                default: upd = phase_c<HR, HB, 8, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
+            }
+            if (upd) {
+                // rare: a new best (or a tie, G14) for some (child, worker) of this lane
+                for (int j = 0; j < kMaxE; ++j) {
+                    if ((upd >> j) & 1u) {
+                        const int slot = sl[j];
+                        double* bp = (double*)(rw + slot * CSb);
+                        uint32_t* mp = bm + slot * W + w;
+                        if (tie_better(bics[j], S, *bp, *mp)) {
+                            *bp = bics[j];
+                            *mp = S;
+                        }
+                    }
+                }
+            }
             rec = nrec;
             // the gang's warps write the two halves of each 256 B region: keep them in step
-            if (G > 1 && (t % P.bar_every) == P.bar_every - 1) __syncthreads();
+            if (G > 1 && --bar_left == 0) {
+                bar_left = P.bar_every;
+                __syncthreads();
+            }
         }
         __syncwarp();
         // fold the per-(slot, worker) bests into the warp's per-child best (a11)
@@ -372,7 +467,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             double b = NINF;
             uint32_t mk = 0xffffffffu;
             if (lane < W) {
-                b = bb[s * W + lane];
+                b = *(const double*)(recb + (s * W + lane) * 16);
                 mk = bm[s * W + lane];
             }
 #pragma unroll
@@ -384,12 +479,10 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                     mk = om;
                 }
             }
-            if (lane == 0) {
-                const int v = __popc(lmt[s]);
-                if (better(b, mk, wbb[v], wbm[v])) {
-                    wbb[v] = b;
-                    wbm[v] = mk;
-                }
+            const int v = __shfl_sync(FULLMASK, slotvar, s);
+            if (lane == 0 && better(b, mk, wbb[v], wbm[v])) {
+                wbb[v] = b;
+                wbm[v] = mk;
             }
             __syncwarp();
         }
