@@ -220,12 +220,12 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         const int64_t ni = (int64_t)P.packs.size();
         while (i0 < ni) {
             const int S0 = m - popc(P.packs[i0] & ((1u << gs) - 1u));
-            int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, P.world == 1);
+            int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, P.world == 1, P.lw);
             if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory"));
             int64_t i1 = i0 + 1;
             while (i1 < ni) {
                 const int S1 = m - popc(P.packs[i1] & ((1u << gs) - 1u));
-                const int o1 = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S1, P.g, P.world == 1);
+                const int o1 = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S1, P.g, P.world == 1, P.lw);
                 if (o1 != occ) break;
                 ++i1;
             }
@@ -240,7 +240,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         if (getenv("BNREG_VERBOSE"))
             for (auto& c : h->classes)
                 fprintf(stderr, "walk class: items [%d, %d) S_alloc %d grid %d smem %zu\n", c.begin, c.end, c.S_alloc,
-                        c.grid, walk_cta_smem(m, P.k, c.S_alloc, P.g));
+                        c.grid, walk_cta_smem(m, P.k, c.S_alloc, P.g, P.lw));
         if (h->classes.empty()) {            // no work items (cannot happen for m >= 2): keep the reduce well-defined
             h->nparts = 1;
         }
@@ -480,6 +480,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     if (P.variant == 0) {
         T.nw = 1 << P.p;
         T.bar_every = h->bar_every;
+        T.lw = P.lw;
         CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
         for (size_t c = 0; c < h->classes.size(); ++c) {
             const auto& C = h->classes[c];

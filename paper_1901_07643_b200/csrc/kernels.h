@@ -35,12 +35,12 @@ struct TravParams {
     int item_begin, item_end;   // this launch's work items [begin, end) of `packs`
     int part_base;              // first row of this launch's warps in part_bic / part_mask
     int bar_every;              // gang barrier every bar_every steps
+    int lw;                     // log2 workers per warp
 };
 
-// walk kernel: 2^lw lockstep workers per warp, gang of 2^g warps per CTA
-constexpr int kWalkLW = 3;
-size_t walk_cta_smem(int m, int k, int S_alloc, int g);
-int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1);
+// walk kernel: 2^lw lockstep workers per warp (lw = 3 or 4), gang of 2^g warps per CTA
+size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);
+int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw);
 cudaError_t launch_walk(const TravParams& P, int grid_ctas, cudaStream_t st);
 
 // smem bytes per warp of the traversal kernel

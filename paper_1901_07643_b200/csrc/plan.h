@@ -116,6 +116,7 @@ inline std::vector<StepRec> step_records(int k, const std::vector<int8_t>& sched
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
     int variant = 0;                          // kernel_variant() at plan time
+    int lw = kPackBits;                       // walk kernel: log2 lockstep workers per warp
     int g = 0;                                // gang bits (the top g of the bh tree bits)
     int L1 = 0, LW = 0;                       // tree depth in global memory / levels derived in-warp
     int world = 1, rank = 0, r = 0;           // rank selector bits r (0 when world == 1)
@@ -167,9 +168,12 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.variant = kernel_variant();
-    P.p = std::min(P.variant == 0 ? kPackBits : kPackBitsLegacy, P.b);
+    P.lw = kPackBits;
+    if (const char* e = std::getenv("BNREG_WALK_LW")) P.lw = (std::atoi(e) == 4) ? 4 : 3;
+    P.p = std::min(P.variant == 0 ? P.lw : kPackBitsLegacy, P.b);
     P.bh = P.b - P.p;
-    P.g = std::min(kGangBits, P.bh);
+    // walk kernel: a CTA's 2^g warps x 2^lw workers = 32 workers = 256 B per (child, step)
+    P.g = std::min(P.variant == 0 ? 5 - P.lw : kGangBits, P.bh);
     if (lw < 0) lw = 4;
     P.LW = std::min(std::max(lw, P.g), P.bh);
     P.L1 = P.bh - P.LW;

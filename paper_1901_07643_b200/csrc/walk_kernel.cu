@@ -66,9 +66,9 @@ __host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
 
 constexpr int kWalkHead = 8192 + 272;   // log table + K(s) table
 
-size_t walk_cta_smem(int m, int k, int SA, int g)
+size_t walk_cta_smem(int m, int k, int SA, int g, int lw)
 {
-    return (size_t)kWalkHead + ((size_t)1 << g) * (size_t)walk_layout(m, k, SA, 1 << kWalkLW).per_warp;
+    return (size_t)kWalkHead + ((size_t)1 << g) * (size_t)walk_layout(m, k, SA, 1 << lw).per_warp;
 }
 
 // user id of seed-tree level l (plan.h hv_id): top ids first, the gang ids last
@@ -123,99 +123,162 @@ __device__ __forceinline__ void sts_pair_if(unsigned a, double x, double u, doub
                  : "memory");
 }
 
-// Per-step values shared by the step bodies.
+// Givens coefficients without the rank-deficiency guard: in the walk, b is the
+// diagonal entry r_{i+1,i+1} of the pivot column, nonzero for full-rank data
+// (checked at create, G26), so h2 > 0.
+__device__ __forceinline__ void givens_fr(double a, double b, double& c, double& s, double& h)
+{
+    const double h2 = fma(a, a, b * b);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+    double e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    c = a * y;
+    s = b * y;
+    h = h2 * y;
+}
+
+// Per-step values of a lane (entries e = h + PP j of the step's list: the free
+// slots after the prefix, in position order, then the back slots).
 struct StepV {
-    unsigned bi;          // shared address of (slot 0, row i, worker w) of the walk state
-    unsigned rw;          // shared address of rec[slot 0][w]
+    unsigned bi;          // shared address of (row i, slot 0, worker w) of the walk state
+    unsigned bb0;         // shared address of the lane's first back entry: bi + (kb + h) * CSb
+    unsigned rb0;         // the same in the record array
+    unsigned rdelta;      // record address - state address (same slot stride)
     int RS;               // bytes between rows i and i+1
-    int h, L, nf, kb;     // part, list length, free entries, back entry e -> slot kb + e
-    uint32_t nl, nh;      // this lane's free-list nibbles
-    uint32_t absent;      // slots whose variable is in this worker's F
-    uint32_t Tsh, Tsh1;   // free part of the prefix set, and >> 1
-    double c, sg;         // rotation
+    int nvalid;           // entries j < nvalid exist for this lane
+    int nfj;              // entries j < nfj are free slots (from the nibble list)
+    uint32_t nl, nh;      // the free-list nibbles shifted to this lane's first entry
+    uint32_t ab0;         // absent >> (kb + h): bit PP j = back entry j's variable is in F
+    uint32_t Tsh, Tsh1;   // free part of the prefix set (user-id bits), and >> 1
+    double c, sg;         // this step's rotation
     double Kw;            // BIC constant of |S|
     int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
 };
 
-constexpr int kMaxE = 8;   // list entries per lane and step (list length <= 4 * kMaxE = 32 > m - 1)
+constexpr int kMaxE = 16;   // list entries per lane and step (PP * kMaxE >= 32 > m - 1)
 
-template <int PP>
-__device__ __forceinline__ int entry_slot(const StepV& v, int j)
+// state address of entry j (free entries from the nibble list, back entries at fixed strides)
+template <int PP, int CSB>
+__device__ __forceinline__ unsigned entry_addr(const StepV& v, int j)
 {
-    const int e = v.h + PP * j;
-    int slot = v.kb + e;
-    if (j < 4 && e < v.nf) slot = (int)(((j < 2 ? v.nl : v.nh) >> (16 * (j & 1))) & 15u);
-    return e < v.L ? slot : 0;
+    constexpr int JF = (15 + PP - 1) / PP;                   // free entries only for e < nf <= 15
+    const unsigned back = v.bb0 + j * (PP * CSB);
+    if (j < JF) {
+        const int sh = 4 * PP * j;                           // nibble of entry e = h + PP j
+        const unsigned f = ((sh < 32 ? v.nl >> (sh & 31) : v.nh >> ((sh - 32) & 31)) & 15u);
+        return j < v.nfj ? v.bi + f * CSB : back;
+    }
+    return back;
 }
 
-// One step of a lane: NE = ceil(L / PP) list entries (e = h + PP j).
-//   phase A: the GRC's rotation of rows i, i+1 of each entry's column and the
-//            new suffix sum U_{i+1} (a7, a8), or the seed pseudo-step's read
-//   phase C: ln RSS, BIC (a9), the two table stores (a10), the running-best
-//            candidates (a11; rare updates resolved by the caller)
-// The caller computes the next step's rotation between the two phases.
-template <bool SEED, int NE, int PP>
-__device__ __forceinline__ void phase_a(const StepV& v, double (&rs)[kMaxE], int (&sl)[kMaxE])
+// One lockstep step of a lane over its NE = ceil(L / PP) entries:
+//   phase A  the GRC's rotation of rows i, i+1 of every entry's column and the
+//            new suffix sum U_{i+1} = U_{i+2} + R'_{i+1}^2 (a7, a8), or the seed
+//            pseudo-step's read of U_{i+1};
+//   pivot    Y (now at position i): E_i = (h, 0), R_{i+1} = 0;
+//   givens   the next step's rotation from its pivot column (overlaps phase C);
+//   phase C  ln RSS, BIC (a9), the two table stores (a10), running-best
+//            candidates; new bests (rare) resolved at the end (a11, G14).
+template <bool SEED, int NE, int PP, int CSB, bool HR, bool HB>
+__device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
+                                          double* out_bic, bool pivot, unsigned pcol, double hh, bool has_next,
+                                          unsigned ncol, double& cn, double& sn, double& hn, uint32_t S, double* bbw,
+                                          uint32_t* bmw)
 {
-    double2 a0[NE], a1[NE];
+    constexpr int NA = NE > 0 ? NE : 1;                       // (NE = 0: an empty list, e.g. the last seed step)
+    double rs[NA];
+    unsigned ad[NA];
+    {
+        double2 a0[NA], a1[NA];
 #pragma unroll
-    for (int j = 0; j < NE; ++j) {
-        sl[j] = entry_slot<PP>(v, j);
-        const unsigned pa = v.bi + sl[j] * (16 * (32 / PP));
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0[j].x), "=d"(a0[j].y) : "r"(pa));
-        if (!SEED) asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a1[j].x), "=d"(a1[j].y) : "r"(pa + v.RS));
-    }
+        for (int j = 0; j < NE; ++j) {
+            ad[j] = entry_addr<PP, CSB>(v, j);
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0[j].x), "=d"(a0[j].y) : "r"(ad[j]));
+            if (!SEED)
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a1[j].x), "=d"(a1[j].y) : "r"(ad[j] + v.RS));
+        }
 #pragma unroll
-    for (int j = 0; j < NE; ++j) {
-        if (SEED) {
-            rs[j] = v.seed0 ? fma(a0[j].x, a0[j].x, a0[j].y) : a0[j].y;   // U_0 or U_{i+1}
-        } else {
-            const double xa = fma(v.c, a0[j].x, v.sg * a1[j].x), ya = fma(v.c, a1[j].x, -v.sg * a0[j].x);
-            const double ra = fma(ya, ya, a1[j].y);
-            rs[j] = ra;
-            const int e = v.h + PP * j;
-            sts_pair_if(v.bi + sl[j] * (16 * (32 / PP)), xa, ra, ya, v.RS, e < v.L);
+        for (int j = 0; j < NE; ++j) {
+            if (SEED) {
+                rs[j] = v.seed0 ? fma(a0[j].x, a0[j].x, a0[j].y) : a0[j].y;   // U_0 or U_{i+1}
+            } else {
+                const double xa = fma(v.c, a0[j].x, v.sg * a1[j].x), ya = fma(v.c, a1[j].x, -v.sg * a0[j].x);
+                const double ra = fma(ya, ya, a1[j].y);
+                rs[j] = ra;
+                sts_pair_if(ad[j], xa, ra, ya, v.RS, j < v.nvalid);
+            }
         }
     }
-}
-
-template <bool HR, bool HB, int NE, int PP>
-__device__ __forceinline__ uint32_t phase_c(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
-                                            double* out_bic, const double (&rs)[kMaxE], const int (&sl)[kMaxE],
-                                            double (&bics)[kMaxE])
-{
+    if (!SEED && pivot) sts_pair_if(pcol, hh, 0.0, 0.0, v.RS, true);
+    __syncwarp();
+    if (has_next) {
+        double a, b;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(ncol));
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(ncol + v.RS));
+        givens_fr(a, b, cn, sn, hn);
+    }
     const double PINF = __longlong_as_double(0x7ff0000000000000LL);
+    constexpr int JF = (15 + PP - 1) / PP;
     uint32_t upd = 0;
+    double bics[NA];
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
-        const int e = v.h + PP * j;
-        const int slot = sl[j];
         const double rss = rs[j];
         const double lnr = fast_ln9(rss, lntab);
         double bic = fma(mhalf_n, lnr, v.Kw);
-        bic = rss > 1e-300 ? bic : PINF;                          // G13
+        bic = rss > 1e-300 ? bic : PINF;                            // G13
         bics[j] = bic;
+        const unsigned ra = (j < JF) ? ad[j] + v.rdelta : v.rb0 + j * (PP * CSB);
         double bb, rr;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(bb), "=d"(rr) : "r"(v.rw + slot * (16 * (32 / PP))));
-        const uint32_t idx = (uint32_t)__double2loint(rr);        // table index of (child, F_w)
-        const uint32_t lm = (uint32_t)__double2hiint(rr);         // (1 << child) - 1
-        const uint32_t ix = idx + ((v.Tsh & lm) | (v.Tsh1 & ~lm)); // + compress(T, child)
-        const bool ok = e < v.L && !((v.absent >> slot) & 1u);
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(bb), "=d"(rr) : "r"(ra));
+        const uint32_t idx = (uint32_t)__double2loint(rr);          // table index of (child, F_w)
+        const uint32_t lm = (uint32_t)__double2hiint(rr);           // (1 << child) - 1
+        const uint32_t ix = idx + ((v.Tsh & lm) | (v.Tsh1 & ~lm));   // + compress(T, child)
+        bool ok = j < v.nvalid;
+        if (j < JF) ok = ok && (j < v.nfj || !((v.ab0 >> (PP * j)) & 1u));
+        else ok = ok && !((v.ab0 >> (PP * j)) & 1u);
         if (HR) stg_cs_if(out_rss + ix, rss, ok);
         if (HB) stg_cs_if(out_bic + ix, bic, ok);
         upd |= (ok && bic >= bb) ? (1u << j) : 0u;
     }
-    return upd;
+    if (upd) {
+        // rare: a new best (or a tie) for some (child, worker) of this lane
+#pragma unroll
+        for (int j = 0; j < NE; ++j) {
+            if ((upd >> j) & 1u) {
+                const unsigned ra = (j < JF) ? ad[j] + v.rdelta : v.rb0 + j * (PP * CSB);
+                double* bp = (double*)__cvta_shared_to_generic(ra);
+                const int q = (int)((ra - (unsigned)__cvta_generic_to_shared(bbw)) / 16u);   // (slot, w) record index
+                uint32_t* mp = bmw + q;
+                if (tie_better(bics[j], S, *bp, *mp)) {
+                    *bp = bics[j];
+                    *mp = S;
+                }
+            }
+        }
+    }
 }
 
+// NE-dispatch of the step body (NE = entries per lane, at most 32 / PP).
+template <bool SEED, int PP, int CSB, bool HR, bool HB, int NE>
+__device__ __forceinline__ void step_ne(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
+                                        double* out_bic, bool pv, unsigned pcol, double hh, bool has_next,
+                                        unsigned ncol, double& cn, double& sn, double& hn, uint32_t S, double* bbw,
+                                        uint32_t* bmw)
+{
+    if constexpr (NE * PP <= 32)
+        walk_step<SEED, NE, PP, CSB, HR, HB>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn,
+                                             hn, S, bbw, bmw);
+}
 
-template <bool WORLD1, bool HR, bool HB>
+template <int LW, bool WORLD1, bool HR, bool HB>
 __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ TravParams P)
 {
-    constexpr int LW = kWalkLW;
     constexpr int W = 1 << LW;
     constexpr int PP = 32 / W;                  // lanes (parts) per worker
-    static_assert(PP * kMaxE >= 32, "list entries");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_item;
     double2* const lntab = (double2*)smem;
@@ -247,6 +310,8 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     double* const out_rss = P.out_rss;
     double* const out_bic = P.out_bic;
     const double mhalf_n = P.mhalf_n;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);     // state of (row 0, slot 0, w)
+    const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb + w * 16);   // rec[slot 0][w]
     __syncthreads();
 
     for (;;) {
@@ -386,74 +451,66 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             const uint32_t S = Fw | Tsh;
             const uint32_t Tsh1 = Tsh >> 1;
             const double Kw = KC[dw + i + 1];
-            // this lane's free-list nibbles: entry h + 4j at bits 16j (j = 0, 1) / 16(j-2) (j = 2, 3)
+            // this lane's entries: e = h + PP j < L; free for e < nf
             const uint32_t nl = __funnelshift_r(rec.z, rec.w, 4 * h);
             const uint32_t nh = rec.w >> (4 * h);
             const bool seed = (rec.x >> 18) & 1u;
             StepV v;
-            v.bi = (unsigned)__cvta_generic_to_shared(sw + (i < 0 ? 0 : i) * RS);
-            v.rw = (unsigned)__cvta_generic_to_shared(rw);
-            v.RS = RS; v.h = h; v.L = L; v.nf = nf; v.kb = kb; v.nl = nl; v.nh = nh; v.absent = absent;
-            v.Tsh = Tsh; v.Tsh1 = Tsh1; v.c = c; v.sg = sg; v.Kw = Kw; v.seed0 = i < 0;
-            double rs[kMaxE], bics[kMaxE];
-            int sl[kMaxE];
+            v.bi = sbase + (i < 0 ? 0 : i) * RS;
+            v.bb0 = v.bi + (kb + h) * CSb;
+            v.rdelta = rbase - v.bi;
+            v.rb0 = rbase + (kb + h) * CSb;
+            v.RS = RS;
+            v.nvalid = w < nw ? (L - h + PP - 1) / PP : 0;   // lanes of absent workers (p < lw) store nothing
+            v.nfj = nf > h ? (nf - h + PP - 1) / PP : 0;
+            v.nl = nl;
+            v.nh = nh;
+            v.ab0 = (kb + h) < 32 ? absent >> (kb + h) : 0u;
+            v.Tsh = Tsh;
+            v.Tsh1 = Tsh1;
+            v.c = c;
+            v.sg = sg;
+            v.Kw = Kw;
+            v.seed0 = i < 0;
+            const bool has_next = !((nrec.x >> 18) & 1u);
+            const unsigned ncol = sbase + ((int)(nrec.x & 31u) - 1) * RS + (int)((nrec.x >> 9) & 15u) * CSb;
+            const unsigned pcol = v.bi + (int)((rec.x >> 9) & 15u) * CSb;
+            const bool pv = h == 0;
             const int ne = (L + PP - 1) / PP;
-#define BN_PA(SEEDV)                                                                      \
-    switch (ne) {                                                                         \
-        case 1: phase_a<SEEDV, 1, PP>(v, rs, sl); break;                                  \
-        case 2: phase_a<SEEDV, 2, PP>(v, rs, sl); break;                                  \
-        case 3: phase_a<SEEDV, 3, PP>(v, rs, sl); break;                                  \
-        case 4: phase_a<SEEDV, 4, PP>(v, rs, sl); break;                                  \
-        case 5: phase_a<SEEDV, 5, PP>(v, rs, sl); break;                                  \
-        case 6: phase_a<SEEDV, 6, PP>(v, rs, sl); break;                                  \
-        case 7: phase_a<SEEDV, 7, PP>(v, rs, sl); break;                                  \
-        default: phase_a<SEEDV, 8, PP>(v, rs, sl); break;                                 \
+            double cn = c, sn = sg, hn = hh;
+#define BN_STEP(SEEDV, NEV)                                                                                   \
+    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
+                                         hn, S, (double*)recb, bm)
+#define BN_SWITCH(SEEDV)                                                                                      \
+    switch (ne) {                                                                                             \
+        case 0: BN_STEP(SEEDV, 0); break;                                                                     \
+        case 1: BN_STEP(SEEDV, 1); break;                                                                     \
+        case 2: BN_STEP(SEEDV, 2); break;                                                                     \
+        case 3: BN_STEP(SEEDV, 3); break;                                                                     \
+        case 4: BN_STEP(SEEDV, 4); break;                                                                     \
+        case 5: BN_STEP(SEEDV, 5); break;                                                                     \
+        case 6: BN_STEP(SEEDV, 6); break;                                                                     \
+        case 7: BN_STEP(SEEDV, 7); break;                                                                     \
+        case 8: BN_STEP(SEEDV, 8); break;                                                                     \
+        case 9: BN_STEP(SEEDV, 9); break;                                                                     \
+        case 10: BN_STEP(SEEDV, 10); break;                                                                   \
+        case 11: BN_STEP(SEEDV, 11); break;                                                                   \
+        case 12: BN_STEP(SEEDV, 12); break;                                                                   \
+        case 13: BN_STEP(SEEDV, 13); break;                                                                   \
+        case 14: BN_STEP(SEEDV, 14); break;                                                                   \
+        case 15: BN_STEP(SEEDV, 15); break;                                                                   \
+        default: BN_STEP(SEEDV, 16); break;                                                                   \
     }
             if (seed) {
-                BN_PA(true)
+                BN_SWITCH(true)
             } else {
-                BN_PA(false)
-                if (h == 0) {
-                    // the pivot Y (now at position i): R_i = h, U_{i+1} = 0, R_{i+1} = 0
-                    unsigned char* const py = sw + i * RS + (int)((rec.x >> 9) & 15u) * CSb;
-                    *(double2*)py = make_double2(hh, 0.0);
-                    *(double*)(py + RS) = 0.0;
-                }
+                BN_SWITCH(false)
             }
-#undef BN_PA
-            __syncwarp();
-            // ---- the next step's rotation (entries (in, in+1) of its pivot column); overlaps phase C
-            if (!((nrec.x >> 18) & 1u)) {
-                const int in = (int)(nrec.x & 31u) - 1, Yn = (int)((nrec.x >> 9) & 15u);
-                const unsigned char* col = sw + in * RS + Yn * CSb;
-                givens(*(const double*)col, *(const double*)(col + RS), c, sg, hh);
-            }
-            // ---- phase C: BIC, table stores, running best (a8-a11)
-            uint32_t upd;
-            switch (ne) {
-                case 1: upd = phase_c<HR, HB, 1, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 2: upd = phase_c<HR, HB, 2, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 3: upd = phase_c<HR, HB, 3, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 4: upd = phase_c<HR, HB, 4, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 5: upd = phase_c<HR, HB, 5, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 6: upd = phase_c<HR, HB, 6, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                case 7: upd = phase_c<HR, HB, 7, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-                default: upd = phase_c<HR, HB, 8, PP>(v, lntab, mhalf_n, out_rss, out_bic, rs, sl, bics); break;
-            }
-            if (upd) {
-                // rare: a new best (or a tie, G14) for some (child, worker) of this lane
-                for (int j = 0; j < kMaxE; ++j) {
-                    if ((upd >> j) & 1u) {
-                        const int slot = sl[j];
-                        double* bp = (double*)(rw + slot * CSb);
-                        uint32_t* mp = bm + slot * W + w;
-                        if (tie_better(bics[j], S, *bp, *mp)) {
-                            *bp = bics[j];
-                            *mp = S;
-                        }
-                    }
-                }
-            }
+#undef BN_SWITCH
+#undef BN_STEP
+            c = cn;
+            sg = sn;
+            hh = hn;
             rec = nrec;
             // the gang's warps write the two halves of each 256 B region: keep them in step
             if (G > 1 && --bar_left == 0) {
@@ -495,36 +552,44 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     }
 }
 
-template <bool W1, bool HR, bool HB>
+template <int LW, bool W1, bool HR, bool HB>
 static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 {
-    const size_t smem = walk_cta_smem(P.m, P.k, P.S_alloc, P.g);
-    cudaError_t e = cudaFuncSetAttribute(walk_kernel<W1, HR, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = walk_cta_smem(P.m, P.k, P.S_alloc, P.g, LW);
+    auto f = walk_kernel<LW, W1, HR, HB>;
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    walk_kernel<W1, HR, HB><<<grid, 32 << P.g, smem, st>>>(P);
+    f<<<grid, 32 << P.g, smem, st>>>(P);
     return cudaGetLastError();
+}
+
+template <int LW>
+static cudaError_t launch_lw(const TravParams& P, int grid, cudaStream_t st)
+{
+    const int key = (P.world1 ? 4 : 0) | (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
+    switch (key) {
+        case 7: return launch_w<LW, true, true, true>(P, grid, st);
+        case 6: return launch_w<LW, true, true, false>(P, grid, st);
+        case 5: return launch_w<LW, true, false, true>(P, grid, st);
+        case 4: return launch_w<LW, true, false, false>(P, grid, st);
+        case 3: return launch_w<LW, false, true, true>(P, grid, st);
+        case 2: return launch_w<LW, false, true, false>(P, grid, st);
+        case 1: return launch_w<LW, false, false, true>(P, grid, st);
+        default: return launch_w<LW, false, false, false>(P, grid, st);
+    }
 }
 
 cudaError_t launch_walk(const TravParams& P, int grid, cudaStream_t st)
 {
-    const int key = (P.world1 ? 4 : 0) | (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
-    switch (key) {
-        case 7: return launch_w<true, true, true>(P, grid, st);
-        case 6: return launch_w<true, true, false>(P, grid, st);
-        case 5: return launch_w<true, false, true>(P, grid, st);
-        case 4: return launch_w<true, false, false>(P, grid, st);
-        case 3: return launch_w<false, true, true>(P, grid, st);
-        case 2: return launch_w<false, true, false>(P, grid, st);
-        case 1: return launch_w<false, false, true>(P, grid, st);
-        default: return launch_w<false, false, false>(P, grid, st);
-    }
+    return P.lw == 4 ? launch_lw<4>(P, grid, st) : launch_lw<3>(P, grid, st);
 }
 
-int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1)
+int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw)
 {
-    const size_t smem = walk_cta_smem(m, k, S_alloc, g);
+    const size_t smem = walk_cta_smem(m, k, S_alloc, g, lw);
     int n = 0;
-    auto f = world1 ? walk_kernel<true, true, true> : walk_kernel<false, true, true>;
+    auto f = lw == 4 ? (world1 ? walk_kernel<4, true, true, true> : walk_kernel<4, false, true, true>)
+                     : (world1 ? walk_kernel<3, true, true, true> : walk_kernel<3, false, true, true>);
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 32 << g, smem) != cudaSuccess) return 0;
     return n;
