@@ -75,6 +75,8 @@ struct bnreg {
     std::vector<WalkClass> classes;
     int nparts = 0;                // rows of d_part_bic / d_part_mask
     unsigned* d_counters = nullptr;
+    uint4* d_wsteps = nullptr;     // per-class walk step tables (plan.h WalkStep)
+    size_t wsteps_len = 0;         // steps per class table
     int bar_every = 1;
 };
 
@@ -94,7 +96,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters};
+                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters, h->d_wsteps};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -245,6 +247,19 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             h->nparts = 1;
         }
         CKH(cudaMalloc(&h->d_counters, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned)));
+        {
+            const auto recs = step_records(P.k, P.sched);
+            h->wsteps_len = recs.size();
+            std::vector<WalkStep> all;
+            for (auto& c : h->classes) {
+                auto tb = walk_step_table(recs, P.k, c.S_alloc, 1 << P.lw);
+                all.insert(all.end(), tb.begin(), tb.end());
+            }
+            if (!all.empty()) {
+                CKH(cudaMalloc(&h->d_wsteps, all.size() * sizeof(WalkStep)));
+                CKH(cudaMemcpy(h->d_wsteps, all.data(), all.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
+            }
+        }
         if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(1, atoi(be));
     } else {
         int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
@@ -489,6 +504,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
             T.item_begin = C.begin;
             T.item_end = C.end;
             T.part_base = C.part_base;
+            T.wsteps = h->d_wsteps + 2 * c * h->wsteps_len;
             CK(launch_walk(T, C.grid, st));
         }
     } else {

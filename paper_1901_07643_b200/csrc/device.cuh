@@ -86,6 +86,24 @@ __device__ __forceinline__ double fast_ln9(double x, const double2* tab)
     return fma(u, q, base);
 }
 
+// fast_ln9 with the table addressed in the shared window (tab = shared address).
+__device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
+{
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int e = (hi >> 20) - 1023;
+    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    double tx, ty;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ((hi >> 7) & 0x1ff0)));
+    const double ed = (double)e;
+    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], ty));
+    const double u = fma(f, tx, -1.0);
+    const double u2 = u * u;
+    const double a = fma(u, c_ln[0], 1.0);
+    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double q = fma(u2, b, a);
+    return fma(u, q, base);
+}
+
 // Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
 __device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
 

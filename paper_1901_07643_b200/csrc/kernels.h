@@ -36,6 +36,7 @@ struct TravParams {
     int part_base;              // first row of this launch's warps in part_bic / part_mask
     int bar_every;              // gang barrier every bar_every steps
     int lw;                     // log2 workers per warp
+    const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, 2 x uint4 per step)
 };
 
 // walk kernel: 2^lw lockstep workers per warp (lw = 3 or 4), gang of 2^g warps per CTA

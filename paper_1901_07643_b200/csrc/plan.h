@@ -113,6 +113,49 @@ inline std::vector<StepRec> step_records(int k, const std::vector<int8_t>& sched
     return out;
 }
 
+// The walk kernel's per-step table for one shared-memory class: the step
+// records above turned into byte offsets of its walk-state layout (slot stride
+// CS = W*16 bytes, row stride RS = SA*W*16 bytes), two uint4 per step:
+//   [0] x: i*RS (0 for i < 0)        y: i*RS + Y*CS (the pivot column after the swap)
+//       z: in*RS + Yn*CS (the next step's pivot column, if it is a GRC)
+//       w: (k - nf)*CS (back entry e -> slot k - nf + e)
+//   [1] x: T (free-slot mask of the new prefix set)  y, z: free-list nibbles
+//       w: nf | seed << 5 | (i < 0) << 6 | next-is-GRC << 7 | (i + 1) << 8
+struct WalkStep {
+    uint32_t offA, offP, offN, kbCS, T, nlo, nhi, flags;
+};
+
+inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, int k, int SA, int W)
+{
+    const uint32_t CS = (uint32_t)W * 16u, RS = (uint32_t)SA * W * 16u;
+    std::vector<WalkStep> out(recs.size());
+    for (size_t t = 0; t < recs.size(); ++t) {
+        const StepRec& r = recs[t];
+        const int i = (int)(r.meta & 31u) - 1;
+        const int Y = (int)((r.meta >> 9) & 15u);
+        const int nf = (int)((r.meta >> 13) & 31u);
+        const bool seed = (r.meta >> 18) & 1u;
+        WalkStep w{};
+        w.offA = i < 0 ? 0u : (uint32_t)i * RS;
+        w.offP = seed ? 0u : (uint32_t)i * RS + (uint32_t)Y * CS;
+        bool next = false;
+        if (t + 1 < recs.size() && !((recs[t + 1].meta >> 18) & 1u)) {
+            next = true;
+            const int in = (int)(recs[t + 1].meta & 31u) - 1;
+            const int Yn = (int)((recs[t + 1].meta >> 9) & 15u);
+            w.offN = (uint32_t)in * RS + (uint32_t)Yn * CS;
+        }
+        w.kbCS = (uint32_t)(k - nf) * CS;
+        w.T = r.T;
+        w.nlo = r.lo;
+        w.nhi = r.hi;
+        w.flags = (uint32_t)nf | ((seed ? 1u : 0u) << 5) | ((i < 0 ? 1u : 0u) << 6) | ((next ? 1u : 0u) << 7) |
+                  ((uint32_t)(i + 1) << 8);
+        out[t] = w;
+    }
+    return out;
+}
+
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
     int variant = 0;                          // kernel_variant() at plan time

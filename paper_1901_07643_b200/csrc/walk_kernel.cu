@@ -183,10 +183,10 @@ __device__ __forceinline__ unsigned entry_addr(const StepV& v, int j)
 //   phase C  ln RSS, BIC (a9), the two table stores (a10), running-best
 //            candidates; new bests (rare) resolved at the end (a11, G14).
 template <bool SEED, int NE, int PP, int CSB, bool HR, bool HB>
-__device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
+__device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double mhalf_n, double* out_rss,
                                           double* out_bic, bool pivot, unsigned pcol, double hh, bool has_next,
-                                          unsigned ncol, double& cn, double& sn, double& hn, uint32_t S, double* bbw,
-                                          uint32_t* bmw)
+                                          unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
+                                          unsigned rec_sh, unsigned bm_sh)
 {
     constexpr int NA = NE > 0 ? NE : 1;                       // (NE = 0: an empty list, e.g. the last seed step)
     double rs[NA];
@@ -227,7 +227,7 @@ __device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, 
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
         const double rss = rs[j];
-        const double lnr = fast_ln9(rss, lntab);
+        const double lnr = fast_ln9s(rss, lntab);
         double bic = fma(mhalf_n, lnr, v.Kw);
         bic = rss > 1e-300 ? bic : PINF;                            // G13
         bics[j] = bic;
@@ -245,17 +245,19 @@ __device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, 
         upd |= (ok && bic >= bb) ? (1u << j) : 0u;
     }
     if (upd) {
-        // rare: a new best (or a tie) for some (child, worker) of this lane
+        // rare: a family beats (or ties, G14) the running best of its (child, worker)
 #pragma unroll
         for (int j = 0; j < NE; ++j) {
             if ((upd >> j) & 1u) {
                 const unsigned ra = (j < JF) ? ad[j] + v.rdelta : v.rb0 + j * (PP * CSB);
-                double* bp = (double*)__cvta_shared_to_generic(ra);
-                const int q = (int)((ra - (unsigned)__cvta_generic_to_shared(bbw)) / 16u);   // (slot, w) record index
-                uint32_t* mp = bmw + q;
-                if (tie_better(bics[j], S, *bp, *mp)) {
-                    *bp = bics[j];
-                    *mp = S;
+                const unsigned ma = bm_sh + ((ra - rec_sh) >> 2);   // bm[slot][w] beside rec[slot][w]
+                double cb;
+                uint32_t cm;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ra));
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(ma));
+                if (tie_better(bics[j], S, cb, cm)) {
+                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(ra), "d"(bics[j]) : "memory");
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
                 }
             }
         }
@@ -264,14 +266,14 @@ __device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, 
 
 // NE-dispatch of the step body (NE = entries per lane, at most 32 / PP).
 template <bool SEED, int PP, int CSB, bool HR, bool HB, int NE>
-__device__ __forceinline__ void step_ne(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
+__device__ __forceinline__ void step_ne(const StepV& v, unsigned lntab, double mhalf_n, double* out_rss,
                                         double* out_bic, bool pv, unsigned pcol, double hh, bool has_next,
-                                        unsigned ncol, double& cn, double& sn, double& hn, uint32_t S, double* bbw,
-                                        uint32_t* bmw)
+                                        unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
+                                        unsigned rec_sh, unsigned bm_sh)
 {
     if constexpr (NE * PP <= 32)
         walk_step<SEED, NE, PP, CSB, HR, HB>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn,
-                                             hn, S, bbw, bmw);
+                                             hn, S, rec_sh, bm_sh);
 }
 
 template <int LW, bool WORLD1, bool HR, bool HB>
@@ -312,6 +314,10 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     const double mhalf_n = P.mhalf_n;
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);     // state of (row 0, slot 0, w)
     const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb + w * 16);   // rec[slot 0][w]
+    const unsigned kcbase = (unsigned)__cvta_generic_to_shared(KC);
+    const unsigned recb_sh = (unsigned)__cvta_generic_to_shared(recb);
+    const unsigned bm_sh = (unsigned)__cvta_generic_to_shared(bm);
+    const unsigned lnbase = (unsigned)__cvta_generic_to_shared(lntab);
     __syncthreads();
 
     for (;;) {
@@ -422,10 +428,12 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                     const uint32_t lm = (1u << v) - 1u;
                     const uint32_t idx = (uint32_t)((long long)v << shb) + block_offset<WORLD1>(P, Fw0, Fw0 >> 1, lm);
                     unsigned char* r = recb + (s * W + w) * 16;
-                    *(double*)r = NINF;
+                    // the running best of (child v, worker w) starts at the warp's best for v so
+                    // far: only families that beat it (rare after the first items) take the update path
+                    *(double*)r = wbb[v];
                     *(uint32_t*)(r + 8) = idx;
                     *(uint32_t*)(r + 12) = lm;
-                    bm[s * W + w] = 0xffffffffu;
+                    bm[s * W + w] = wbm[v];
                 }
             }
         }
@@ -436,51 +444,51 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         const int dw = __popc(Fw);
         const uint32_t absent = (w < nw) ? ((uint32_t)w << k) : 0xffffffffu;
         const int NB = Sw - k;
-        unsigned char* const sw = st + w * 16;
-        unsigned char* const rw = recb + w * 16;
         double c = 1.0, sg = 0.0, hh = 0.0;
         int bar_left = P.bar_every;
-        uint4 rec = __ldg(P.steps);
+        const unsigned sb_h = sbase + h * CSb;              // + kbCS: the lane's first back entry
+        const unsigned rb_h = rbase + h * CSb;
+        const uint32_t ab_h = absent >> h;
+        const unsigned kc_w = kcbase + dw * 8;               // K(|S|) = KC[dw + i + 1]
+        uint4 r0 = __ldg(P.wsteps), r1 = __ldg(P.wsteps + 1);
         for (int t = 0; t < P.nsteps; ++t) {
-            const uint4 nrec = (t + 1 < P.nsteps) ? __ldg(P.steps + t + 1) : make_uint4(1u << 18, 0, 0, 0);
-            const int i = (int)(rec.x & 31u) - 1;
-            const int nf = (int)((rec.x >> 13) & 31u);
-            const int L = nf + NB;
-            const int kb = k - nf;                               // back entry e -> slot kb + e
-            const uint32_t Tsh = rec.y << fv0;                   // the free part of the prefix set
+            const uint4 q0 = r0, q1 = r1;
+            if (t + 1 < P.nsteps) {
+                r0 = __ldg(P.wsteps + 2 * t + 2);
+                r1 = __ldg(P.wsteps + 2 * t + 3);
+            }
+            const uint32_t fl = q1.w;
+            const uint32_t nf = fl & 31u;
+            const uint32_t L = nf + (uint32_t)NB;
+            const uint32_t Tsh = q1.x << fv0;                    // the free part of the prefix set
             const uint32_t S = Fw | Tsh;
-            const uint32_t Tsh1 = Tsh >> 1;
-            const double Kw = KC[dw + i + 1];
-            // this lane's entries: e = h + PP j < L; free for e < nf
-            const uint32_t nl = __funnelshift_r(rec.z, rec.w, 4 * h);
-            const uint32_t nh = rec.w >> (4 * h);
-            const bool seed = (rec.x >> 18) & 1u;
             StepV v;
-            v.bi = sbase + (i < 0 ? 0 : i) * RS;
-            v.bb0 = v.bi + (kb + h) * CSb;
+            v.bi = sbase + q0.x;
+            v.bb0 = sb_h + q0.x + q0.w;
             v.rdelta = rbase - v.bi;
-            v.rb0 = rbase + (kb + h) * CSb;
+            v.rb0 = rb_h + q0.w;
             v.RS = RS;
-            v.nvalid = w < nw ? (L - h + PP - 1) / PP : 0;   // lanes of absent workers (p < lw) store nothing
-            v.nfj = nf > h ? (nf - h + PP - 1) / PP : 0;
-            v.nl = nl;
-            v.nh = nh;
-            v.ab0 = (kb + h) < 32 ? absent >> (kb + h) : 0u;
+            v.nvalid = w < nw ? (int)((L + (PP - 1) - h) / PP) : 0;  // lanes of absent workers (p < lw) store nothing
+            v.nfj = (int)((nf + (PP - 1) - min((uint32_t)h, nf)) / PP);
+            v.nl = __funnelshift_r(q1.y, q1.z, 4 * h);
+            v.nh = q1.z >> (4 * h);
+            v.ab0 = ab_h >> (q0.w / CSb);
             v.Tsh = Tsh;
-            v.Tsh1 = Tsh1;
+            v.Tsh1 = Tsh >> 1;
             v.c = c;
             v.sg = sg;
-            v.Kw = Kw;
-            v.seed0 = i < 0;
-            const bool has_next = !((nrec.x >> 18) & 1u);
-            const unsigned ncol = sbase + ((int)(nrec.x & 31u) - 1) * RS + (int)((nrec.x >> 9) & 15u) * CSb;
-            const unsigned pcol = v.bi + (int)((rec.x >> 9) & 15u) * CSb;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.Kw) : "r"(kc_w + ((fl >> 8) & 31u) * 8));
+            v.seed0 = (fl >> 6) & 1u;
+            const bool seed = (fl >> 5) & 1u;
+            const bool has_next = (fl >> 7) & 1u;
+            const unsigned ncol = sbase + q0.z;
+            const unsigned pcol = sbase + q0.y;
             const bool pv = h == 0;
-            const int ne = (L + PP - 1) / PP;
+            const int ne = (int)((L + (PP - 1)) / PP);
             double cn = c, sn = sg, hn = hh;
 #define BN_STEP(SEEDV, NEV)                                                                                   \
-    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
-                                         hn, S, (double*)recb, bm)
+    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lnbase, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
+                                         hn, S, recb_sh, bm_sh)
 #define BN_SWITCH(SEEDV)                                                                                      \
     switch (ne) {                                                                                             \
         case 0: BN_STEP(SEEDV, 0); break;                                                                     \
@@ -511,7 +519,6 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             c = cn;
             sg = sn;
             hh = hn;
-            rec = nrec;
             // the gang's warps write the two halves of each 256 B region: keep them in step
             if (G > 1 && --bar_left == 0) {
                 bar_left = P.bar_every;
