@@ -38,6 +38,7 @@ namespace bnr {
 
 constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
+constexpr int kMaxFreeWalk = 9;  // walk kernel: a step's free list (<= 8 slots) fits one u32 of nibbles
 constexpr int kPackBits = 3;     // 8 lockstep workers per warp (walk kernel)
 constexpr int kPackBitsLegacy = 2;  // 4 per warp (legacy traversal kernels, BNREG_LEGACY_TRAVERSE / BNREG_WS_TRAVERSE)
 
@@ -209,6 +210,8 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     // k = 9: the column stride is (k|1) 16 B, so k = 8 and k = 9 take the same shared memory
     if (k <= 0) k = std::min(m, 9);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
+    if (kernel_variant() == 0 && k > kMaxFreeWalk)
+        throw std::invalid_argument("the walk kernel takes at most 9 free variables (k <= 9)");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.variant = kernel_variant();
     P.lw = kPackBits;

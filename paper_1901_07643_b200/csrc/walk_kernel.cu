@@ -164,7 +164,7 @@ constexpr int kMaxE = 16;   // list entries per lane and step (PP * kMaxE >= 32 
 template <int PP, int CSB>
 __device__ __forceinline__ unsigned entry_addr(const StepV& v, int j)
 {
-    constexpr int JF = (15 + PP - 1) / PP;                   // free entries only for e < nf <= 15
+    constexpr int JF = 8 / PP;                               // free entries only for e < nf <= k - 1 <= 8
     const unsigned back = v.bb0 + j * (PP * CSB);
     if (j < JF) {
         const int sh = 4 * PP * j;                           // nibble of entry e = h + PP j
@@ -221,7 +221,7 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
         givens_fr(a, b, cn, sn, hn);
     }
     const double PINF = __longlong_as_double(0x7ff0000000000000LL);
-    constexpr int JF = (15 + PP - 1) / PP;
+    constexpr int JF = 8 / PP;
     uint32_t upd = 0;
     double bics[NA];
 #pragma unroll

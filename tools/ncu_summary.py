@@ -16,7 +16,11 @@ def page(args):
 
 rows = page(["--page", "raw", "--csv"])
 h = rows[0]
-d = dict(zip(h, rows[2]))
+# several launches captured: summarise the longest one
+ti = h.index("gpu__time_duration.sum")
+best = max(range(2, len(rows)), key=lambda r: float(rows[r][ti] or 0))
+d = dict(zip(h, rows[best]))
+launch_id = d.get("ID")
 for k in ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
           "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
           "dram__bytes_write.sum", "dram__bytes_read.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -25,9 +29,20 @@ for k in ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_acti
           "launch__shared_mem_per_block_dynamic", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]:
     print(f"  {k:70s} {d.get(k)}")
 rows = page(["--page", "source", "--csv", "--print-source", "sass"])
-hi = next(i for i, x in enumerate(rows) if x and x[0] == "Address")
-h = rows[hi]
-data = rows[hi + 1:]
+heads = [i for i, x in enumerate(rows) if x and x[0] == "Address"]
+def section(k):
+    h = rows[heads[k]]
+    end = heads[k + 1] if k + 1 < len(heads) else len(rows)
+    return h, [x for x in rows[heads[k] + 1:end] if len(x) == len(h)]
+
+
+def weight(k):
+    h, data = section(k)
+    ei = h.index("Instructions Executed")
+    return sum(float(x[ei] or 0) for x in data)
+
+
+h, data = section(max(range(len(heads)), key=weight))   # the launch with the most instructions
 si, ei = h.index("Source"), h.index("Instructions Executed")
 sc = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
 tot = collections.Counter()
@@ -52,3 +67,23 @@ if len(sys.argv) > 3:
         for i, x in enumerate(data):
             if vals[i] >= 0.1 * mx:
                 f.write(f"{i:5d} {vals[i] / mx:6.3f} {x[si].strip()[:100]}\n")
+
+if len(sys.argv) > 4:
+    # basic blocks (runs of equal execution count) by instruction share
+    si, ei = h.index("Source"), h.index("Instructions Executed")
+    vals = [float(x[ei] or 0) for x in data]
+    tot = sum(vals) or 1
+    blocks, start = [], 0
+    for i in range(1, len(vals) + 1):
+        if i == len(vals) or vals[i] != vals[start]:
+            blocks.append((start, i, vals[start] * (i - start), vals[start]))
+            start = i
+    blocks.sort(key=lambda b: -b[2])
+    acc = 0
+    for b in blocks[:int(sys.argv[4])]:
+        acc += b[2]
+        ops = collections.Counter(data[j][si].strip().split()[0].lstrip("@!P0123456789T ").split(".")[0]
+                                  if not data[j][si].strip().startswith("@") else data[j][si].strip().split()[1].split(".")[0]
+                                  for j in range(b[0], b[1]))
+        print(f"{b[0]:5d}-{b[1]:5d} n={b[1] - b[0]:3d} cnt={b[3]:.3e} share={100 * b[2] / tot:5.2f}% cum={100 * acc / tot:5.1f}% "
+              + " ".join(f"{o}:{c}" for o, c in ops.most_common(6)))
