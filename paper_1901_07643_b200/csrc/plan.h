@@ -207,8 +207,9 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (n < m + 1) throw std::invalid_argument("need n >= m + 1");
     if (world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
         throw std::invalid_argument("world must be a power of two and 0 <= rank < world");
-    // k = 9: the column stride is (k|1) 16 B, so k = 8 and k = 9 take the same shared memory
-    if (k <= 0) k = std::min(m, 9);
+    // default k: the walk kernel's shared memory grows with k (k rows of state per slot);
+    // k = 8 balances it against the seed derivation (~2k GRCs per worker, 2^k - k - 1 walk steps)
+    if (k <= 0) k = std::min(m, kernel_variant() == 0 ? 8 : 9);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
     if (kernel_variant() == 0 && k > kMaxFreeWalk)
         throw std::invalid_argument("the walk kernel takes at most 9 free variables (k <= 9)");

@@ -214,10 +214,16 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
     }
     if (!SEED && pivot) sts_pair_if(pcol, hh, 0.0, 0.0, v.RS, true);
     __syncwarp();
-    if (has_next) {
+    {
+        // unconditional (no branch: the chain interleaves with phase C); without a next
+        // GRC the table points at a valid slot and the result is unused
         double a, b;
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(ncol));
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(ncol + v.RS));
+        if (!has_next) {
+            a = 0.0;
+            b = 1.0;
+        }
         givens_fr(a, b, cn, sn, hn);
     }
     const double PINF = __longlong_as_double(0x7ff0000000000000LL);
