@@ -76,8 +76,10 @@ struct bnreg {
     int nparts = 0;                // rows of d_part_bic / d_part_mask
     unsigned* d_counters = nullptr;
     uint4* d_wsteps = nullptr;     // per-class walk step tables (plan.h WalkStep)
+    unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
+    std::vector<size_t> seed_off;       // byte offset of each class's blocks
     size_t wsteps_len = 0;         // steps per class table
-    int bar_every = 1;
+    int bar_every = 0;             // gang barrier every n walk steps (0: none; measured faster without)
 };
 
 static bnreg_options defaults(const bnreg_options* o)
@@ -96,7 +98,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters, h->d_wsteps};
+                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -226,6 +228,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory"));
             int64_t i1 = i0 + 1;
             while (i1 < ni) {
+                if (h->classes.size() + 1 >= (size_t)kMaxClasses) { i1 = ni; break; }   // the rest in one class
                 const int S1 = m - popc(P.packs[i1] & ((1u << gs) - 1u));
                 const int o1 = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S1, P.g, P.world == 1, P.lw);
                 if (o1 != occ) break;
@@ -238,6 +241,14 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             h->nparts += c.grid * h->wpc;
             h->classes.push_back(c);
             i0 = i1;
+        }
+        {
+            size_t off = 0;
+            for (auto& c : h->classes) {
+                h->seed_off.push_back(off);
+                off += (size_t)(c.end - c.begin) * (size_t)h->wpc * seed_block_bytes(P.k, c.S_alloc, P.lw);
+            }
+            CKH(cudaMalloc(&h->d_seeds, std::max<size_t>(off, 16)));
         }
         if (getenv("BNREG_VERBOSE"))
             for (auto& c : h->classes)
@@ -260,7 +271,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
                 CKH(cudaMemcpy(h->d_wsteps, all.data(), all.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
             }
         }
-        if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(1, atoi(be));
+        if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(0, atoi(be));
     } else {
         int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
         int64_t want = (int64_t)h->num_sms * per_sm;
@@ -497,6 +508,21 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         T.bar_every = h->bar_every;
         T.lw = P.lw;
         CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
+        // a5: every pack's seeds, in the walk kernel's layout
+        SeedParams SP{};
+        SP.m = P.m; SP.k = P.k; SP.p = P.p; SP.bh = P.bh; SP.g = P.g; SP.L1 = P.L1; SP.nw = 1 << P.p; SP.lw = P.lw;
+        SP.nclass = (int)h->classes.size();
+        for (size_t c = 0; c < h->classes.size(); ++c) {
+            SP.cls_begin[c] = h->classes[c].begin;
+            SP.cls_end[c] = h->classes[c].end;
+            SP.cls_SA[c] = h->classes[c].S_alloc;
+            SP.cls_off[c] = h->seed_off[c];
+        }
+        SP.item_begin = 0;
+        SP.item_end = (int)P.packs.size();
+        SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = h->d_seeds;
+        CK(launch_seed(SP, st));
+        if (h->timing) CK(cudaEventRecord(h->ev[1], st));
         for (size_t c = 0; c < h->classes.size(); ++c) {
             const auto& C = h->classes[c];
             T.counter = h->d_counters + c;
@@ -505,6 +531,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
             T.item_end = C.end;
             T.part_base = C.part_base;
             T.wsteps = h->d_wsteps + 2 * c * h->wsteps_len;
+            T.seeds = h->d_seeds + h->seed_off[c];
             CK(launch_walk(T, C.grid, st));
         }
     } else {

@@ -37,7 +37,25 @@ struct TravParams {
     int bar_every;              // gang barrier every bar_every steps
     int lw;                     // log2 workers per warp
     const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, 2 x uint4 per step)
+    const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
 };
+
+// seed kernel: one warp per pack derives its 2^p workers' seeds (the remaining
+// tree levels + the Gray path over the warp variables) and writes them in the
+// walk kernel's state layout to `seeds` (one block per (item, warp) of each class)
+constexpr int kMaxClasses = 8;
+struct SeedParams {
+    int m, k, p, bh, g, L1, nw, lw;
+    int nclass;
+    int cls_begin[kMaxClasses], cls_end[kMaxClasses], cls_SA[kMaxClasses];
+    unsigned long long cls_off[kMaxClasses];   // byte offset of the class's first block
+    int item_begin, item_end;                  // items (gangs) of this launch
+    const double* nodes;                       // seed-tree nodes at depth L1
+    const uint32_t* packs;
+    unsigned char* seeds;
+};
+__host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw);
+cudaError_t launch_seed(const SeedParams& P, cudaStream_t st);
 
 // walk kernel: 2^lw lockstep workers per warp (lw = 3 or 4), gang of 2^g warps per CTA
 size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);

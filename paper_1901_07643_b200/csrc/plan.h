@@ -216,7 +216,6 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.variant = kernel_variant();
     P.lw = kPackBits;
-    if (const char* e = std::getenv("BNREG_WALK_LW")) P.lw = (std::atoi(e) == 4) ? 4 : 3;
     P.p = std::min(P.variant == 0 ? P.lw : kPackBitsLegacy, P.b);
     P.bh = P.b - P.p;
     // walk kernel: a CTA's 2^g warps x 2^lw workers = 32 workers = 256 B per (child, step)

@@ -24,6 +24,7 @@
 //     block: k + j GRCs), each seed converted into its worker's walk state.
 #include <cstdint>
 #include <cmath>
+#include <algorithm>
 #include "kernels.h"
 #include "device.cuh"
 
@@ -52,8 +53,7 @@ __host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
     o += al16(k * SA * W * 16);
     L.scratch = o;
     L.bm = o + SA * W * 16;
-    const int tri = (m * (m + 1) / 2) * 8, rec = SA * W * 20;
-    o += al16(tri > rec ? tri : rec);
+    o += al16(SA * W * 20);
     L.wbb = o;
     o += 32 * 8;
     L.wbm = o;
@@ -80,32 +80,6 @@ __device__ __forceinline__ void grc_pv(double* A, int s, int J, int lane, int& m
     grc_packed(A, s, J, s, lane);
     const int src = lane == J ? J + 1 : (lane == J + 1 ? J : lane);
     myvar = __shfl_sync(FULLMASK, myvar, src);
-}
-
-// Seed -> walk state of worker wc: the sub-triangle from position og (side
-// sn - og) = [free block (k) | back columns]; lane = position q.  For every
-// column: its free rows og..og+k-1 and the suffix sums of squares down to the
-// diagonal (rows below the free block form the tail), by addition from the
-// bottom.
-template <int W>
-__device__ __forceinline__ void snapshot(const double* A, int sn, int og, int k, int SA, int wc, int lane, int myvar,
-                                         const uint8_t* slotof, unsigned char* st)
-{
-    const int q = lane;
-    if (q >= og && q < sn) {
-        const int slot = slotof[myvar];
-        unsigned char* col = st + (slot * W + wc) * 16;
-        const int RS = SA * W * 16;
-        double acc = 0.0;
-        for (int l = q - og + 1; l < k; ++l)                 // rows below the diagonal (free columns)
-            *(double2*)(col + l * RS) = make_double2(0.0, 0.0);
-        for (int r = q; r >= og; --r) {
-            const double x = A[poff(r, sn) + q - r];
-            const int l = r - og;
-            if (l < k) *(double2*)(col + l * RS) = make_double2(x, acc);
-            acc = fma(x, x, acc);
-        }
-    }
 }
 
 // Predicated stores that stay predicated (no branch around them, so the
@@ -157,6 +131,26 @@ struct StepV {
     double Kw;            // BIC constant of |S|
     int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
 };
+
+// Seed -> walk state of worker wc, written to its part of a worker-major seed
+// block ([row l][slot] of 16 B E pairs, row stride SA*16): the sub-triangle from
+// position og = [free block (k) | back columns]; lane = position q.  Rows are
+// processed bottom-up in lockstep (suffix sums of squares by addition; rows
+// below the free block form the tail), so each row's stores are contiguous.
+__device__ __forceinline__ void snapshot_g(const double* A, int sn, int og, int k, int SA, int lane, int myvar,
+                                           const uint8_t* slotof, unsigned char* wblk)
+{
+    const int q = lane;
+    const bool mine = q >= og && q < sn;
+    const int slot = mine ? slotof[myvar] : 0;
+    double acc = 0.0;
+    for (int r = sn - 1; r >= og; --r) {
+        const double x = (mine && q >= r) ? A[poff(r, sn) + q - r] : 0.0;
+        const int l = r - og;
+        if (mine && l < k) *(double2*)(wblk + (l * SA + slot) * 16) = make_double2(x, acc);
+        acc = fma(x, x, acc);
+    }
+}
 
 constexpr int kMaxE = 16;   // list entries per lane and step (PP * kMaxE >= 32 > m - 1)
 
@@ -301,12 +295,10 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     const WalkLayout Ly = walk_layout(m, k, SA, W);
     unsigned char* const wb = smem + kWalkHead + wib * Ly.per_warp;
     unsigned char* const st = wb + Ly.state;
-    double* const tri = (double*)(wb + Ly.scratch);
     unsigned char* const recb = wb + Ly.scratch;            // rec[slot][w], 16 B
     uint32_t* const bm = (uint32_t*)(wb + Ly.bm);           // bm[slot][w]
     double* const wbb = (double*)(wb + Ly.wbb);
     uint32_t* const wbm = (uint32_t*)(wb + Ly.wbm);
-    uint8_t* const slotof = wb + Ly.slotof;
     const int w = lane & (W - 1), h = lane >> LW;
     const double NINF = -__longlong_as_double(0x7ff0000000000000LL);
     wbb[lane] = NINF;
@@ -341,40 +333,19 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         }
         const int Sw = k + p + nB;              // walk slots of this warp: free, warp vars, back set
 
-        // ---- a5: node at depth L1 (all loads in flight at once)
-        const uint32_t nid = pack & ((1u << P.L1) - 1u);
-        const int sn = m - __popc(nid);
+        // ---- a5: this warp's seeds (seed kernel): worker-major blocks [w][row l][slot] of
+        //      16 B E pairs, transposed into the interleaved state [l][slot][w] (cp.async)
         {
-            const double* src = P.nodes + (size_t)nid * m * m;
-            const int tot = sn * (sn + 1) / 2;
-            for (int e = lane; e < tot; e += 32) {
-                int r = (int)((2.0f * sn + 1.0f - sqrtf((2.0f * sn + 1.0f) * (2.0f * sn + 1.0f) - 8.0f * e)) * 0.5f);
-                if (r < 0) r = 0;
-                while (r > 0 && poff(r, sn) > e) --r;
-                while (r + 1 < sn && poff(r + 1, sn) <= e) ++r;
-                const int c = r + (e - poff(r, sn));
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(tri + e);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + c));
+            const unsigned char* src =
+                P.seeds + ((size_t)(item - P.item_begin) * G + wib) * (size_t)(k * RS);
+            const unsigned dst = sbase - w * 16;
+            for (int r = 0; r < nw * k; ++r) {          // (worker, row) pairs; lane = slot
+                const int ww = r / k, l = r - ww * k;
+                if (lane < Sw)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((l * SA + lane) * W + ww) * 16),
+                                 "l"(src + ((size_t)(ww * k + l) * SA + lane) * 16));
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-        }
-        // variable at each node position (lane = position):
-        // [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
-        int myvar = -1;                          // -1: no column at this position
-        {
-            const int nlev = bh - P.L1;
-            const int q = lane;
-            if (q < nlev) myvar = hv_of(P.L1 + q, m, gs, fv0);
-            else if (q < nlev + p) myvar = p - 1 - (q - nlev);
-            else if (q < nlev + p + k) myvar = fv0 + (q - nlev - p);
-            else if (q < sn) {
-                int c = q - nlev - p - k;
-                for (int l = P.L1 - 1; l >= 0; --l)
-                    if (!((pack >> l) & 1u)) {
-                        if (c == 0) { myvar = hv_of(l, m, gs, fv0); break; }
-                        --c;
-                    }
-            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
         // slot -> variable: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
         int slotvar = -1;
@@ -390,39 +361,8 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                         --c;
                     }
             }
-            slotof[slotvar] = (uint8_t)s;
         }
-        __syncwarp();
-        // remaining tree levels in-warp: F -> drop the leading row/column, B -> bubble it behind the free block
-        int org = 0;
-        for (int l = P.L1; l < bh; ++l) {
-            if ((pack >> l) & 1u) {
-                ++org;
-                continue;
-            }
-            const int T = (bh - l - 1) + p + k;
-            for (int j = 0; j < T; ++j) grc_pv(tri, sn, org + j, lane, myvar);
-        }
-        // Gray path over the warp variables: start with all of them in F (front
-        // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
-        // variable j across the free block and the j lower warp variables
-        int wcur = nw - 1;
-        snapshot<W>(tri, sn, org + p, k, SA, wcur, lane, myvar, slotof, st);
-        for (int i = 1; i < nw; ++i) {
-            const int j = __ffs(i) - 1;
-            const int pj = __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1;
-            const int d = k + j;
-            __syncwarp();
-            if ((wcur >> j) & 1) {
-                for (int t = 0; t < d; ++t) grc_pv(tri, sn, pj + t, lane, myvar);
-            } else {
-                for (int t = 1; t <= d; ++t) grc_pv(tri, sn, pj - t, lane, myvar);
-            }
-            wcur ^= 1 << j;
-            snapshot<W>(tri, sn, org + __popc(wcur), k, SA, wcur, lane, myvar, slotof, st);
-        }
-        __syncwarp();
-        // per (slot, worker) records (they overlay the triangle): running best,
+        // per (slot, worker) records: running best,
         // table index of (child v, F_w) -- the free part is added per step -- and lm
         {
             // lane = (slot group, worker): 4 slots per pass
@@ -443,6 +383,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                 }
             }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
 
         // ---- a6-a11: the walk, k+1 seed pseudo-steps then d + Upsilon(k), in lockstep
@@ -526,7 +467,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             sg = sn;
             hh = hn;
             // the gang's warps write the two halves of each 256 B region: keep them in step
-            if (G > 1 && --bar_left == 0) {
+            if (P.bar_every > 0 && G > 1 && --bar_left == 0) {
                 bar_left = P.bar_every;
                 __syncthreads();
             }
@@ -565,6 +506,140 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     }
 }
 
+// ---------------------------------------------------------------- a5: the seed kernel
+// One warp per pack (item, warp of the gang): the pack's node at tree depth L1
+// (tree_level_kernel), the remaining tree levels, then the W workers' seeds
+// along a Gray path over the warp variables, each converted into walk state
+// (E pairs of the free rows + suffix sums) and written to the pack's block of
+// `seeds` in the walk kernel's shared-memory layout.  Separate from the walk so
+// that its serial GRC chains run at high occupancy (triangle-only smem).
+__host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw) { return (size_t)k * S_alloc * (16u << lw); }
+
+template <int LW>
+__global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedParams P)
+{
+    constexpr int W = 1 << LW;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
+    const int fv0 = p + g, gs = bh - g, G = 1 << g;
+    const int tri_bytes = al16((m * (m + 1) / 2) * 8);
+    double* const tri = (double*)(smem + wib * (tri_bytes + 32));
+    uint8_t* const slotof = smem + wib * (tri_bytes + 32) + tri_bytes;
+    const int npk = (P.item_end - P.item_begin) * G;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
+        const int item = P.item_begin + q / G, gw = q % G;
+        int c = 0;
+        while (c + 1 < P.nclass && item >= P.cls_end[c]) ++c;
+        const int SA = P.cls_SA[c];
+        unsigned char* const blk =
+            P.seeds + P.cls_off[c] + ((size_t)(item - P.cls_begin[c]) * G + gw) * seed_block_bytes(k, SA, LW);
+        const uint32_t pack = P.packs[item] | ((uint32_t)gw << gs);
+        int nB = 0;
+        for (int l = 0; l < bh; ++l) nB += !((pack >> l) & 1u);
+        const int Sw = k + p + nB;
+        // the node at depth L1 (all loads in flight at once)
+        const uint32_t nid = pack & ((1u << P.L1) - 1u);
+        const int sn = m - __popc(nid);
+        {
+            const double* src = P.nodes + (size_t)nid * m * m;
+            const int tot = sn * (sn + 1) / 2;
+            for (int e = lane; e < tot; e += 32) {
+                int r = (int)((2.0f * sn + 1.0f - sqrtf((2.0f * sn + 1.0f) * (2.0f * sn + 1.0f) - 8.0f * e)) * 0.5f);
+                if (r < 0) r = 0;
+                while (r > 0 && poff(r, sn) > e) --r;
+                while (r + 1 < sn && poff(r + 1, sn) <= e) ++r;
+                const int cc = r + (e - poff(r, sn));
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(tri + e);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + cc));
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+        // variable at each node position (lane = position):
+        // [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
+        int myvar = -1;                          // -1: no column at this position
+        {
+            const int nlev = bh - P.L1;
+            const int qq = lane;
+            if (qq < nlev) myvar = hv_of(P.L1 + qq, m, gs, fv0);
+            else if (qq < nlev + p) myvar = p - 1 - (qq - nlev);
+            else if (qq < nlev + p + k) myvar = fv0 + (qq - nlev - p);
+            else if (qq < sn) {
+                int cc = qq - nlev - p - k;
+                for (int l = P.L1 - 1; l >= 0; --l)
+                    if (!((pack >> l) & 1u)) {
+                        if (cc == 0) { myvar = hv_of(l, m, gs, fv0); break; }
+                        --cc;
+                    }
+            }
+        }
+        // variable -> walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        if (lane < Sw) {
+            const int s = lane;
+            int v;
+            if (s < k) v = fv0 + s;
+            else if (s < k + p) v = s - k;
+            else {
+                int cc = s - k - p;
+                v = 0;
+                for (int l = bh - 1; l >= 0; --l)
+                    if (!((pack >> l) & 1u)) {
+                        if (cc == 0) { v = hv_of(l, m, gs, fv0); break; }
+                        --cc;
+                    }
+            }
+            slotof[v] = (uint8_t)s;
+        }
+        __syncwarp();
+        // remaining tree levels: F -> drop the leading row/column, B -> bubble it behind the free block
+        int org = 0;
+        for (int l = P.L1; l < bh; ++l) {
+            if ((pack >> l) & 1u) {
+                ++org;
+                continue;
+            }
+            const int T = (bh - l - 1) + p + k;
+            for (int j = 0; j < T; ++j) grc_pv(tri, sn, org + j, lane, myvar);
+        }
+        // Gray path over the warp variables: start with all of them in F (front
+        // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
+        // variable j across the free block and the j lower warp variables
+        int wcur = P.nw - 1;
+        const size_t wsz = (size_t)k * SA * 16;      // one worker's part of the block
+        snapshot_g(tri, sn, org + p, k, SA, lane, myvar, slotof, blk + wcur * wsz);
+        for (int i = 1; i < P.nw; ++i) {
+            const int j = __ffs(i) - 1;
+            const int pj = __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1;
+            const int d = k + j;
+            __syncwarp();
+            if ((wcur >> j) & 1) {
+                for (int t = 0; t < d; ++t) grc_pv(tri, sn, pj + t, lane, myvar);
+            } else {
+                for (int t = 1; t <= d; ++t) grc_pv(tri, sn, pj - t, lane, myvar);
+            }
+            wcur ^= 1 << j;
+            snapshot_g(tri, sn, org + __popc(wcur), k, SA, lane, myvar, slotof, blk + wcur * wsz);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
+{
+    const int m = P.m;
+    const size_t smem = (size_t)4 * (al16((m * (m + 1) / 2) * 8) + 32);
+    const int npk = (P.item_end - P.item_begin) << P.g;
+    if (npk <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min((npk + 3) / 4, sms * 16);
+    if (P.lw != 3) return cudaErrorInvalidValue;
+    seed_kernel<3><<<grid, 128, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
 template <int LW, bool W1, bool HR, bool HB>
 static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 {
@@ -594,15 +669,16 @@ static cudaError_t launch_lw(const TravParams& P, int grid, cudaStream_t st)
 
 cudaError_t launch_walk(const TravParams& P, int grid, cudaStream_t st)
 {
-    return P.lw == 4 ? launch_lw<4>(P, grid, st) : launch_lw<3>(P, grid, st);
+    if (P.lw != 3) return cudaErrorInvalidValue;   // 8 workers per warp (plan.h kPackBits)
+    return launch_lw<3>(P, grid, st);
 }
 
 int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw)
 {
     const size_t smem = walk_cta_smem(m, k, S_alloc, g, lw);
     int n = 0;
-    auto f = lw == 4 ? (world1 ? walk_kernel<4, true, true, true> : walk_kernel<4, false, true, true>)
-                     : (world1 ? walk_kernel<3, true, true, true> : walk_kernel<3, false, true, true>);
+    if (lw != 3) return 0;
+    auto f = world1 ? walk_kernel<3, true, true, true> : walk_kernel<3, false, true, true>;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 32 << g, smem) != cudaSuccess) return 0;
     return n;
