@@ -300,7 +300,7 @@ def bench_ours(args):
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_FAMILY * F / (trav_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(f"cfg{args.config}"), "kernel": "traverse_kernel",
+            "traffic": ncu_traffic(f"cfg{args.config}"), "kernel": "walk_kernel (all shared-memory classes of a step)",
             "kernel_ms": trav_ms, "algorithmic_bytes_per_launch": BYTES_PER_FAMILY * F,
             "peak_source": peak_src,
             "step_frac": (BYTES_PER_FAMILY * total * args.steps / (ms / 1e3) / 1e9) / peak / world}

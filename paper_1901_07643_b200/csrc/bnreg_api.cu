@@ -530,7 +530,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
             T.item_begin = C.begin;
             T.item_end = C.end;
             T.part_base = C.part_base;
-            T.wsteps = h->d_wsteps + 2 * c * h->wsteps_len;
+            T.wsteps = h->d_wsteps + c * h->wsteps_len;
             T.seeds = h->d_seeds + h->seed_off[c];
             CK(launch_walk(T, C.grid, st));
         }

@@ -36,7 +36,7 @@ struct TravParams {
     int part_base;              // first row of this launch's warps in part_bic / part_mask
     int bar_every;              // gang barrier every bar_every steps
     int lw;                     // log2 workers per warp
-    const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, 2 x uint4 per step)
+    const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, one uint4 per step)
     const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
 };
 

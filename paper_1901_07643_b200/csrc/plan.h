@@ -116,14 +116,13 @@ inline std::vector<StepRec> step_records(int k, const std::vector<int8_t>& sched
 
 // The walk kernel's per-step table for one shared-memory class: the step
 // records above turned into byte offsets of its walk-state layout (slot stride
-// CS = W*16 bytes, row stride RS = SA*W*16 bytes), two uint4 per step:
-//   [0] x: i*RS (0 for i < 0)        y: i*RS + Y*CS (the pivot column after the swap)
-//       z: in*RS + Yn*CS (the next step's pivot column, if it is a GRC)
-//       w: (k - nf)*CS (back entry e -> slot k - nf + e)
-//   [1] x: T (free-slot mask of the new prefix set)  y, z: free-list nibbles
-//       w: nf | seed << 5 | (i < 0) << 6 | next-is-GRC << 7 | (i + 1) << 8
+// CS = W*16 bytes, row stride RS = SA*W*16 bytes), one uint4 per step:
+//   x: i*RS (0 for i < 0)
+//   y: in*RS + Yn*CS, the next step's pivot column if the next step is a GRC (else 0)
+//   z: the free-list nibbles (k <= 9: the list after a prefix has <= 8 slots)
+//   w: nf | seed << 5 | (i < 0) << 6 | next-is-GRC << 7 | (i + 1) << 8 | Y << 13 | T << 17
 struct WalkStep {
-    uint32_t offA, offP, offN, kbCS, T, nlo, nhi, flags;
+    uint32_t offA, offN, nib, flags;
 };
 
 inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, int k, int SA, int W)
@@ -138,7 +137,6 @@ inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, i
         const bool seed = (r.meta >> 18) & 1u;
         WalkStep w{};
         w.offA = i < 0 ? 0u : (uint32_t)i * RS;
-        w.offP = seed ? 0u : (uint32_t)i * RS + (uint32_t)Y * CS;
         bool next = false;
         if (t + 1 < recs.size() && !((recs[t + 1].meta >> 18) & 1u)) {
             next = true;
@@ -146,12 +144,9 @@ inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, i
             const int Yn = (int)((recs[t + 1].meta >> 9) & 15u);
             w.offN = (uint32_t)in * RS + (uint32_t)Yn * CS;
         }
-        w.kbCS = (uint32_t)(k - nf) * CS;
-        w.T = r.T;
-        w.nlo = r.lo;
-        w.nhi = r.hi;
+        w.nib = r.lo;
         w.flags = (uint32_t)nf | ((seed ? 1u : 0u) << 5) | ((i < 0 ? 1u : 0u) << 6) | ((next ? 1u : 0u) << 7) |
-                  ((uint32_t)(i + 1) << 8);
+                  ((uint32_t)(i + 1) << 8) | ((uint32_t)(seed ? 0 : Y) << 13) | (r.T << 17);
         out[t] = w;
     }
     return out;

@@ -397,29 +397,29 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         const unsigned rb_h = rbase + h * CSb;
         const uint32_t ab_h = absent >> h;
         const unsigned kc_w = kcbase + dw * 8;               // K(|S|) = KC[dw + i + 1]
-        uint4 r0 = __ldg(P.wsteps), r1 = __ldg(P.wsteps + 1);
+        const int nv_h = (w < nw) ? NB + (PP - 1) - h : -64; // entries: nvalid = (nf + nv_h) / PP (absent workers: none)
+        const int nfj_h = (PP - 1) - h;                      // free entries: nfj = (nf + nfj_h) / PP
+        uint4 r0 = __ldg(P.wsteps);
         for (int t = 0; t < P.nsteps; ++t) {
-            const uint4 q0 = r0, q1 = r1;
-            if (t + 1 < P.nsteps) {
-                r0 = __ldg(P.wsteps + 2 * t + 2);
-                r1 = __ldg(P.wsteps + 2 * t + 3);
-            }
-            const uint32_t fl = q1.w;
-            const uint32_t nf = fl & 31u;
-            const uint32_t L = nf + (uint32_t)NB;
-            const uint32_t Tsh = q1.x << fv0;                    // the free part of the prefix set
+            const uint4 q = r0;
+            if (t + 1 < P.nsteps) r0 = __ldg(P.wsteps + t + 1);
+            const uint32_t fl = q.w;
+            const int nf = (int)(fl & 31u);
+            const int L = nf + NB;
+            const uint32_t Tsh = (fl >> 17) << fv0;              // the free part of the prefix set
             const uint32_t S = Fw | Tsh;
             StepV v;
-            v.bi = sbase + q0.x;
-            v.bb0 = sb_h + q0.x + q0.w;
+            v.bi = sbase + q.x;
+            const unsigned kbcs = (unsigned)(k - nf) * CSb;
+            v.bb0 = sb_h + q.x + kbcs;
             v.rdelta = rbase - v.bi;
-            v.rb0 = rb_h + q0.w;
+            v.rb0 = rb_h + kbcs;
             v.RS = RS;
-            v.nvalid = w < nw ? (int)((L + (PP - 1) - h) / PP) : 0;  // lanes of absent workers (p < lw) store nothing
-            v.nfj = (int)((nf + (PP - 1) - min((uint32_t)h, nf)) / PP);
-            v.nl = __funnelshift_r(q1.y, q1.z, 4 * h);
-            v.nh = q1.z >> (4 * h);
-            v.ab0 = ab_h >> (q0.w / CSb);
+            v.nvalid = (nf + nv_h) >> (5 - LW);               // / PP (arithmetic: negative = none)
+            v.nfj = (nf + nfj_h) >> (5 - LW);
+            v.nl = q.z >> (4 * h);
+            v.nh = 0;
+            v.ab0 = ab_h >> (k - nf);
             v.Tsh = Tsh;
             v.Tsh1 = Tsh >> 1;
             v.c = c;
@@ -428,10 +428,10 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             v.seed0 = (fl >> 6) & 1u;
             const bool seed = (fl >> 5) & 1u;
             const bool has_next = (fl >> 7) & 1u;
-            const unsigned ncol = sbase + q0.z;
-            const unsigned pcol = sbase + q0.y;
+            const unsigned ncol = sbase + q.y;
+            const unsigned pcol = v.bi + ((fl >> 13) & 15u) * CSb;
             const bool pv = h == 0;
-            const int ne = (int)((L + (PP - 1)) / PP);
+            const int ne = (L + PP - 1) >> (5 - LW);
             double cn = c, sn = sg, hn = hh;
 #define BN_STEP(SEEDV, NEV)                                                                                   \
     step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lnbase, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \

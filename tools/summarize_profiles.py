@@ -1,8 +1,11 @@
 """Summarise ncu outputs (launch list CSV + one --set full capture) into profiles/.
 
 usage: python tools/summarize_profiles.py <launches.csv> <prof.ncu-rep> <config> <tag>
-Writes profiles/<tag>_launches.md and profiles/<tag>_traverse_ncu.md, and
-profiles/traverse_ncu_summary.json (read by bench.py for roofline.traffic)."""
+Writes profiles/<tag>_launches.md and profiles/<tag>_walk_ncu.md, and
+profiles/traverse_ncu_summary.json (read by bench.py for roofline.traffic).
+The capture holds the walk kernel's launches of one step (one per shared-memory
+class): their DRAM bytes are summed (the bench's "dominant kernel" is all of
+them, timed together)."""
 import csv
 import json
 import os
@@ -43,39 +46,50 @@ open(os.path.join(out, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n"
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
-names, units, vals = r[0], r[1], r[2]
-d = {names[i]: (vals[i], units[i]) for i in range(len(names))}
+names, units = r[0], r[1]
+launch_rows = r[2:]
+
+
+def val(row, k):
+    i = names.index(k)
+    return float(row[i].replace(",", "") or 0), units[i]
+
+
+def to_bytes(v, u):
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
+
+
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.per_cycle_active",
+        "launch__grid_size", "launch__shared_mem_per_block_dynamic",
         "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
         "lts__t_sectors_op_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
-stall = [k for k in names if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued")]
-sv = sorted(((float(d[k][0].replace(",", "") or 0), k) for k in stall), reverse=True)
-st = sum(x for x, _ in sv) or 1
-md = [f"# {tag}: traverse_kernel, ncu --set full ({config})", "",
-      "One launch of the fused traversal kernel, `ncu --set full --clock-control none --import-source on`.", "",
-      "| metric | value |", "|---|---|"]
+md = [f"# {tag}: walk_kernel, ncu --set full ({config})", "",
+      f"The walk kernel's {len(launch_rows)} launch(es) of one step (one per shared-memory class), "
+      "`ncu --set full --clock-control none --import-source on`.", "",
+      "| metric | " + " | ".join(f"launch {j}" for j in range(len(launch_rows))) + " |",
+      "|---|" + "---|" * len(launch_rows)]
 for k in keys:
-    if k in d:
-        md.append(f"| {k} | {d[k][0]} {d[k][1]} |")
-md += ["", "| stall reason (pc sampling) | share |", "|---|---|"]
+    if k in names:
+        md.append(f"| {k} | " + " | ".join(f"{row[names.index(k)]} {units[names.index(k)]}" for row in launch_rows) + " |")
+# stall mix of the longest launch
+ti = names.index("gpu__time_duration.sum")
+big = max(launch_rows, key=lambda row: float(row[ti].replace(",", "") or 0))
+stall = [k for k in names if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued")]
+sv = sorted(((float(big[names.index(k)].replace(",", "") or 0), k) for k in stall), reverse=True)
+st = sum(x for x, _ in sv) or 1
+md += ["", "| stall reason (pc sampling, longest launch) | share |", "|---|---|"]
 for x, k in sv[:10]:
     md.append(f"| {k.replace('smsp__pcsamp_warps_issue_stalled_', '')} | {x / st:.3f} |")
-open(os.path.join(out, f"{tag}_traverse_ncu.md"), "w").write("\n".join(md) + "\n")
+open(os.path.join(out, f"{tag}_walk_ncu.md"), "w").write("\n".join(md) + "\n")
 
-
-def bytes_of(k):
-    v, u = d[k]
-    v = float(v.replace(",", ""))
-    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
-
-
-summary = {"config": config, "tag": tag,
-           "traffic_bytes_per_launch": bytes_of("dram__bytes_read.sum") + bytes_of("dram__bytes_write.sum"),
-           "dram_read_bytes": bytes_of("dram__bytes_read.sum"), "dram_write_bytes": bytes_of("dram__bytes_write.sum")}
+rd = sum(to_bytes(*val(row, "dram__bytes_read.sum")) for row in launch_rows)
+wr = sum(to_bytes(*val(row, "dram__bytes_write.sum")) for row in launch_rows)
+summary = {"config": config, "tag": tag, "kernel": "walk_kernel", "launches_per_step": len(launch_rows),
+           "traffic_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+           "note": "per step: the sum over the walk kernel's per-class launches"}
 json.dump(summary, open(os.path.join(out, "traverse_ncu_summary.json"), "w"), indent=1)
 print(open(os.path.join(out, f"{tag}_launches.md")).read())
-print(open(os.path.join(out, f"{tag}_traverse_ncu.md")).read())
-print(summary)
+print(open(os.path.join(out, f"{tag}_walk_ncu.md")).read())
