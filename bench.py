@@ -310,7 +310,7 @@ def bench_ours(args):
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{done} families uniformly sampled from cfg{args.config}'s {total} "
                          f"(O1 per-family Householder QR, n={n}), {el:.1f} s on the host"}
-    launches = args.steps * (plan["L1"] + 2 + (2 if rank == 0 else 0))
+    launches = args.steps * (h.launches_per_run() + (2 if rank == 0 else 0))
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,

@@ -140,6 +140,11 @@ bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, 
  * kernel, [3] = best reduce; *runs = number of runs accumulated. */
 bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* runs);
 
+/* Kernel launches of one bnreg_run / bnreg_run_async on this handle (the seed
+ * tree levels, the seed kernel, one walk launch per shared-memory class, the
+ * best reduction); bnreg_load adds 2 (centre, TSQR).  -1 for a NULL handle. */
+int64_t bnreg_launches_per_run(const bnreg_t* h);
+
 /* Plan introspection (host only, no GPU): info[0..11] = k, b, p, bh, L1, LW,
  * npacks (this rank), schedule length, local families, total families,
  * traversal smem bytes per warp, r (rank selector bits). */

@@ -26,7 +26,7 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
            "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
-           "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_plan_query",
+           "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
            "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_last_error", "bnreg_destroy"]
 
 
@@ -81,6 +81,7 @@ def lib():
         "bnreg_plan_local_index": ([i32, i64, POPT, i64], i64),
         "bnreg_best_merge": ([i32, i32, P, P, P, P], i32),
         "bnreg_timing": ([H, i32, P, P], i32),
+        "bnreg_launches_per_run": ([H], i64),
         "bnreg_plan_query": ([i32, i64, POPT, P], i32),
         "bnreg_schedule": ([i32, P, i64], i64),
         "bnreg_plan_packs": ([i32, i64, POPT, P, i64], i64),
@@ -244,6 +245,9 @@ class Bnreg:
         _check(lib().bnreg_shard_ranges(self._h, ctypes.byref(cnt), _hptr(starts), _hptr(lens)))
         c = cnt.value
         return starts[:c].copy(), lens[:c].copy()
+
+    def launches_per_run(self) -> int:
+        return lib().bnreg_launches_per_run(self._h)
 
     def timing(self, enable: int = -1):
         ms = np.zeros(4)

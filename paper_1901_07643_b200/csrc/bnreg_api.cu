@@ -399,6 +399,13 @@ bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host)
 
 int64_t bnreg_num_families(const bnreg_t* h) { return h ? h->plan.local_families : -1; }
 
+int64_t bnreg_launches_per_run(const bnreg_t* h)
+{
+    if (!h) return -1;
+    if (h->plan.variant == 0) return (int64_t)h->plan.L1 + 1 + (int64_t)h->classes.size() + 1;
+    return (int64_t)h->plan.L1 + 2;
+}
+
 int64_t bnreg_local_index(const bnreg_t* h, int64_t g)
 {
     if (!h || g < 0 || g >= h->plan.total_families) return -1;
