@@ -51,23 +51,19 @@ struct bnreg {
     double* d_root = nullptr;      // root R (m*m)
     double* d_nodes[2] = {nullptr, nullptr};
     uint32_t* d_packs = nullptr;
-    uint4* d_steps = nullptr;
-    unsigned* d_counter = nullptr;
     double* d_part_bic = nullptr;
     uint32_t* d_part_mask = nullptr;
     double* d_best_bic = nullptr;
     uint32_t* d_best_mask = nullptr;
     int* d_status = nullptr;
-    double2* d_lntab = nullptr;    // fast-log table (a9), 128 entries (legacy kernels)
     double2* d_lntab9 = nullptr;   // fast-log table (a9), 512 entries (walk kernel, debug_ln)
-    int grid_ctas = 0, wpc = 2;
+    int wpc = 4;                   // warps per walk CTA (one gang)
     bool loaded = false;
     // timing
     bool timing = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double acc_ms[4] = {0, 0, 0, 0};
     int64_t runs = 0;
-    unsigned long long* dbg = nullptr;
     // walk kernel: one launch per shared-memory class of work items
     struct WalkClass {
         int begin, end, S_alloc, grid, part_base;
@@ -97,8 +93,8 @@ static void free_all(bnreg* h)
 {
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
-                    h->d_packs, h->d_steps, h->d_counter, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds};
+                    h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
+                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -133,7 +129,7 @@ bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* o, int6
         Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
         info[0] = P.k; info[1] = P.b; info[2] = P.p; info[3] = P.bh; info[4] = P.L1; info[5] = P.LW;
         info[6] = (int64_t)P.packs.size(); info[7] = (int64_t)P.sched.size(); info[8] = P.local_families;
-        info[9] = P.total_families; info[10] = (int64_t)traverse_smem_per_warp(P.m, P.k); info[11] = P.r;
+        info[9] = P.total_families; info[10] = (int64_t)walk_cta_smem(P.m, P.k, P.m, P.g, P.lw) >> P.g; info[11] = P.r;
         info[12] = P.g;
     } catch (std::exception& e) {
         return fail(BNREG_E_INVAL, e.what());
@@ -205,17 +201,11 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_packs, std::max<size_t>(1, P.packs.size()) * sizeof(uint32_t)));
     if (!P.packs.empty())
         CKH(cudaMemcpy(h->d_packs, P.packs.data(), P.packs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    {
-        auto recs = step_records(P.k, P.sched);
-        CKH(cudaMalloc(&h->d_steps, recs.size() * sizeof(uint4)));
-        CKH(cudaMemcpy(h->d_steps, recs.data(), recs.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-    }
-    CKH(cudaMalloc(&h->d_counter, sizeof(unsigned)));
     h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
     (void)d.warps_per_cta;
-    if (P.variant == 0 && P.local_families > (int64_t)0xffffffffLL)
+    if (P.local_families > (int64_t)0xffffffffLL)
         return bail(fail(BNREG_E_INVAL, "this rank's table exceeds 2^32 entries (use more ranks)"));
-    if (P.variant == 0) {
+    {
         // walk kernel: items are sorted costliest first = most walk slots first
         // (a gang's slots: m - |F among its tree levels|); consecutive items with
         // the same occupancy share a launch sized for the first (largest) one
@@ -272,17 +262,11 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             }
         }
         if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(0, atoi(be));
-    } else {
-        int per_sm = d.ctas_per_sm > 0 ? d.ctas_per_sm : traverse_max_ctas_per_sm(m, P.k, h->wpc);
-        int64_t want = (int64_t)h->num_sms * per_sm;
-        int64_t need = (int64_t)P.packs.size();
-        h->grid_ctas = (int)std::max<int64_t>(1, std::min(want, need));
-        h->nparts = h->grid_ctas * h->wpc * traverse_warps_per_cta_factor();
     }
     size_t gw = (size_t)h->nparts;
     CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
     CKH(cudaMalloc(&h->d_part_mask, gw * m * sizeof(uint32_t)));
-    if (P.variant == 0 && h->classes.empty()) {
+    if (h->classes.empty()) {
         std::vector<double> nb(m, -INFINITY);
         std::vector<uint32_t> nm(m, 0xffffffffu);
         CKH(cudaMemcpy(h->d_part_bic, nb.data(), m * sizeof(double), cudaMemcpyHostToDevice));
@@ -292,16 +276,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
     {
-        // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/128)); -ln r_j in long double
-        std::vector<double2> tab(128);
-        for (int j = 0; j < 128; ++j) {
-            long double t = 1.0L + ((long double)j + 0.5L) / 128.0L;
-            double r = (double)(1.0L / t);
-            tab[j].x = r;
-            tab[j].y = (double)(-logl((long double)r));
-        }
-        CKH(cudaMalloc(&h->d_lntab, 128 * sizeof(double2)));
-        CKH(cudaMemcpy(h->d_lntab, tab.data(), 128 * sizeof(double2), cudaMemcpyHostToDevice));
+        // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/512)); -ln r_j in long double
         std::vector<double2> tab9(512);
         for (int j = 0; j < 512; ++j) {
             long double t = 1.0L + ((long double)j + 0.5L) / 512.0L;
@@ -402,8 +377,7 @@ int64_t bnreg_num_families(const bnreg_t* h) { return h ? h->plan.local_families
 int64_t bnreg_launches_per_run(const bnreg_t* h)
 {
     if (!h) return -1;
-    if (h->plan.variant == 0) return (int64_t)h->plan.L1 + 1 + (int64_t)h->classes.size() + 1;
-    return (int64_t)h->plan.L1 + 2;
+    return (int64_t)h->plan.L1 + 1 + (int64_t)h->classes.size() + 1;
 }
 
 int64_t bnreg_local_index(const bnreg_t* h, int64_t g)
@@ -484,66 +458,48 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
         nodes = ch;
     }
-    if (h->timing) CK(cudaEventRecord(h->ev[1], st));
     TravParams T{};
-    T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p; T.g = P.g;
-    T.NCS = P.m; T.SA = P.m | 1;
-    T.sched_len = (int)P.sched.size();
-    if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) T.sched_len = std::min(T.sched_len, atoi(dbg));  // profiling aid
-    T.nsteps = P.k + 1 + T.sched_len;
-    T.dbg = nullptr;
-    if (getenv("BNREG_DEBUG_STEP_CLOCKS")) {   // profiling aid: step phase clocks of warp 0
-        static unsigned long long* dd = nullptr;
-        if (!dd) cudaMalloc(&dd, (1 + 3 * 4000) * sizeof(unsigned long long));
-        cudaMemsetAsync(dd, 0, 8, st);
-        T.dbg = dd;
-        h->dbg = dd;
-    }
-    T.npacks = (int)P.packs.size();
-    T.steps = h->d_steps; T.nodes = nodes; T.packs = h->d_packs; T.counter = h->d_counter;
+    T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p; T.g = P.g; T.lw = P.lw;
+    int sched_len = (int)P.sched.size();
+    if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) sched_len = std::min(sched_len, atoi(dbg));  // profiling aid
+    T.nsteps = P.k + 1 + sched_len;
+    T.packs = h->d_packs;
     T.out_rss = out_rss; T.out_bic = out_bic;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
-    T.lntab = h->d_lntab;
     T.lntab9 = h->d_lntab9;
     T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
     T.r = P.r;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
-    if (P.variant == 0) {
-        T.nw = 1 << P.p;
-        T.bar_every = h->bar_every;
-        T.lw = P.lw;
-        CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
-        // a5: every pack's seeds, in the walk kernel's layout
-        SeedParams SP{};
-        SP.m = P.m; SP.k = P.k; SP.p = P.p; SP.bh = P.bh; SP.g = P.g; SP.L1 = P.L1; SP.nw = 1 << P.p; SP.lw = P.lw;
-        SP.nclass = (int)h->classes.size();
-        for (size_t c = 0; c < h->classes.size(); ++c) {
-            SP.cls_begin[c] = h->classes[c].begin;
-            SP.cls_end[c] = h->classes[c].end;
-            SP.cls_SA[c] = h->classes[c].S_alloc;
-            SP.cls_off[c] = h->seed_off[c];
-        }
-        SP.item_begin = 0;
-        SP.item_end = (int)P.packs.size();
-        SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = h->d_seeds;
-        CK(launch_seed(SP, st));
-        if (h->timing) CK(cudaEventRecord(h->ev[1], st));
-        for (size_t c = 0; c < h->classes.size(); ++c) {
-            const auto& C = h->classes[c];
-            T.counter = h->d_counters + c;
-            T.S_alloc = C.S_alloc;
-            T.item_begin = C.begin;
-            T.item_end = C.end;
-            T.part_base = C.part_base;
-            T.wsteps = h->d_wsteps + c * h->wsteps_len;
-            T.seeds = h->d_seeds + h->seed_off[c];
-            CK(launch_walk(T, C.grid, st));
-        }
-    } else {
-        CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned), st));
-        CK(launch_traverse(T, h->grid_ctas, h->wpc, st));
+    T.bar_every = h->bar_every;
+    CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
+    // a5: every pack's seeds, in the walk kernel's layout
+    SeedParams SP{};
+    SP.m = P.m; SP.k = P.k; SP.p = P.p; SP.bh = P.bh; SP.g = P.g; SP.L1 = P.L1; SP.nw = 1 << P.p; SP.lw = P.lw;
+    SP.nclass = (int)h->classes.size();
+    for (size_t c = 0; c < h->classes.size(); ++c) {
+        SP.cls_begin[c] = h->classes[c].begin;
+        SP.cls_end[c] = h->classes[c].end;
+        SP.cls_SA[c] = h->classes[c].S_alloc;
+        SP.cls_off[c] = h->seed_off[c];
+    }
+    SP.item_begin = 0;
+    SP.item_end = (int)P.packs.size();
+    SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = h->d_seeds;
+    CK(launch_seed(SP, st));
+    if (h->timing) CK(cudaEventRecord(h->ev[1], st));
+    // a6-a11: the walk, one launch per shared-memory class
+    for (size_t c = 0; c < h->classes.size(); ++c) {
+        const auto& C = h->classes[c];
+        T.counter = h->d_counters + c;
+        T.S_alloc = C.S_alloc;
+        T.item_begin = C.begin;
+        T.item_end = C.end;
+        T.part_base = C.part_base;
+        T.wsteps = h->d_wsteps + c * h->wsteps_len;
+        T.seeds = h->d_seeds + h->seed_off[c];
+        CK(launch_walk(T, C.grid, st));
     }
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
     CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->nparts, P.m,
@@ -570,17 +526,6 @@ bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* b
 {
     bnreg_status s = run_impl(h, out_rss, out_bic, nullptr, nullptr);
     if (s != BNREG_OK) return s;
-    if (h->dbg) {
-        std::vector<unsigned long long> v(1 + 3 * 4000);
-        cudaMemcpy(v.data(), h->dbg, v.size() * 8, cudaMemcpyDeviceToHost);
-        double a = 0, b = 0, n = 0;
-        for (unsigned long long q = 20; q < v[0]; ++q) {
-            a += (double)(v[2 + 3 * q] - v[1 + 3 * q]);
-            b += (double)(v[3 + 3 * q] - v[2 + 3 * q]);
-            n += 1;
-        }
-        fprintf(stderr, "step clocks (warp 0, %g steps): start->A-done %.0f, A-done->end %.0f\n", n, a / n, b / n);
-    }
     const int m = h->plan.m;
     if (best_mask)
         CK(cudaMemcpyAsync(best_mask, h->d_best_mask, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));

@@ -39,37 +39,16 @@ __device__ __forceinline__ void givens(double a, double b, double& c, double& s,
 }
 
 // Constants of the fast log (constant bank: usable as DFMA operands directly).
-static __constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, -1.0 / 6.0, 0.2,
+static __constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, 0.0, 0.0,
                                6.93147180369123816490e-01,   // ln2 hi (exact products e * hi for |e| < 2^11)
                                1.90821492927058770002e-10,   // ln2 lo
                                0.0};
 
-// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 7 bits of
-// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/128) (host,
-// long double); u = f r_j - 1 (|u| <= 3.9e-3);  ln x = e ln2 + (-ln r_j) + log1p(u),
-// log1p(u) = u q(u) with q the degree-5 Taylor polynomial (Estrin form;
-// truncation u^7/7 < 2e-18).  Absolute error ~1e-15 for normal x.
-__device__ __forceinline__ double fast_ln(double x, const double2* tab)
-{
-    const int hi = __double2hiint(x), lo = __double2loint(x);
-    const int e = (hi >> 20) - 1023;
-    const int j = (hi >> 13) & 127;
-    const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 t = tab[j];
-    const double ed = (double)e;
-    const double base = fma(ed, c_ln[5], fma(ed, c_ln[6], t.y));
-    const double u = fma(f, t.x, -1.0);
-    const double u2 = u * u;
-    const double a = fma(u, c_ln[0], 1.0);
-    const double b = fma(u, c_ln[1], c_ln[2]);
-    const double c = fma(u, c_ln[3], c_ln[4]);
-    const double q = fma(u2, fma(u2, c, b), a);
-    return fma(u, q, base);
-}
-
-// The walk kernel's log: the same reduction with a 512-entry table,
-// r_j ~ 1/(1 + (j+0.5)/512), |u| <= 9.8e-4, so log1p(u) = u q(u) with q the
-// degree-3 Taylor polynomial (truncation u^5/5 < 2e-16).
+// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 9 bits of
+// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/512) (host,
+// long double); u = f r_j - 1 (|u| <= 9.8e-4);  ln x = e ln2 + (-ln r_j) + log1p(u),
+// log1p(u) = u q(u) with q the degree-3 Taylor polynomial (truncation u^5/5 <
+// 2e-16).  Absolute error ~1e-15 for normal x (tests/test_gpu_parity.py).
 __device__ __forceinline__ double fast_ln9(double x, const double2* tab)
 {
     const int hi = __double2hiint(x), lo = __double2loint(x);

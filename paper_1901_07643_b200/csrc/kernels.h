@@ -9,33 +9,26 @@ namespace bnr {
 // Parameters of the fused traversal kernel (K4 seed derivation + K5 walk +
 // a8 harvest + a9 BIC + a10 store + a11 per-child running best).
 struct TravParams {
-    int m, k, p, bh, L1, nw, NCS, SA;
+    int m, k, p, bh, L1, nw;
     int g;                      // gang bits: 2^g lockstep warps per CTA
-    int sched_len;
-    int npacks;
+    int lw;                     // log2 workers per warp
     int world1;                 // 1: single rank, identity table layout
-    const uint4* steps;         // step records (plan.h StepRec): k+1 seed steps, then Upsilon(k)
-    int nsteps;
-    const double* nodes;        // seed-tree nodes at depth L1, m*m doubles each
+    int nsteps;                 // k + 1 seed pseudo-steps + Upsilon(k)
     const uint32_t* packs;      // this rank's work items = gang base pack ids (costliest first)
-    unsigned int* counter;      // work-queue counter (zeroed before launch)
+    unsigned int* counter;      // this launch's work-queue counter (zeroed before the launches)
     double* out_rss;            // rank-local RSS table (device) or nullptr
     double* out_bic;            // rank-local BIC table (device) or nullptr
-    double* part_bic;           // [grid warps][m] per-warp best BIC
-    uint32_t* part_mask;        // [grid warps][m] per-warp best mask
+    double* part_bic;           // [warps of all launches][m] per-warp best BIC
+    uint32_t* part_mask;        // [warps of all launches][m] per-warp best mask
     double mhalf_n;             // -n/2
-    const double2* lntab;       // fast-log table (128 x (r_j, -ln r_j)), legacy kernels
-    const double2* lntab9;      // fast-log table (512 x (r_j, -ln r_j)), walk kernel
+    const double2* lntab9;      // fast-log table (512 x (r_j, -ln r_j))
     double Kc[33];              // BIC constant per parent-set size
     int r;                      // rank-selector bits (world > 1)
     unsigned patlo;             // smaller selector pattern of this rank (non-selector children)
-    unsigned long long* dbg;    // profiling aid (BNREG_DEBUG_STEP_CLOCKS): per-step clock64 stamps, or nullptr
-    // walk kernel (walk_kernel.cu): one launch per smem class of work items
     int S_alloc;                // walk slots allocated per warp (>= every item's slot count)
     int item_begin, item_end;   // this launch's work items [begin, end) of `packs`
     int part_base;              // first row of this launch's warps in part_bic / part_mask
-    int bar_every;              // gang barrier every bar_every steps
-    int lw;                     // log2 workers per warp
+    int bar_every;              // gang barrier every bar_every steps (0: none)
     const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, one uint4 per step)
     const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
 };
@@ -62,8 +55,6 @@ size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);
 int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw);
 cudaError_t launch_walk(const TravParams& P, int grid_ctas, cudaStream_t st);
 
-// smem bytes per warp of the traversal kernel
-size_t traverse_smem_per_warp(int m, int k);
 
 cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev,
                           double* Xr, int* status, cudaStream_t st);
@@ -71,9 +62,6 @@ cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsign
                         int nleaf2, int rb, double* Rroot, int* status, cudaStream_t st);
 cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
                               cudaStream_t st);
-cudaError_t launch_traverse(const TravParams& P, int grid_ctas, int warps_per_cta, cudaStream_t st);
-int traverse_max_ctas_per_sm(int m, int k, int warps_per_cta);
-int traverse_warps_per_cta_factor();   // warps per gang pack (2 with warp specialisation)
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st);
 

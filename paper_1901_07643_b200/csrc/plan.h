@@ -40,16 +40,6 @@ constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
 constexpr int kMaxFreeWalk = 9;  // walk kernel: a step's free list (<= 8 slots) fits one u32 of nibbles
 constexpr int kPackBits = 3;     // 8 lockstep workers per warp (walk kernel)
-constexpr int kPackBitsLegacy = 2;  // 4 per warp (legacy traversal kernels, BNREG_LEGACY_TRAVERSE / BNREG_WS_TRAVERSE)
-
-// 0 = walk kernel (default), 1 = legacy traversal, 2 = warp-specialised traversal
-inline int kernel_variant()
-{
-    if (std::getenv("BNREG_LEGACY_TRAVERSE")) return 1;
-    if (std::getenv("BNREG_WS_TRAVERSE")) return 2;
-    return 0;
-}
-constexpr int kGangBits = 2;     // 4 lockstep warps per CTA
 
 // Alg.1 GreedySwaps(m) with Eq.10's +1.
 // Returns 1-based swap positions, length 2^m - m - 1 (Eq.9).
@@ -154,7 +144,6 @@ inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, i
 
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
-    int variant = 0;                          // kernel_variant() at plan time
     int lw = kPackBits;                       // walk kernel: log2 lockstep workers per warp
     int g = 0;                                // gang bits (the top g of the bh tree bits)
     int L1 = 0, LW = 0;                       // tree depth in global memory / levels derived in-warp
@@ -204,17 +193,16 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
         throw std::invalid_argument("world must be a power of two and 0 <= rank < world");
     // default k: the walk kernel's shared memory grows with k (k rows of state per slot);
     // k = 8 balances it against the seed derivation (~2k GRCs per worker, 2^k - k - 1 walk steps)
-    if (k <= 0) k = std::min(m, kernel_variant() == 0 ? 8 : 9);
+    if (k <= 0) k = std::min(m, 8);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
-    if (kernel_variant() == 0 && k > kMaxFreeWalk)
+    if (k > kMaxFreeWalk)
         throw std::invalid_argument("the walk kernel takes at most 9 free variables (k <= 9)");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
-    P.variant = kernel_variant();
     P.lw = kPackBits;
-    P.p = std::min(P.variant == 0 ? P.lw : kPackBitsLegacy, P.b);
+    P.p = std::min(P.lw, P.b);
     P.bh = P.b - P.p;
     // walk kernel: a CTA's 2^g warps x 2^lw workers = 32 workers = 256 B per (child, step)
-    P.g = std::min(P.variant == 0 ? 5 - P.lw : kGangBits, P.bh);
+    P.g = std::min(5 - P.lw, P.bh);
     if (lw < 0) lw = 4;
     P.LW = std::min(std::max(lw, P.g), P.bh);
     P.L1 = P.bh - P.LW;
@@ -223,9 +211,9 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     P.sched = greedy_swaps(k);
     // root order: [hv[0..bh-1], pack vars, free p+g..p+g+k-1]
     for (int l = 0; l < P.bh; ++l) P.root_order.push_back(hv_id(P, l));
-    // the walk kernel's Gray path wants the warp variables in descending id
-    // next to the free block ([w_{p-1} .. w_0 | free]); the legacy kernels ascending
-    for (int j = 0; j < P.p; ++j) P.root_order.push_back(P.variant == 0 ? P.p - 1 - j : j);
+    // the seed kernel's Gray path wants the warp variables in descending id
+    // next to the free block ([w_{p-1} .. w_0 | free])
+    for (int j = 0; j < P.p; ++j) P.root_order.push_back(P.p - 1 - j);
     for (int f = 0; f < k; ++f) P.root_order.push_back(P.p + P.g + f);
 
     // rank selector: top r hi bits (hv[0..r-1] = ids m-1..m-r), complementary patterns
