@@ -33,10 +33,10 @@ namespace bnr {
 // ---------------------------------------------------------------- shared memory layout
 // Per CTA: [log table 512 x 16 B][K(s) 33 doubles] then per warp:
 //   state   k * SA * W * 16 B   E(l, slot, w) at ((l*SA + slot)*W + w)*16
-//   scratch                     derivation triangle (packed, side <= m), then
-//                               rec[slot][w] (16 B: running best BIC, table index of
-//                               (child, F_w) with no free variable, lm = (1 << v) - 1)
-//                               and bm[slot][w] (mask of the running best)
+//   rec     SA * 16 B           per slot (shared by the warp's workers): the warp's running
+//                               best BIC of the slot's child, the table index of (child,
+//                               F without the warp and free variables), lm = (1 << v) - 1
+//   bm      SA * 4 B            the mask of that running best
 //   wbb/wbm 32 * 12 B           the warp's running best per child (kept across items)
 //   slotof  32 B                variable -> slot
 struct WalkLayout {
@@ -52,8 +52,8 @@ __host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
     L.state = o;
     o += al16(k * SA * W * 16);
     L.scratch = o;
-    L.bm = o + SA * W * 16;
-    o += al16(SA * W * 20);
+    L.bm = o + SA * 16;
+    o += al16(SA * 20);
     L.wbb = o;
     o += 32 * 8;
     L.wbm = o;
@@ -119,14 +119,14 @@ __device__ __forceinline__ void givens_fr(double a, double b, double& c, double&
 struct StepV {
     unsigned bi;          // shared address of (row i, slot 0, worker w) of the walk state
     unsigned bb0;         // shared address of the lane's first back entry: bi + (kb + h) * CSb
-    unsigned rb0;         // the same in the record array
-    unsigned rdelta;      // record address - state address (same slot stride)
+    unsigned rb0;         // record address of the lane's first back entry: rec + (kb + h) * 16
+    unsigned rf;          // record array base (free entries: rf + f * 16)
     int RS;               // bytes between rows i and i+1
     int nvalid;           // entries j < nvalid exist for this lane
     int nfj;              // entries j < nfj are free slots (from the nibble list)
     uint32_t nl, nh;      // the free-list nibbles shifted to this lane's first entry
     uint32_t ab0;         // absent >> (kb + h): bit PP j = back entry j's variable is in F
-    uint32_t Tsh, Tsh1;   // free part of the prefix set (user-id bits), and >> 1
+    uint32_t X, X1;       // free part of the prefix set | this worker's warp-variable bits, and >> 1
     double c, sg;         // this step's rotation
     double Kw;            // BIC constant of |S|
     int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
@@ -151,6 +151,10 @@ __device__ __forceinline__ void snapshot_g(const double* A, int sn, int og, int 
         acc = fma(x, x, acc);
     }
 }
+
+// Record address of a free entry from its state address (same slot index; the
+// state's slot stride is W*16 bytes, the records' 16 bytes).
+__device__ __forceinline__ unsigned rec_of(const StepV& v, unsigned sa) { return v.rf + ((sa - v.bi) >> 3); }
 
 constexpr int kMaxE = 16;   // list entries per lane and step (PP * kMaxE >= 32 > m - 1)
 
@@ -231,12 +235,12 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
         double bic = fma(mhalf_n, lnr, v.Kw);
         bic = rss > 1e-300 ? bic : PINF;                            // G13
         bics[j] = bic;
-        const unsigned ra = (j < JF) ? ad[j] + v.rdelta : v.rb0 + j * (PP * CSB);
+        const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
         double bb, rr;
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(bb), "=d"(rr) : "r"(ra));
         const uint32_t idx = (uint32_t)__double2loint(rr);          // table index of (child, F_w)
         const uint32_t lm = (uint32_t)__double2hiint(rr);           // (1 << child) - 1
-        const uint32_t ix = idx + ((v.Tsh & lm) | (v.Tsh1 & ~lm));   // + compress(T, child)
+        const uint32_t ix = idx + ((v.X & lm) | (v.X1 & ~lm));       // + compress(T | w-bits, child)
         bool ok = j < v.nvalid;
         if (j < JF) ok = ok && (j < v.nfj || !((v.ab0 >> (PP * j)) & 1u));
         else ok = ok && !((v.ab0 >> (PP * j)) & 1u);
@@ -244,23 +248,30 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
         if (HB) stg_cs_if(out_bic + ix, bic, ok);
         upd |= (ok && bic >= bb) ? (1u << j) : 0u;
     }
-    if (upd) {
-        // rare: a family beats (or ties, G14) the running best of its (child, worker)
+    unsigned bal = __ballot_sync(FULLMASK, upd != 0);
+    while (bal) {
+        // rare: a family beats (or ties, G14) the warp's running best of its child; the
+        // 8 workers share the record, so lanes with candidates take turns
+        const int l = __ffs(bal) - 1;
+        bal &= bal - 1;
+        if ((int)(threadIdx.x & 31) == l) {
 #pragma unroll
-        for (int j = 0; j < NE; ++j) {
-            if ((upd >> j) & 1u) {
-                const unsigned ra = (j < JF) ? ad[j] + v.rdelta : v.rb0 + j * (PP * CSB);
-                const unsigned ma = bm_sh + ((ra - rec_sh) >> 2);   // bm[slot][w] beside rec[slot][w]
-                double cb;
-                uint32_t cm;
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ra));
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(ma));
-                if (tie_better(bics[j], S, cb, cm)) {
-                    asm volatile("st.shared.f64 [%0], %1;" ::"r"(ra), "d"(bics[j]) : "memory");
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
+            for (int j = 0; j < NE; ++j) {
+                if ((upd >> j) & 1u) {
+                    const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
+                    const unsigned ma = bm_sh + ((ra - rec_sh) >> 2);   // bm[slot] beside rec[slot]
+                    double cb;
+                    uint32_t cm;
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ra));
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(ma));
+                    if (tie_better(bics[j], S, cb, cm)) {
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(ra), "d"(bics[j]) : "memory");
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
+                    }
                 }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -295,8 +306,9 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     const WalkLayout Ly = walk_layout(m, k, SA, W);
     unsigned char* const wb = smem + kWalkHead + wib * Ly.per_warp;
     unsigned char* const st = wb + Ly.state;
-    unsigned char* const recb = wb + Ly.scratch;            // rec[slot][w], 16 B
-    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);           // bm[slot][w]
+    unsigned char* const recb = wb + Ly.scratch;            // rec[slot], 16 B
+    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);           // bm[slot]
+    static_assert(W == 8, "rec_of assumes a state slot stride of 8 x 16 B");
     double* const wbb = (double*)(wb + Ly.wbb);
     uint32_t* const wbm = (uint32_t*)(wb + Ly.wbm);
     const int w = lane & (W - 1), h = lane >> LW;
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     double* const out_bic = P.out_bic;
     const double mhalf_n = P.mhalf_n;
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);     // state of (row 0, slot 0, w)
-    const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb + w * 16);   // rec[slot 0][w]
+    const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb);            // rec[slot 0]
     const unsigned kcbase = (unsigned)__cvta_generic_to_shared(KC);
     const unsigned recb_sh = (unsigned)__cvta_generic_to_shared(recb);
     const unsigned bm_sh = (unsigned)__cvta_generic_to_shared(bm);
@@ -362,26 +374,18 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
                     }
             }
         }
-        // per (slot, worker) records: running best,
-        // table index of (child v, F_w) -- the free part is added per step -- and lm
-        {
-            // lane = (slot group, worker): 4 slots per pass
-            for (int s0 = 0; s0 < Sw; s0 += PP) {
-                const int s = s0 + h;
-                const int v = __shfl_sync(FULLMASK, slotvar, s & 31);
-                if (s < Sw) {
-                    const uint32_t Fw0 = Fhi | (uint32_t)w;
-                    const uint32_t lm = (1u << v) - 1u;
-                    const uint32_t idx = (uint32_t)((long long)v << shb) + block_offset<WORLD1>(P, Fw0, Fw0 >> 1, lm);
-                    unsigned char* r = recb + (s * W + w) * 16;
-                    // the running best of (child v, worker w) starts at the warp's best for v so
-                    // far: only families that beat it (rare after the first items) take the update path
-                    *(double*)r = wbb[v];
-                    *(uint32_t*)(r + 8) = idx;
-                    *(uint32_t*)(r + 12) = lm;
-                    bm[s * W + w] = wbm[v];
-                }
-            }
+        // per-slot records: the warp's running best of the slot's child (from the warp's
+        // best so far: only families that beat it take the update path), the table index
+        // of (child v, F without the warp and free variables) and lm
+        if (lane < Sw) {
+            const int v = slotvar;
+            const uint32_t lm = (1u << v) - 1u;
+            const uint32_t idx = (uint32_t)((long long)v << shb) + block_offset<WORLD1>(P, Fhi, Fhi >> 1, lm);
+            unsigned char* r = recb + lane * 16;
+            *(double*)r = wbb[v];
+            *(uint32_t*)(r + 8) = idx;
+            *(uint32_t*)(r + 12) = lm;
+            bm[lane] = wbm[v];
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         double c = 1.0, sg = 0.0, hh = 0.0;
         int bar_left = P.bar_every;
         const unsigned sb_h = sbase + h * CSb;              // + kbCS: the lane's first back entry
-        const unsigned rb_h = rbase + h * CSb;
+        const unsigned rb_h = rbase + h * 16;
         const uint32_t ab_h = absent >> h;
         const unsigned kc_w = kcbase + dw * 8;               // K(|S|) = KC[dw + i + 1]
         const int nv_h = (w < nw) ? NB + (PP - 1) - h : -64; // entries: nvalid = (nf + nv_h) / PP (absent workers: none)
@@ -412,16 +416,16 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             v.bi = sbase + q.x;
             const unsigned kbcs = (unsigned)(k - nf) * CSb;
             v.bb0 = sb_h + q.x + kbcs;
-            v.rdelta = rbase - v.bi;
-            v.rb0 = rb_h + kbcs;
+            v.rf = rbase;
+            v.rb0 = rb_h + (unsigned)(k - nf) * 16;
             v.RS = RS;
             v.nvalid = (nf + nv_h) >> (5 - LW);               // / PP (arithmetic: negative = none)
             v.nfj = (nf + nfj_h) >> (5 - LW);
             v.nl = q.z >> (4 * h);
             v.nh = 0;
             v.ab0 = ab_h >> (k - nf);
-            v.Tsh = Tsh;
-            v.Tsh1 = Tsh >> 1;
+            v.X = Tsh | (uint32_t)w;
+            v.X1 = v.X >> 1;
             v.c = c;
             v.sg = sg;
             asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.Kw) : "r"(kc_w + ((fl >> 8) & 31u) * 8));
@@ -473,30 +477,12 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             }
         }
         __syncwarp();
-        // fold the per-(slot, worker) bests into the warp's per-child best (a11)
-        for (int s = 0; s < Sw; ++s) {
-            double b = NINF;
-            uint32_t mk = 0xffffffffu;
-            if (lane < W) {
-                b = *(const double*)(recb + (s * W + lane) * 16);
-                mk = bm[s * W + lane];
-            }
-#pragma unroll
-            for (int o = 1; o < W; o <<= 1) {
-                const double ob = __shfl_xor_sync(FULLMASK, b, o);
-                const uint32_t om = __shfl_xor_sync(FULLMASK, mk, o);
-                if (better(ob, om, b, mk)) {
-                    b = ob;
-                    mk = om;
-                }
-            }
-            const int v = __shfl_sync(FULLMASK, slotvar, s);
-            if (lane == 0 && better(b, mk, wbb[v], wbm[v])) {
-                wbb[v] = b;
-                wbm[v] = mk;
-            }
-            __syncwarp();
+        // the per-slot records are the warp's per-child bests (a11)
+        if (lane < Sw) {
+            wbb[slotvar] = *(const double*)(recb + lane * 16);
+            wbm[slotvar] = bm[lane];
         }
+        __syncwarp();
     }
     __syncwarp();
     if (lane < m) {
