@@ -83,39 +83,6 @@ __device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
     return fma(u, q, base);
 }
 
-// Packed row-major upper triangle of side s: row r starts at r*s - r(r-1)/2.
-__device__ __forceinline__ int poff(int r, int s) { return r * s - ((r * (r - 1)) >> 1); }
-
-// GRC on the packed triangle: swap (physical) columns J, J+1
-// and restore the triangle with one rotation of rows J, J+1.  Warp-collective,
-// lane = column for the rotation (columns J+2..end-1), lane = row for the swap.
-__device__ __forceinline__ void grc_packed(double* A, int s, int J, int end, int lane)
-{
-    const int oJ = poff(J, s), oJ1 = poff(J + 1, s);
-    double a = A[oJ + 1];
-    double b = A[oJ1];
-    double rjj = A[oJ];
-    double c, sn, h;
-    givens(a, b, c, sn, h);
-    __syncwarp();
-    const int q = lane;
-    if (q < J) {
-        const int oq = poff(q, s);
-        double t0 = A[oq + J - q], t1 = A[oq + J + 1 - q];
-        A[oq + J - q] = t1;
-        A[oq + J + 1 - q] = t0;
-    } else if (q == J) {
-        A[oJ] = h;
-        A[oJ + 1] = c * rjj;
-        A[oJ1] = -sn * rjj;
-    } else if (q >= J + 2 && q < end) {
-        double x = A[oJ + q - J], y = A[oJ1 + q - J - 1];
-        A[oJ + q - J] = fma(c, x, sn * y);
-        A[oJ1 + q - J - 1] = fma(c, y, -sn * x);
-    }
-    __syncwarp();
-}
-
 // BIC (reading G5): -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi) - (|S|/2) ln n
 //   = mhalf_n * ln RSS + K(|S|);  +inf for RSS <= 1e-300 (G13).
 __device__ __forceinline__ double bic_of(double rss, double lnr, double mhalf_n, double Kw)

@@ -74,13 +74,6 @@ size_t walk_cta_smem(int m, int k, int SA, int g, int lw)
 // user id of seed-tree level l (plan.h hv_id): top ids first, the gang ids last
 __device__ __forceinline__ int hv_of(int l, int m, int gs, int fv0) { return l < gs ? m - 1 - l : fv0 - 1 - (l - gs); }
 
-// GRC on the derivation triangle; myvar (lane = position) follows the swap.
-__device__ __forceinline__ void grc_pv(double* A, int s, int J, int lane, int& myvar)
-{
-    grc_packed(A, s, J, s, lane);
-    const int src = lane == J ? J + 1 : (lane == J + 1 ? J : lane);
-    myvar = __shfl_sync(FULLMASK, myvar, src);
-}
 
 // Predicated stores that stay predicated (no branch around them, so the
 // entries of a step remain one basic block the scheduler can interleave).
@@ -131,26 +124,6 @@ struct StepV {
     double Kw;            // BIC constant of |S|
     int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
 };
-
-// Seed -> walk state of worker wc, written to its part of a worker-major seed
-// block ([row l][slot] of 16 B E pairs, row stride SA*16): the sub-triangle from
-// position og = [free block (k) | back columns]; lane = position q.  Rows are
-// processed bottom-up in lockstep (suffix sums of squares by addition; rows
-// below the free block form the tail), so each row's stores are contiguous.
-__device__ __forceinline__ void snapshot_g(const double* A, int sn, int og, int k, int SA, int lane, int myvar,
-                                           const uint8_t* slotof, unsigned char* wblk)
-{
-    const int q = lane;
-    const bool mine = q >= og && q < sn;
-    const int slot = mine ? slotof[myvar] : 0;
-    double acc = 0.0;
-    for (int r = sn - 1; r >= og; --r) {
-        const double x = (mine && q >= r) ? A[poff(r, sn) + q - r] : 0.0;
-        const int l = r - og;
-        if (mine && l < k) *(double2*)(wblk + (l * SA + slot) * 16) = make_double2(x, acc);
-        acc = fma(x, x, acc);
-    }
-}
 
 // Record address of a free entry from its state address (same slot index; the
 // state's slot stride is W*16 bytes, the records' 16 bytes).
@@ -497,21 +470,66 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
 // (tree_level_kernel), the remaining tree levels, then the W workers' seeds
 // along a Gray path over the warp variables, each converted into walk state
 // (E pairs of the free rows + suffix sums) and written to the pack's block of
-// `seeds` in the walk kernel's shared-memory layout.  Separate from the walk so
-// that its serial GRC chains run at high occupancy (triangle-only smem).
+// `seeds`.  Separate from the walk so that its serial GRC chains run at high
+// occupancy.
+//
+// The node lives in a square array A[row position][physical column] and each
+// lane owns one physical column (its variable never changes) and tracks the
+// column's position: a GRC at positions J, J+1 rotates rows
+// J, J+1 of every column at a position >= J and exchanges the two positions --
+// no data moves for the swap itself.
 __host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw) { return (size_t)k * S_alloc * (16u << lw); }
+
+// GRC at positions J, J+1 on the square node (lane = physical column, pos = its position).
+__device__ __forceinline__ void grc_cols(double* A, int SA, int J, int lane, int& pos)
+{
+    const int Y = __ffs(__ballot_sync(FULLMASK, pos == J + 1)) - 1;   // the column at position J+1
+    const double a = A[J * SA + Y], b = A[(J + 1) * SA + Y];
+    double c, s, h;
+    givens_fr(a, b, c, s, h);
+    const bool live = pos < 32;                                        // lanes past the node's columns idle
+    double* const p0 = A + J * SA + (live ? lane : 0);
+    const double x = p0[0], y = p0[SA];
+    __syncwarp();
+    if (live && pos >= J) {
+        const bool isY = lane == Y;
+        p0[0] = isY ? h : fma(c, x, s * y);
+        p0[SA] = isY ? 0.0 : fma(c, y, -s * x);
+    }
+    __syncwarp();
+    pos = pos == J ? J + 1 : (pos == J + 1 ? J : pos);
+}
+
+// Seed -> walk state of one worker, written to its part of a worker-major seed
+// block ([row l][slot] of 16 B E pairs, row stride SA*16): the columns at
+// positions >= og = [free block (k) | back columns].  Rows are processed
+// bottom-up in lockstep (suffix sums of squares by addition; rows below the
+// free block form the tail), so each row's stores are contiguous.
+__device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, int og, int k, int SA, int lane, int pos,
+                                            int slot, unsigned char* wblk)
+{
+    const bool mine = pos >= og && pos < sn;
+    double acc = 0.0;
+    const double* pa = A + (sn - 1) * SAq + lane;
+    unsigned char* pw = wblk + ((long long)(sn - 1 - og) * SA + slot) * 16;
+    for (int r = sn - 1; r >= og; --r) {
+        const double x = (mine && r <= pos) ? *pa : 0.0;
+        if (mine && r - og < k) *(double2*)pw = make_double2(x, acc);
+        acc = fma(x, x, acc);
+        pa -= SAq;
+        pw -= (size_t)SA * 16;
+    }
+}
 
 template <int LW>
 __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedParams P)
 {
-    constexpr int W = 1 << LW;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
     const int fv0 = p + g, gs = bh - g, G = 1 << g;
-    const int tri_bytes = al16((m * (m + 1) / 2) * 8);
-    double* const tri = (double*)(smem + wib * (tri_bytes + 32));
-    uint8_t* const slotof = smem + wib * (tri_bytes + 32) + tri_bytes;
+    const int SAq = m | 1;
+    double* const A = (double*)smem + (size_t)wib * m * SAq;
     const int npk = (P.item_end - P.item_begin) * G;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
@@ -522,29 +540,23 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
         unsigned char* const blk =
             P.seeds + P.cls_off[c] + ((size_t)(item - P.cls_begin[c]) * G + gw) * seed_block_bytes(k, SA, LW);
         const uint32_t pack = P.packs[item] | ((uint32_t)gw << gs);
-        int nB = 0;
-        for (int l = 0; l < bh; ++l) nB += !((pack >> l) & 1u);
-        const int Sw = k + p + nB;
-        // the node at depth L1 (all loads in flight at once)
+        // the node at depth L1: sn x sn, row-major (stride m) in global memory
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
         const int sn = m - __popc(nid);
         {
             const double* src = P.nodes + (size_t)nid * m * m;
-            const int tot = sn * (sn + 1) / 2;
-            for (int e = lane; e < tot; e += 32) {
-                int r = (int)((2.0f * sn + 1.0f - sqrtf((2.0f * sn + 1.0f) * (2.0f * sn + 1.0f) - 8.0f * e)) * 0.5f);
-                if (r < 0) r = 0;
-                while (r > 0 && poff(r, sn) > e) --r;
-                while (r + 1 < sn && poff(r + 1, sn) <= e) ++r;
-                const int cc = r + (e - poff(r, sn));
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(tri + e);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + cc));
-            }
+            if (lane < sn)
+                for (int r = 0; r < sn; ++r) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(A + r * SAq + lane);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + lane));
+                }
             asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
         }
-        // variable at each node position (lane = position):
-        // [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
-        int myvar = -1;                          // -1: no column at this position
+        // the lane's physical column: its position (initially the column index) and variable,
+        // node order [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
+        int pos = lane < sn ? lane : 1 << 20;
+        int myvar = -1;
         {
             const int nlev = bh - P.L1;
             const int qq = lane;
@@ -560,25 +572,20 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
                     }
             }
         }
-        // variable -> walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
-        if (lane < Sw) {
-            const int s = lane;
-            int v;
-            if (s < k) v = fv0 + s;
-            else if (s < k + p) v = s - k;
+        // the column's walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        int slot = 0;
+        if (myvar >= 0) {
+            if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
+            else if (myvar < p) slot = k + myvar;
             else {
-                int cc = s - k - p;
-                v = 0;
+                int cnt = 0;                           // back variables with a smaller id (not in F)
                 for (int l = bh - 1; l >= 0; --l)
-                    if (!((pack >> l) & 1u)) {
-                        if (cc == 0) { v = hv_of(l, m, gs, fv0); break; }
-                        --cc;
-                    }
+                    if (!((pack >> l) & 1u) && hv_of(l, m, gs, fv0) < myvar) ++cnt;
+                slot = k + p + cnt;
             }
-            slotof[v] = (uint8_t)s;
         }
-        __syncwarp();
-        // remaining tree levels: F -> drop the leading row/column, B -> bubble it behind the free block
+        // remaining tree levels: F -> the leading position joins the front (dropped),
+        // B -> bubble it behind the remaining tree levels, the warp variables and the free block
         int org = 0;
         for (int l = P.L1; l < bh; ++l) {
             if ((pack >> l) & 1u) {
@@ -586,26 +593,25 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
                 continue;
             }
             const int T = (bh - l - 1) + p + k;
-            for (int j = 0; j < T; ++j) grc_pv(tri, sn, org + j, lane, myvar);
+            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
         }
         // Gray path over the warp variables: start with all of them in F (front
         // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
         // variable j across the free block and the j lower warp variables
-        int wcur = P.nw - 1;
         const size_t wsz = (size_t)k * SA * 16;      // one worker's part of the block
-        snapshot_g(tri, sn, org + p, k, SA, lane, myvar, slotof, blk + wcur * wsz);
+        int wcur = P.nw - 1;
+        snapshot_sq(A, SAq, sn, org + p, k, SA, lane, pos, slot, blk + wcur * wsz);
         for (int i = 1; i < P.nw; ++i) {
             const int j = __ffs(i) - 1;
-            const int pj = __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1;
+            const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
             const int d = k + j;
-            __syncwarp();
             if ((wcur >> j) & 1) {
-                for (int t = 0; t < d; ++t) grc_pv(tri, sn, pj + t, lane, myvar);
+                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
             } else {
-                for (int t = 1; t <= d; ++t) grc_pv(tri, sn, pj - t, lane, myvar);
+                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
             }
             wcur ^= 1 << j;
-            snapshot_g(tri, sn, org + __popc(wcur), k, SA, lane, myvar, slotof, blk + wcur * wsz);
+            snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SA, lane, pos, slot, blk + wcur * wsz);
         }
         __syncwarp();
     }
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;
-    const size_t smem = (size_t)4 * (al16((m * (m + 1) / 2) * 8) + 32);
+    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
     const int npk = (P.item_end - P.item_begin) << P.g;
     if (npk <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
@@ -622,6 +628,8 @@ cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::min((npk + 3) / 4, sms * 16);
     if (P.lw != 3) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(seed_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     seed_kernel<3><<<grid, 128, smem, st>>>(P);
     return cudaGetLastError();
 }
