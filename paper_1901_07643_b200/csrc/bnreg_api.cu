@@ -75,7 +75,6 @@ struct bnreg {
     unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
     size_t wsteps_len = 0;         // steps per class table
-    int bar_every = 0;             // gang barrier every n walk steps (0: none; measured faster without)
 };
 
 static bnreg_options defaults(const bnreg_options* o)
@@ -261,7 +260,6 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
                 CKH(cudaMemcpy(h->d_wsteps, all.data(), all.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
             }
         }
-        if (const char* be = getenv("BNREG_BAR_EVERY")) h->bar_every = std::max(0, atoi(be));
     }
     size_t gw = (size_t)h->nparts;
     CKH(cudaMalloc(&h->d_part_bic, gw * m * sizeof(double)));
@@ -472,7 +470,6 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
     T.r = P.r;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
-    T.bar_every = h->bar_every;
     CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
     // a5: every pack's seeds, in the walk kernel's layout
     SeedParams SP{};

@@ -28,7 +28,6 @@ struct TravParams {
     int S_alloc;                // walk slots allocated per warp (>= every item's slot count)
     int item_begin, item_end;   // this launch's work items [begin, end) of `packs`
     int part_base;              // first row of this launch's warps in part_bic / part_mask
-    int bar_every;              // gang barrier every bar_every steps (0: none)
     const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, one uint4 per step)
     const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
 };

@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     const unsigned recb_sh = (unsigned)__cvta_generic_to_shared(recb);
     const unsigned bm_sh = (unsigned)__cvta_generic_to_shared(bm);
     const unsigned lnbase = (unsigned)__cvta_generic_to_shared(lntab);
+    const int nsteps = P.nsteps;                // kernel parameters the step loop needs, in registers
+    const uint4* const wsteps = P.wsteps;
     __syncthreads();
 
     for (;;) {
@@ -369,17 +371,16 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         const uint32_t absent = (w < nw) ? ((uint32_t)w << k) : 0xffffffffu;
         const int NB = Sw - k;
         double c = 1.0, sg = 0.0, hh = 0.0;
-        int bar_left = P.bar_every;
         const unsigned sb_h = sbase + h * CSb;              // + kbCS: the lane's first back entry
         const unsigned rb_h = rbase + h * 16;
         const uint32_t ab_h = absent >> h;
         const unsigned kc_w = kcbase + dw * 8;               // K(|S|) = KC[dw + i + 1]
         const int nv_h = (w < nw) ? NB + (PP - 1) - h : -64; // entries: nvalid = (nf + nv_h) / PP (absent workers: none)
         const int nfj_h = (PP - 1) - h;                      // free entries: nfj = (nf + nfj_h) / PP
-        uint4 r0 = __ldg(P.wsteps);
-        for (int t = 0; t < P.nsteps; ++t) {
+        uint4 r0 = __ldg(wsteps);
+        for (int t = 0; t < nsteps; ++t) {
             const uint4 q = r0;
-            if (t + 1 < P.nsteps) r0 = __ldg(P.wsteps + t + 1);
+            if (t + 1 < nsteps) r0 = __ldg(wsteps + t + 1);
             const uint32_t fl = q.w;
             const int nf = (int)(fl & 31u);
             const int L = nf + NB;
@@ -444,10 +445,6 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             sg = sn;
             hh = hn;
             // the gang's warps write the two halves of each 256 B region: keep them in step
-            if (P.bar_every > 0 && G > 1 && --bar_left == 0) {
-                bar_left = P.bar_every;
-                __syncthreads();
-            }
         }
         __syncwarp();
         // the per-slot records are the warp's per-child bests (a11)
