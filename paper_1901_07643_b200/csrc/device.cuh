@@ -38,10 +38,11 @@ __device__ __forceinline__ void givens(double a, double b, double& c, double& s,
     h = ok ? h2 * y : 0.0;
 }
 
-// Constants of the fast log (constant bank: usable as DFMA operands directly).
-static __constant__ double c_ln[8] = {-0.5, -0.25, 1.0 / 3.0, 0.0, 0.0,
-                               6.93147180559945309417e-01,   // ln2, correctly rounded: e * ln2 in one FMA
-                               0.0, 0.0};                    // (error |e| * 2.3e-17 <= 2.4e-14 for |e| <= 1023)
+// Constants of the fast log (compile-time literals: the compiler keeps them in
+// its constant bank and uses them as DFMA operands directly).
+constexpr double kLnC0 = -0.5, kLnC1 = -0.25, kLnC2 = 1.0 / 3.0;
+constexpr double kLn2 = 6.93147180559945309417e-01;   // correctly rounded: e * ln2 in one FMA
+                                                        // (error |e| * 2.3e-17 <= 2.4e-14 for |e| <= 1023)
 
 // Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 9 bits of
 // f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/512) (host,
@@ -55,11 +56,11 @@ __device__ __forceinline__ double fast_ln9(double x, const double2* tab)
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double2 t = *(const double2*)((const char*)tab + ((hi >> 7) & 0x1ff0));
     const double ed = (double)e;
-    const double base = fma(ed, c_ln[5], t.y);
+    const double base = fma(ed, kLn2, t.y);
     const double u = fma(f, t.x, -1.0);
     const double u2 = u * u;
-    const double a = fma(u, c_ln[0], 1.0);
-    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double a = fma(u, kLnC0, 1.0);
+    const double b = fma(u, kLnC1, kLnC2);
     const double q = fma(u2, b, a);
     return fma(u, q, base);
 }
@@ -73,11 +74,11 @@ __device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
     double tx, ty;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ((hi >> 7) & 0x1ff0)));
     const double ed = (double)e;
-    const double base = fma(ed, c_ln[5], ty);
+    const double base = fma(ed, kLn2, ty);
     const double u = fma(f, tx, -1.0);
     const double u2 = u * u;
-    const double a = fma(u, c_ln[0], 1.0);
-    const double b = fma(u, c_ln[1], c_ln[2]);
+    const double a = fma(u, kLnC0, 1.0);
+    const double b = fma(u, kLnC1, kLnC2);
     const double q = fma(u2, b, a);
     return fma(u, q, base);
 }
