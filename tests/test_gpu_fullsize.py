@@ -1,0 +1,167 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (default options: k = 8, the walk kernel's shared-memory classes):
+cfg4 (m=24, 201 M families) and cfg5 (m=28, 3.76 G families, 60 GB of tables).
+
+The oracle cannot compute these tables whole, so the CUDA path is checked
+  * element by element on stratified samples against O1 (per-family Householder,
+    oracle/oracle.c): uniform families, every family of the worker with F = {}
+    (the empty set and the seed prefixes of sizes 0..k), every family of the
+    worker with all pinned variables in F, and for every child the empty set,
+    V minus the child, the reported best set and its m-1 add/remove neighbours;
+  * by properties that hold at any size, on the GPU's own full table: every
+    entry written (NaN-prefilled), the chain rule
+    RSS(u|S) RSS(v|S+u) = RSS(v|S) RSS(u|S+v) on random quadruples, the product
+    of RSS along a full chain = det(Xc^T Xc), BIC = the formula of its RSS, and
+    the reported per-child best = the maximum of the child's BIC block (with the
+    G14 tie-break) and locally optimal under O1.
+Tolerances as in test_gpu_parity.py: RSS relative 1e-9, BIC absolute 1e-6."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RSS_RTOL = 1e-9
+BIC_ATOL = 1e-6
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _bic(rss, n, ks):
+    return -(n / 2) * np.log(rss / n) - (n / 2) * (1 + np.log(2 * np.pi)) - (ks / 2) * np.log(n)
+
+
+def _run_full(cfg):
+    """The bench configuration: default options, tables on the device."""
+    import torch
+    import paper_1901_07643_b200 as bn
+    X = datagen.config_data(cfg)
+    n, m = X.shape
+    h = bn.Bnreg.create(X)
+    F = h.num_families()
+    assert F == m << (m - 1)
+    rss = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+    bic = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+    bm, bb = h.run(rss, bic)
+    torch.cuda.synchronize()
+    plan = bn.bnreg_plan_query(m, n)
+    h.close()
+    return X, rss, bic, bm, bb, plan
+
+
+def _index(m, v, S):
+    """Flat table index: v 2^(m-1) + S with bit v deleted (vectorised)."""
+    v = np.asarray(v, dtype=np.int64)
+    S = np.asarray(S, dtype=np.int64)
+    lo = (np.int64(1) << v) - 1
+    return (v << (m - 1)) + ((S & lo) | ((S >> 1) & ~lo))
+
+
+def _gather(t, idx):
+    import torch
+    return t[torch.from_numpy(np.asarray(idx, dtype=np.int64)).cuda()].cpu().numpy()
+
+
+def _check(cfg, n_uniform, n_chain):
+    import torch
+    X, rss, bic, bm, bb, plan = _run_full(cfg)
+    n, m = X.shape
+    Xc = oracle.centre(X)
+    # every entry written, every value finite and positive
+    assert not torch.isnan(rss).any().item() and not torch.isnan(bic).any().item()
+    assert (rss > 0).all().item()
+
+    # ---- stratified O1 sample
+    rng = np.random.default_rng(1000 + cfg)
+    idx = list(datagen.sample_indices(m, n_uniform, 77 + cfg))
+    k, b = plan["k"], plan["b"]
+    # the Alg.2 roles (plan.h): free variables are user ids p+g .. p+g+k-1, pinned the rest
+    p, g = plan["p"], plan["g"]
+    free = list(range(p + g, p + g + k))
+    pinned = [u for u in range(m) if u not in free]
+    for Fset in (0, sum(1 << u for u in pinned)):          # worker with F = {} and with F = all pinned
+        for v in range(m):
+            if (Fset >> v) & 1:
+                continue
+            fr = [u for u in free if u != v]
+            for T in rng.choice(1 << len(fr), size=min(64, 1 << len(fr)), replace=False):
+                S = Fset | sum(1 << fr[q] for q in range(len(fr)) if (int(T) >> q) & 1)
+                idx.append(oracle.index(m, v, S))
+    full = (1 << m) - 1
+    for v in range(m):
+        others = full & ~(1 << v)
+        best = int(bm[v])
+        idx += [oracle.index(m, v, 0), oracle.index(m, v, others), oracle.index(m, v, best)]
+        for u in range(m):
+            if u != v:
+                idx.append(oracle.index(m, v, best ^ (1 << u)))
+    idx = np.array(sorted(set(int(i) for i in idx)), dtype=np.int64)
+    got = _gather(rss, idx)
+    gotb = _gather(bic, idx)
+    ref = oracle.rss_indices(Xc, idx)
+    err = np.abs(got - ref) / ref
+    assert err.max() <= RSS_RTOL, f"max rel RSS err {err.max():.3e} at {int(idx[err.argmax()])}"
+    v_, S_ = oracle.masks_of(m, idx)
+    ks = np.array([bin(int(s)).count("1") for s in S_])
+    assert np.abs(gotb - _bic(ref, n, ks)).max() <= BIC_ATOL
+    # local optimality of the reported best under O1 (no single add/remove improves)
+    refb = dict(zip(idx.tolist(), _bic(ref, n, ks).tolist()))
+    for v in range(m):
+        best = int(bm[v])
+        bv = refb[oracle.index(m, v, best)]
+        for u in range(m):
+            if u != v:
+                assert refb[oracle.index(m, v, best ^ (1 << u))] <= bv + BIC_ATOL
+
+    # ---- properties on the GPU's own table
+    # chain rule on random quadruples (S, u, v): both sides equal det G_{S+u+v} / det G_S
+    vs = rng.integers(0, m, size=n_chain)
+    us = (vs + rng.integers(1, m, size=n_chain)) % m
+    Ss = rng.integers(0, 1 << m, size=n_chain, dtype=np.int64) & ~((np.int64(1) << vs) | (np.int64(1) << us))
+    one = np.int64(1)
+    i1 = _index(m, us, Ss)
+    i2 = _index(m, vs, Ss | (one << us))
+    i3 = _index(m, vs, Ss)
+    i4 = _index(m, us, Ss | (one << vs))
+    a = _gather(rss, i1) * _gather(rss, i2)
+    c = _gather(rss, i3) * _gather(rss, i4)
+    assert (np.abs(a - c) / c).max() <= 4 * RSS_RTOL
+    # product of RSS along a full chain = det(Xc^T Xc)
+    order = rng.permutation(m)
+    chain = [oracle.index(m, int(order[j]), sum(1 << int(order[q]) for q in range(j))) for j in range(m)]
+    ld = np.log(_gather(rss, chain)).sum()
+    sign, ref_ld = np.linalg.slogdet(Xc.T @ Xc)
+    assert sign > 0 and abs(ld - ref_ld) <= 1e-9 * max(1.0, abs(ref_ld))
+    # BIC = the formula of the table's own RSS, on a sample
+    bs = datagen.sample_indices(m, 200000, 5 + cfg)
+    r_s, b_s = _gather(rss, bs), _gather(bic, bs)
+    _, S2 = oracle.masks_of(m, bs)
+    k2 = np.array([bin(int(s)).count("1") for s in S2])
+    assert np.abs(b_s - _bic(r_s, n, k2)).max() <= BIC_ATOL
+    # the reported best = the maximum of each child's BIC block
+    blk = bic.view(m, 1 << (m - 1))
+    mx = blk.max(dim=1).values.cpu().numpy()
+    np.testing.assert_array_equal(mx, bb)
+    for v in range(m):
+        assert _gather(bic, [oracle.index(m, v, int(bm[v]))])[0] == bb[v]
+    del rss, bic
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_full_size():
+    _check(4, 20000, 100000)
+
+
+def test_cfg5_full_size():
+    import torch
+    free, total = torch.cuda.mem_get_info()
+    if free < 64e9:
+        pytest.skip("cfg5 needs 60 GB of device memory for its tables")
+    _check(5, 5000, 100000)
