@@ -205,8 +205,8 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
     for (int j = 0; j < NE; ++j) {
         const double rss = rs[j];
         const double lnr = fast_ln9s(rss, lntab);
-        double bic = fma(mhalf_n, lnr, v.Kw);
-        bic = rss > 1e-300 ? bic : PINF;                            // G13
+        const double bic = fma(mhalf_n, lnr, v.Kw);
+        const bool tiny = rss <= 1e-300;                             // G13: BIC = +inf, fixed on the rare path
         bics[j] = bic;
         const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
         double bb, rr;
@@ -219,7 +219,7 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
         else ok = ok && !((v.ab0 >> (PP * j)) & 1u);
         if (HR) stg_cs_if(out_rss + ix, rss, ok);
         if (HB) stg_cs_if(out_bic + ix, bic, ok);
-        upd |= (ok && bic >= bb) ? (1u << j) : 0u;
+        upd |= (ok && (bic >= bb || tiny)) ? (1u << j) : 0u;
     }
     unsigned bal = __ballot_sync(FULLMASK, upd != 0);
     while (bal) {
@@ -233,6 +233,14 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
                 if ((upd >> j) & 1u) {
                     const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
                     const unsigned ma = bm_sh + ((ra - rec_sh) >> 2);   // bm[slot] beside rec[slot]
+                    if (rs[j] <= 1e-300) {
+                        // a perfect fit (G13): BIC = +inf, stored over the finite value written above
+                        bics[j] = PINF;
+                        double rr;
+                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rr) : "r"(ra + 8));
+                        const uint32_t idx = (uint32_t)__double2loint(rr), lm = (uint32_t)__double2hiint(rr);
+                        if (HB) out_bic[idx + ((v.X & lm) | (v.X1 & ~lm))] = PINF;
+                    }
                     double cb;
                     uint32_t cm;
                     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ra));
