@@ -86,9 +86,12 @@ int64_t bnreg_index(int32_t m, int32_t child, uint32_t mask);
 /* Rank-local offset of a global index, -1 if another rank owns it. */
 int64_t bnreg_local_index(const bnreg_t* h, int64_t global_index);
 
-/* The fused hot path (a5-a11): seed tree, traversal with harvest, BIC, stores,
- * per-child best.  out_rss / out_bic: caller-owned DEVICE buffers of
- * bnreg_num_families(h) doubles; either may be NULL (not written).
+/* The fused hot path (a5-a11): seed tree, seed kernel, walk with harvest, BIC,
+ * stores, per-child best.  out_rss / out_bic: caller-owned DEVICE buffers of
+ * bnreg_num_families(h) doubles; either may be NULL (not written).  The work is
+ * ordered on the handle's stream (its own non-blocking stream unless
+ * bnreg_set_stream): device buffers the caller fills or reads on another stream
+ * must be ordered against it by the caller (e.g. a device synchronise).
  * best_mask / best_bic: HOST arrays of m entries (either may be NULL); with
  * world > 1 they hold this rank's best only (merge with bnreg_best_merge). */
 bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask, double* best_bic);

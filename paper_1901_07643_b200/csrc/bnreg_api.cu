@@ -375,7 +375,7 @@ int64_t bnreg_num_families(const bnreg_t* h) { return h ? h->plan.local_families
 int64_t bnreg_launches_per_run(const bnreg_t* h)
 {
     if (!h) return -1;
-    return (int64_t)h->plan.L1 + 1 + (int64_t)h->classes.size() + 1;
+    return (int64_t)(h->plan.L1 > 0 ? 1 : 0) + 1 + (int64_t)h->classes.size() + 1;
 }
 
 int64_t bnreg_local_index(const bnreg_t* h, int64_t g)
@@ -448,13 +448,20 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     const Plan& P = h->plan;
     cudaStream_t st = h->stream;
     if (h->timing) CK(cudaEventRecord(h->ev[0], st));
-    // a5: seed tree levels 0 -> L1 in global memory
+    // a5: the seed tree's nodes at depth L1 (one launch; BNREG_TREE_LEVELS=1: level by level)
     const double* nodes = h->d_root;
-    for (int L = 0; L < P.L1; ++L) {
-        const double* par = (L == 0) ? h->d_root : h->d_nodes[(L - 1) & 1];
-        double* ch = h->d_nodes[L & 1];
-        CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
-        nodes = ch;
+    if (P.L1 > 0) {
+        if (getenv("BNREG_TREE_LEVELS")) {
+            for (int L = 0; L < P.L1; ++L) {
+                const double* par = (L == 0) ? h->d_root : h->d_nodes[(L - 1) & 1];
+                double* ch = h->d_nodes[L & 1];
+                CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
+                nodes = ch;
+            }
+        } else {
+            CK(launch_tree_direct(h->d_root, h->d_nodes[0], P.m, P.L1, P.bh, P.p, P.k, st));
+            nodes = h->d_nodes[0];
+        }
     }
     TravParams T{};
     T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p; T.g = P.g; T.lw = P.lw;

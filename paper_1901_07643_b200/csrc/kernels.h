@@ -48,6 +48,9 @@ struct SeedParams {
 };
 __host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw);
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st);
+// the seed tree's nodes at depth L1 in one launch (one warp per node, derived from the root)
+cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
+                               cudaStream_t st);
 
 // walk kernel: 2^lw lockstep workers per warp (lw = 3 or 4), gang of 2^g warps per CTA
 size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);

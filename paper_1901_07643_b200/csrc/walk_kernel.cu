@@ -526,6 +526,55 @@ __device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, in
     }
 }
 
+// The seed tree's nodes at depth L1, all in one launch: one warp per node
+// derives it from the root R directly (the same GRC sequence the level-by-level
+// tree applies: a level's variable in F stays at the front and is dropped, one
+// not in F is bubbled behind the remaining tree levels, the warp variables and
+// the free block).  Output: m x m row-major, top-left sn x sn in position order.
+__global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restrict__ root, double* __restrict__ nodes,
+                                                          int m, int L1, int bh, int p, int k)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int SAq = m | 1;
+    double* const A = (double*)smem + (size_t)wib * m * SAq;
+    const uint32_t nid = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (nid >= (1u << L1)) return;
+    if (lane < m)
+        for (int r = 0; r < m; ++r) A[r * SAq + lane] = root[r * m + lane];
+    __syncwarp();
+    int pos = lane < m ? lane : 1 << 20;
+    int org = 0;
+    for (int l = 0; l < L1; ++l) {
+        if ((nid >> l) & 1u) {
+            ++org;
+            continue;
+        }
+        const int T = (bh - l - 1) + p + k;
+        for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+    }
+    // write the node in position order, without the dropped front
+    const int sn = m - org;
+    double* const dst = nodes + (size_t)nid * m * m;
+    if (pos < 32 && pos >= org) {
+        const int cq = pos - org;
+        for (int r = org; r < m; ++r) dst[(r - org) * m + cq] = A[r * SAq + lane];
+    }
+    (void)sn;
+}
+
+cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
+                               cudaStream_t st)
+{
+    if (L1 <= 0) return cudaSuccess;
+    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const unsigned n = 1u << L1;
+    cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tree_direct_kernel<<<(n + 3) / 4, 128, smem, st>>>(root, nodes, m, L1, bh, p, k);
+    return cudaGetLastError();
+}
+
 template <int LW>
 __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedParams P)
 {

@@ -15,12 +15,14 @@ def run_tables(X, opt=None, want_rss=True, want_bic=True, fill=np.nan, device_lo
     h = bn.Bnreg(n, m, opt)
     if device_load:
         Xd = torch.from_numpy(X.T.copy()).cuda()  # (m, n) row-major == column-major (n, m)
+        torch.cuda.synchronize()                  # the copy runs on torch's stream, the handle on its own
         h.load(Xd.data_ptr())
     else:
         h.load(X)
     F = h.num_families()
     r = torch.full((F,), fill, dtype=torch.float64, device="cuda") if want_rss else None
     b = torch.full((F,), fill, dtype=torch.float64, device="cuda") if want_bic else None
+    torch.cuda.synchronize()      # the fills run on torch's stream, the handle on its own
     bm, bb = h.run(r, b)
     torch.cuda.synchronize()
     rr = r.cpu().numpy() if r is not None else None

@@ -49,6 +49,7 @@ def _run_full(cfg):
     assert F == m << (m - 1)
     rss = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
     bic = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()      # the NaN fills run on torch's stream, the handle on its own
     bm, bb = h.run(rss, bic)
     torch.cuda.synchronize()
     plan = bn.bnreg_plan_query(m, n)

@@ -173,10 +173,12 @@ def test_all_rss_and_bic_entry_points():
     F = h.num_families()
     r = torch.full((F,), np.nan, dtype=torch.float64, device="cuda")
     b = torch.full((F,), np.nan, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()      # the fills run on torch's stream, the handle on its own
     h.all_rss(r)
     h.bic(b)
     r2 = torch.zeros(F, dtype=torch.float64, device="cuda")
     b2 = torch.zeros(F, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
     h.run(r2, b2)
     assert torch.equal(r, r2) and torch.equal(b, b2)
     h.close()
@@ -229,3 +231,23 @@ def test_fast_ln_accuracy():
     err = np.abs(y - ref) / np.maximum(1.0, np.abs(ref))
     assert err.max() <= 4e-15, err.max()
     h.close()
+
+
+def test_tree_direct_matches_level_by_level():
+    """The seed tree's depth-L1 nodes derived per node from the root in one launch
+    equal the level-by-level tree (BNREG_TREE_LEVELS=1) bit for bit: same GRC
+    sequence, same arithmetic."""
+    import os
+    from gpu_util import run_tables
+    bn = _bn()
+    X = datagen.config_data(2)
+    opt = bn.options(free_vars=4, levels_in_warp=2)   # a deep global tree (L1 = 7)
+    r1, b1, m1, _, h1 = run_tables(X, opt)
+    h1.close()
+    os.environ["BNREG_TREE_LEVELS"] = "1"
+    try:
+        r2, b2, m2, _, h2 = run_tables(X, opt)
+        h2.close()
+    finally:
+        del os.environ["BNREG_TREE_LEVELS"]
+    assert np.array_equal(r1, r2) and np.array_equal(b1, b2) and np.array_equal(m1, m2)
