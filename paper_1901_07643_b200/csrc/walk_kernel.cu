@@ -496,11 +496,14 @@ __device__ __forceinline__ void grc_cols(double* A, int SA, int J, int lane, int
     double* const p0 = A + J * SA + (live ? lane : 0);
     const double x = p0[0], y = p0[SA];
     __syncwarp();
-    if (live && pos >= J) {
-        const bool isY = lane == Y;
-        p0[0] = isY ? h : fma(c, x, s * y);
-        p0[SA] = isY ? 0.0 : fma(c, y, -s * x);
-    }
+    const bool isY = lane == Y;
+    const double xn = isY ? h : fma(c, x, s * y);
+    const double yn = isY ? 0.0 : fma(c, y, -s * x);
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(p0);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q st.shared.f64 [%0], %1;\n\t"
+                 "@q st.shared.f64 [%2], %3;\n\t}" ::"r"(sa), "d"(xn), "r"(sa + SA * 8), "d"(yn),
+                 "r"((unsigned)(live && pos >= J))
+                 : "memory");
     __syncwarp();
     pos = pos == J ? J + 1 : (pos == J + 1 ? J : pos);
 }
@@ -516,13 +519,18 @@ __device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, in
     const bool mine = pos >= og && pos < sn;
     double acc = 0.0;
     const double* pa = A + (sn - 1) * SAq + lane;
-    unsigned char* pw = wblk + ((long long)(sn - 1 - og) * SA + slot) * 16;
-    for (int r = sn - 1; r >= og; --r) {
+    int r = sn - 1;
+    // the tail: rows below the free block only add to the suffix sum
+    for (; r >= og + k; --r, pa -= SAq) {
         const double x = (mine && r <= pos) ? *pa : 0.0;
-        if (mine && r - og < k) *(double2*)pw = make_double2(x, acc);
         acc = fma(x, x, acc);
-        pa -= SAq;
-        pw -= (size_t)SA * 16;
+    }
+    // the free rows og..og+k-1: E_l = (R_l, U_{l+1}), l = r - og
+    double2* pw = (double2*)(wblk + (size_t)slot * 16) + (size_t)(r - og) * SA;
+    for (; r >= og; --r, pa -= SAq, pw -= SA) {
+        const double x = (mine && r <= pos) ? *pa : 0.0;
+        if (mine) *pw = make_double2(x, acc);
+        acc = fma(x, x, acc);
     }
 }
 
