@@ -154,7 +154,7 @@ __device__ __forceinline__ unsigned entry_addr(const StepV& v, int j)
 //   phase C  ln RSS, BIC (a9), the two table stores (a10), running-best
 //            candidates; new bests (rare) resolved at the end (a11, G14).
 template <bool SEED, int NE, int PP, int CSB, bool HR, bool HB>
-__device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double mhalf_n, double* out_rss,
+__device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
                                           double* out_bic, bool pivot, unsigned pcol, double hh, bool has_next,
                                           unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
                                           unsigned rec_sh, unsigned bm_sh)
@@ -204,7 +204,7 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
         const double rss = rs[j];
-        const double lnr = fast_ln9s(rss, lntab);
+        const double lnr = fast_ln9(rss, lntab);
         const double bic = fma(mhalf_n, lnr, v.Kw);
         const bool tiny = rss <= 1e-300;                             // G13: BIC = +inf, fixed on the rare path
         bics[j] = bic;
@@ -258,7 +258,7 @@ __device__ __forceinline__ void walk_step(const StepV& v, unsigned lntab, double
 
 // NE-dispatch of the step body (NE = entries per lane, at most 32 / PP).
 template <bool SEED, int PP, int CSB, bool HR, bool HB, int NE>
-__device__ __forceinline__ void step_ne(const StepV& v, unsigned lntab, double mhalf_n, double* out_rss,
+__device__ __forceinline__ void step_ne(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
                                         double* out_bic, bool pv, unsigned pcol, double hh, bool has_next,
                                         unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
                                         unsigned rec_sh, unsigned bm_sh)
@@ -305,10 +305,8 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
     const double mhalf_n = P.mhalf_n;
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);     // state of (row 0, slot 0, w)
     const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb);            // rec[slot 0]
-    const unsigned kcbase = (unsigned)__cvta_generic_to_shared(KC);
     const unsigned recb_sh = (unsigned)__cvta_generic_to_shared(recb);
     const unsigned bm_sh = (unsigned)__cvta_generic_to_shared(bm);
-    const unsigned lnbase = (unsigned)__cvta_generic_to_shared(lntab);
     const int nsteps = P.nsteps;                // kernel parameters the step loop needs, in registers
     const uint4* const wsteps = P.wsteps;
     __syncthreads();
@@ -382,7 +380,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         const unsigned sb_h = sbase + h * CSb;              // + kbCS: the lane's first back entry
         const unsigned rb_h = rbase + h * 16;
         const uint32_t ab_h = absent >> h;
-        const unsigned kc_w = kcbase + dw * 8;               // K(|S|) = KC[dw + i + 1]
+        const double* const KCw = KC + dw;                  // K(|S|) = KC[dw + i + 1]
         const int nv_h = (w < nw) ? NB + (PP - 1) - h : -64; // entries: nvalid = (nf + nv_h) / PP (absent workers: none)
         const int nfj_h = (PP - 1) - h;                      // free entries: nfj = (nf + nfj_h) / PP
         uint4 r0 = __ldg(wsteps);
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             v.X1 = v.X >> 1;
             v.c = c;
             v.sg = sg;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.Kw) : "r"(kc_w + ((fl >> 8) & 31u) * 8));
+            v.Kw = KCw[(fl >> 8) & 31u];                          // read-only table: plain load
             v.seed0 = (fl >> 6) & 1u;
             const bool seed = (fl >> 5) & 1u;
             const bool has_next = (fl >> 7) & 1u;
@@ -420,7 +418,7 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             const int ne = (L + PP - 1) >> (5 - LW);
             double cn = c, sn = sg, hn = hh;
 #define BN_STEP(SEEDV, NEV)                                                                                   \
-    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lnbase, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
+    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
                                          hn, S, recb_sh, bm_sh)
 #define BN_SWITCH(SEEDV)                                                                                      \
     switch (ne) {                                                                                             \
