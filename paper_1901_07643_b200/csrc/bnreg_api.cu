@@ -66,7 +66,7 @@ struct bnreg {
     int64_t runs = 0;
     // walk kernel: one launch per shared-memory class of work items
     struct WalkClass {
-        int begin, end, S_alloc, grid, part_base;
+        int begin, end, S_alloc, grid, part_base, jbmax;
     };
     std::vector<WalkClass> classes;
     int nparts = 0;                // rows of d_part_bic / d_part_mask
@@ -206,25 +206,25 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         return bail(fail(BNREG_E_INVAL, "this rank's table exceeds 2^32 entries (use more ranks)"));
     {
         // walk kernel: items are sorted costliest first = most walk slots first
-        // (a gang's slots: m - |F among its tree levels|); consecutive items with
-        // the same occupancy share a launch sized for the first (largest) one
+        // (a gang's slots: m - |F among its tree levels|).  A launch ("class") takes
+        // the items whose warps need the same TMEM allocation (back entries per lane
+        // JB = ceil(back slots / 4): JB <= 4 or more), sized for its first item
         const int gs = P.bh - P.g;
         int64_t i0 = 0;
         const int64_t ni = (int64_t)P.packs.size();
+        auto slots_of = [&](int64_t i) { return m - popc(P.packs[i] & ((1u << gs) - 1u)); };
+        auto jb_of = [&](int S) { return (S - P.k + 3) / 4; };
         while (i0 < ni) {
-            const int S0 = m - popc(P.packs[i0] & ((1u << gs) - 1u));
-            int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, P.world == 1, P.lw);
-            if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory"));
+            const int S0 = slots_of(i0);
+            const int jb0 = jb_of(S0);
+            const bool big = jb0 > 4;
+            int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, big ? jb0 : 4);
+            if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory / TMEM"));
             int64_t i1 = i0 + 1;
-            while (i1 < ni) {
-                if (h->classes.size() + 1 >= (size_t)kMaxClasses) { i1 = ni; break; }   // the rest in one class
-                const int S1 = m - popc(P.packs[i1] & ((1u << gs) - 1u));
-                const int o1 = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S1, P.g, P.world == 1, P.lw);
-                if (o1 != occ) break;
-                ++i1;
-            }
+            while (i1 < ni && (jb_of(slots_of(i1)) > 4) == big) ++i1;   // (slots are non-increasing)
             bnreg::WalkClass c;
             c.begin = (int)i0; c.end = (int)i1; c.S_alloc = S0;
+            c.jbmax = big ? jb0 : std::min(jb0, 4);
             c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * occ, i1 - i0));
             c.part_base = h->nparts;
             h->nparts += c.grid * h->wpc;
@@ -241,8 +241,9 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         }
         if (getenv("BNREG_VERBOSE"))
             for (auto& c : h->classes)
-                fprintf(stderr, "walk class: items [%d, %d) S_alloc %d grid %d smem %zu\n", c.begin, c.end, c.S_alloc,
-                        c.grid, walk_cta_smem(m, P.k, c.S_alloc, P.g, P.lw));
+                fprintf(stderr, "walk class: items [%d, %d) S_alloc %d jbmax %d tmem %d grid %d smem %zu\n", c.begin,
+                        c.end, c.S_alloc, c.jbmax, walk_tmem_cols(P.k, c.jbmax), c.grid,
+                        walk_cta_smem(m, P.k, c.S_alloc, P.g, P.lw));
         if (h->classes.empty()) {            // no work items (cannot happen for m >= 2): keep the reduce well-defined
             h->nparts = 1;
         }
@@ -252,7 +253,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             h->wsteps_len = recs.size();
             std::vector<WalkStep> all;
             for (auto& c : h->classes) {
-                auto tb = walk_step_table(recs, P.k, c.S_alloc, 1 << P.lw);
+                auto tb = walk_step_table(recs, P.k, P.k, 1 << P.lw);   // free-slot state: k slots
                 all.insert(all.end(), tb.begin(), tb.end());
             }
             if (!all.empty()) {
@@ -498,6 +499,8 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         const auto& C = h->classes[c];
         T.counter = h->d_counters + c;
         T.S_alloc = C.S_alloc;
+        T.jbmax = C.jbmax;
+        T.tm_cols = walk_tmem_cols(P.k, C.jbmax);
         T.item_begin = C.begin;
         T.item_end = C.end;
         T.part_base = C.part_base;

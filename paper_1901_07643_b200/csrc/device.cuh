@@ -38,6 +38,26 @@ __device__ __forceinline__ void givens(double a, double b, double& c, double& s,
     h = ok ? h2 * y : 0.0;
 }
 
+// Givens coefficients without the rank-deficiency guard: in the walk and the
+// seed derivation, b is a diagonal entry r_{i+1,i+1}, nonzero for full-rank
+// data (checked at create, G26), so h2 > 0.
+__device__ __forceinline__ void givens_fr(double a, double b, double& c, double& s, double& h)
+{
+    const double h2 = fma(a, a, b * b);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
+    double e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-h2, y * y, 1.0);
+    y = fma(0.5 * y, e, y);
+    c = a * y;
+    s = b * y;
+    h = h2 * y;
+}
+
+// user id of seed-tree level l (plan.h hv_id): top ids first, the gang ids last
+__device__ __forceinline__ int hv_of(int l, int m, int gs, int fv0) { return l < gs ? m - 1 - l : fv0 - 1 - (l - gs); }
+
 // Constants of the fast log (compile-time literals: the compiler keeps them in
 // its constant bank and uses them as DFMA operands directly).
 constexpr double kLnC0 = -0.5, kLnC1 = -0.25, kLnC2 = 1.0 / 3.0;

@@ -30,6 +30,8 @@ struct TravParams {
     int part_base;              // first row of this launch's warps in part_bic / part_mask
     const uint4* wsteps;        // this launch's walk step table (plan.h WalkStep, one uint4 per step)
     const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
+    int jbmax;                  // most back entries per lane of this launch's warps (ceil(back slots / 4))
+    int tm_cols;                // TMEM columns per CTA (walk_tmem_cols(k, jbmax))
 };
 
 // seed kernel: one warp per pack derives its 2^p workers' seeds (the remaining
@@ -52,9 +54,11 @@ cudaError_t launch_seed(const SeedParams& P, cudaStream_t st);
 cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
                                cudaStream_t st);
 
-// walk kernel: 2^lw lockstep workers per warp (lw = 3 or 4), gang of 2^g warps per CTA
+// walk kernel: 2^lw = 8 lockstep workers per warp, gang of 2^g warps per CTA; the back
+// slots' walk state in TMEM (walk_tmem_cols per CTA), the free slots' in shared memory
 size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);
-int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw);
+int walk_tmem_cols(int k, int jbmax);
+int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int jbmax);
 cudaError_t launch_walk(const TravParams& P, int grid_ctas, cudaStream_t st);
 
 

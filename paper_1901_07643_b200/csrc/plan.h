@@ -38,7 +38,7 @@ namespace bnr {
 
 constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
-constexpr int kMaxFreeWalk = 9;  // walk kernel: a step's free list (<= 8 slots) fits one u32 of nibbles
+constexpr int kMaxFreeWalk = 8;  // walk kernel: a step's free list (<= 8 slots) fits one u32 of nibbles, <= 2 per lane
 constexpr int kPackBits = 3;     // 8 lockstep workers per warp (walk kernel)
 
 // Alg.1 GreedySwaps(m) with Eq.10's +1.
@@ -196,7 +196,7 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (k <= 0) k = std::min(m, 8);
     if (k < 2 || k > m || k > kMaxFree) throw std::invalid_argument("free count k must be in [2, min(m,16)]");
     if (k > kMaxFreeWalk)
-        throw std::invalid_argument("the walk kernel takes at most 9 free variables (k <= 9)");
+        throw std::invalid_argument("the walk kernel takes at most 8 free variables (k <= 8)");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
     P.lw = kPackBits;
     P.p = std::min(P.lw, P.b);

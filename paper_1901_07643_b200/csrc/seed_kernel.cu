@@ -1,0 +1,240 @@
+// seed_kernel.cu -- a5 of the bnreg path: the seed tree's
+// nodes at depth L1 (tree_direct_kernel) and every pack's worker seeds
+// (seed_kernel), written in the layout the walk kernel (walk_kernel.cu) loads.
+// Alg.2's seeds (readings G7-G11) are derived by GRCs
+// (Eq.3-4 with reading G1) from the root R.
+#include <cstdint>
+#include <cmath>
+#include <algorithm>
+#include "kernels.h"
+#include "device.cuh"
+
+namespace bnr {
+
+// ---------------------------------------------------------------- a5: the seed kernel
+// One warp per pack (item, warp of the gang): the pack's node at tree depth L1
+// (tree_level_kernel), the remaining tree levels, then the W workers' seeds
+// along a Gray path over the warp variables, each converted into walk state
+// (E pairs of the free rows + suffix sums) and written to the pack's block of
+// `seeds`.  Separate from the walk so that its serial GRC chains run at high
+// occupancy.
+//
+// The node lives in a square array A[row position][physical column] and each
+// lane owns one physical column (its variable never changes) and tracks the
+// column's position: a GRC at positions J, J+1 rotates rows
+// J, J+1 of every column at a position >= J and exchanges the two positions --
+// no data moves for the swap itself.
+__host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw) { return (size_t)k * S_alloc * (16u << lw); }
+
+// GRC at positions J, J+1 on the square node (lane = physical column, pos = its position).
+__device__ __forceinline__ void grc_cols(double* A, int SA, int J, int lane, int& pos)
+{
+    const int Y = __ffs(__ballot_sync(FULLMASK, pos == J + 1)) - 1;   // the column at position J+1
+    const double a = A[J * SA + Y], b = A[(J + 1) * SA + Y];
+    double c, s, h;
+    givens_fr(a, b, c, s, h);
+    const bool live = pos < 32;                                        // lanes past the node's columns idle
+    double* const p0 = A + J * SA + (live ? lane : 0);
+    const double x = p0[0], y = p0[SA];
+    __syncwarp();
+    const bool isY = lane == Y;
+    const double xn = isY ? h : fma(c, x, s * y);
+    const double yn = isY ? 0.0 : fma(c, y, -s * x);
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(p0);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q st.shared.f64 [%0], %1;\n\t"
+                 "@q st.shared.f64 [%2], %3;\n\t}" ::"r"(sa), "d"(xn), "r"(sa + SA * 8), "d"(yn),
+                 "r"((unsigned)(live && pos >= J))
+                 : "memory");
+    __syncwarp();
+    pos = pos == J ? J + 1 : (pos == J + 1 ? J : pos);
+}
+
+// Seed -> walk state of one worker, written to its part of a worker-major seed
+// block ([row l][slot] of 16 B E pairs, row stride SA*16): the columns at
+// positions >= og = [free block (k) | back columns].  Rows are processed
+// bottom-up in lockstep (suffix sums of squares by addition; rows below the
+// free block form the tail), so each row's stores are contiguous.
+__device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, int og, int k, int SA, int lane, int pos,
+                                            int slot, unsigned char* wblk)
+{
+    const bool mine = pos >= og && pos < sn;
+    double acc = 0.0;
+    const double* pa = A + (sn - 1) * SAq + lane;
+    int r = sn - 1;
+    // the tail: rows below the free block only add to the suffix sum
+    for (; r >= og + k; --r, pa -= SAq) {
+        const double x = (mine && r <= pos) ? *pa : 0.0;
+        acc = fma(x, x, acc);
+    }
+    // the free rows og..og+k-1: E_l = (R_l, U_{l+1}), l = r - og
+    double2* pw = (double2*)(wblk + (size_t)slot * 16) + (size_t)(r - og) * SA;
+    for (; r >= og; --r, pa -= SAq, pw -= SA) {
+        const double x = (mine && r <= pos) ? *pa : 0.0;
+        if (mine) *pw = make_double2(x, acc);
+        acc = fma(x, x, acc);
+    }
+}
+
+// The seed tree's nodes at depth L1, all in one launch: one warp per node
+// derives it from the root R directly (the same GRC sequence the level-by-level
+// tree applies: a level's variable in F stays at the front and is dropped, one
+// not in F is bubbled behind the remaining tree levels, the warp variables and
+// the free block).  Output: m x m row-major, top-left sn x sn in position order.
+__global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restrict__ root, double* __restrict__ nodes,
+                                                          int m, int L1, int bh, int p, int k)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int SAq = m | 1;
+    double* const A = (double*)smem + (size_t)wib * m * SAq;
+    const uint32_t nid = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (nid >= (1u << L1)) return;
+    if (lane < m)
+        for (int r = 0; r < m; ++r) A[r * SAq + lane] = root[r * m + lane];
+    __syncwarp();
+    int pos = lane < m ? lane : 1 << 20;
+    int org = 0;
+    for (int l = 0; l < L1; ++l) {
+        if ((nid >> l) & 1u) {
+            ++org;
+            continue;
+        }
+        const int T = (bh - l - 1) + p + k;
+        for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+    }
+    // write the node in position order, without the dropped front
+    const int sn = m - org;
+    double* const dst = nodes + (size_t)nid * m * m;
+    if (pos < 32 && pos >= org) {
+        const int cq = pos - org;
+        for (int r = org; r < m; ++r) dst[(r - org) * m + cq] = A[r * SAq + lane];
+    }
+    (void)sn;
+}
+
+cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
+                               cudaStream_t st)
+{
+    if (L1 <= 0) return cudaSuccess;
+    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const unsigned n = 1u << L1;
+    cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    tree_direct_kernel<<<(n + 3) / 4, 128, smem, st>>>(root, nodes, m, L1, bh, p, k);
+    return cudaGetLastError();
+}
+
+template <int LW>
+__global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
+    const int fv0 = p + g, gs = bh - g, G = 1 << g;
+    const int SAq = m | 1;
+    double* const A = (double*)smem + (size_t)wib * m * SAq;
+    const int npk = (P.item_end - P.item_begin) * G;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
+        const int item = P.item_begin + q / G, gw = q % G;
+        int c = 0;
+        while (c + 1 < P.nclass && item >= P.cls_end[c]) ++c;
+        const int SA = P.cls_SA[c];
+        unsigned char* const blk =
+            P.seeds + P.cls_off[c] + ((size_t)(item - P.cls_begin[c]) * G + gw) * seed_block_bytes(k, SA, LW);
+        const uint32_t pack = P.packs[item] | ((uint32_t)gw << gs);
+        // the node at depth L1: sn x sn, row-major (stride m) in global memory
+        const uint32_t nid = pack & ((1u << P.L1) - 1u);
+        const int sn = m - __popc(nid);
+        {
+            const double* src = P.nodes + (size_t)nid * m * m;
+            if (lane < sn)
+                for (int r = 0; r < sn; ++r) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(A + r * SAq + lane);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + lane));
+                }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+        }
+        // the lane's physical column: its position (initially the column index) and variable,
+        // node order [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
+        int pos = lane < sn ? lane : 1 << 20;
+        int myvar = -1;
+        {
+            const int nlev = bh - P.L1;
+            const int qq = lane;
+            if (qq < nlev) myvar = hv_of(P.L1 + qq, m, gs, fv0);
+            else if (qq < nlev + p) myvar = p - 1 - (qq - nlev);
+            else if (qq < nlev + p + k) myvar = fv0 + (qq - nlev - p);
+            else if (qq < sn) {
+                int cc = qq - nlev - p - k;
+                for (int l = P.L1 - 1; l >= 0; --l)
+                    if (!((pack >> l) & 1u)) {
+                        if (cc == 0) { myvar = hv_of(l, m, gs, fv0); break; }
+                        --cc;
+                    }
+            }
+        }
+        // the column's walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        int slot = 0;
+        if (myvar >= 0) {
+            if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
+            else if (myvar < p) slot = k + myvar;
+            else {
+                int cnt = 0;                           // back variables with a smaller id (not in F)
+                for (int l = bh - 1; l >= 0; --l)
+                    if (!((pack >> l) & 1u) && hv_of(l, m, gs, fv0) < myvar) ++cnt;
+                slot = k + p + cnt;
+            }
+        }
+        // remaining tree levels: F -> the leading position joins the front (dropped),
+        // B -> bubble it behind the remaining tree levels, the warp variables and the free block
+        int org = 0;
+        for (int l = P.L1; l < bh; ++l) {
+            if ((pack >> l) & 1u) {
+                ++org;
+                continue;
+            }
+            const int T = (bh - l - 1) + p + k;
+            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+        }
+        // Gray path over the warp variables: start with all of them in F (front
+        // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
+        // variable j across the free block and the j lower warp variables
+        const size_t wsz = (size_t)k * SA * 16;      // one worker's part of the block
+        int wcur = P.nw - 1;
+        snapshot_sq(A, SAq, sn, org + p, k, SA, lane, pos, slot, blk + wcur * wsz);
+        for (int i = 1; i < P.nw; ++i) {
+            const int j = __ffs(i) - 1;
+            const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
+            const int d = k + j;
+            if ((wcur >> j) & 1) {
+                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
+            } else {
+                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
+            }
+            wcur ^= 1 << j;
+            snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SA, lane, pos, slot, blk + wcur * wsz);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
+{
+    const int m = P.m;
+    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const int npk = (P.item_end - P.item_begin) << P.g;
+    if (npk <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min((npk + 3) / 4, sms * 16);
+    if (P.lw != 3) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(seed_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    seed_kernel<3><<<grid, 128, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace bnr

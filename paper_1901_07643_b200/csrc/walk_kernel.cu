@@ -1,4 +1,4 @@
-// walk_kernel.cu -- the hot kernel of the bnreg path (SURVEY.md §8(a) a5-a11):
+// walk_kernel.cu -- the hot kernel of the bnreg path (SURVEY.md §8(a) a6-a11):
 // Alg.2 workers each walk d + Upsilon(k) (Alg.1 with Eq.10's
 // +1) from their seed R, one GRC per step
 // (Eq.3-4 with reading G1), harvesting every new family from
@@ -7,21 +7,25 @@
 // table (a10) and keeping a per-child running best (a11, G14).
 //
 // B200 mapping:
-//   * a warp runs W = 8 workers in lockstep; lane = (worker w = lane % W,
-//     part h = lane / W).  All workers of a warp follow the same step records,
-//     so control flow is uniform; part h takes list entries h, h+4, h+8, ...
+//   * a warp runs W = 8 workers in lockstep; lane = (worker w = lane % 8,
+//     part h = lane / 8).  All workers of a warp follow the same step records,
+//     so control flow is warp-uniform.  A step's list of entries is
+//     [back slots | free slots after the prefix], dealt round-robin to the 4
+//     parts: back slot b always belongs to part b % 4 (entry j = b / 4), free
+//     list entry f to part (NB + f) % 4.
 //   * the W workers differ in the W lowest user ids (the "warp variables"), the
 //     CTA's 4 warps in the next 2 ids (the "gang variables"): for every child
 //     and step a CTA writes 32 adjacent entries = 256 B of each table at the same
-//     time (DRAM write combining needs that: profiles/r01_storebench.txt)
-//   * walk state in shared memory, E(l, slot, w) = (R_l, U_{l+1}) of free row l
-//     of the slot's column, U_l = sum_{r >= l} R_r^2 (+ the rows below the free
-//     block), worker-interleaved so that every LDS/STS.128 phase reads 128
-//     contiguous bytes; suffix sums are updated by addition only
-//   * seeds: the gang's node at tree depth L1 (global memory, tree_level_kernel)
-//     -> the remaining tree levels in-warp -> the W workers' seeds along a Gray
-//     path over the warp variables (each flip moves one variable across the free
-//     block: k + j GRCs), each seed converted into its worker's walk state.
+//     time (DRAM write combining: profiles/r01_storebench.txt)
+//   * walk state E(l, slot) = (R_l, U_{l+1}) of the k free rows l of a column,
+//     U_l = sum_{r >= l} R_r^2 (+ the rows below the free block); suffix sums
+//     are updated by addition only.  Back slots are statically
+//     owned by one lane, so their state lives in TENSOR MEMORY (tcgen05.ld/st,
+//     the lane's own TMEM lane: rows i, i+1 of all its back slots are one
+//     contiguous column range); the free slots, whose list position moves every
+//     step, live in shared memory (worker-interleaved, 128 B per LDS phase).
+//     Moving the back state out of shared memory is what lets 16 warps share an
+//     SM (shared memory held 8 before).
 #include <cstdint>
 #include <cmath>
 #include <algorithm>
@@ -30,36 +34,127 @@
 
 namespace bnr {
 
+constexpr int kW = 8;          // lockstep workers per warp
+constexpr int kPP = 4;         // lanes (parts) per worker
+constexpr int kCS = kW * 16;   // bytes between free slots of the shared state
+
+// ---------------------------------------------------------------- tensor memory
+__device__ __forceinline__ void tm_ld4(uint32_t a, uint32_t* r)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_ld8(uint32_t a, uint32_t* r)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_ld16(uint32_t a, uint32_t* r)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_ld32(uint32_t a, uint32_t* r)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                   "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+                   "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                   "=r"(r[30]), "=r"(r[31])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_st4(uint32_t a, const uint32_t* r)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3]));
+}
+__device__ __forceinline__ void tm_st8(uint32_t a, const uint32_t* r)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
+__device__ __forceinline__ void tm_st16(uint32_t a, const uint32_t* r)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(a),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tm_st32(uint32_t a, const uint32_t* r)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                 "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(a),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+                 "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+                 "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+// N consecutive 32-bit columns of the lane's TMEM lane (N a multiple of 4)
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t* r)
+{
+    if constexpr (N >= 32) { tm_ld32(a, r); tm_ld<N - 32>(a + 32, r + 32); }
+    else if constexpr (N >= 16) { tm_ld16(a, r); tm_ld<N - 16>(a + 16, r + 16); }
+    else if constexpr (N >= 8) { tm_ld8(a, r); tm_ld<N - 8>(a + 8, r + 8); }
+    else if constexpr (N >= 4) { tm_ld4(a, r); tm_ld<N - 4>(a + 4, r + 4); }
+}
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t* r)
+{
+    if constexpr (N >= 32) { tm_st32(a, r); tm_st<N - 32>(a + 32, r + 32); }
+    else if constexpr (N >= 16) { tm_st16(a, r); tm_st<N - 16>(a + 16, r + 16); }
+    else if constexpr (N >= 8) { tm_st8(a, r); tm_st<N - 8>(a + 8, r + 8); }
+    else if constexpr (N >= 4) { tm_st4(a, r); tm_st<N - 4>(a + 4, r + 4); }
+}
+// wait for the lane's outstanding tcgen05.ld, then pin the destination
+// registers behind the wait (the compiler does not know the wait defines them)
+template <int N>
+__device__ __forceinline__ void tm_wait_ld(uint32_t* r)
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_f64(const uint32_t* r) { return __hiloint2double((int)r[1], (int)r[0]); }
+__device__ __forceinline__ void tm_put(uint32_t* r, double x)
+{
+    r[0] = (uint32_t)__double2loint(x);
+    r[1] = (uint32_t)__double2hiint(x);
+}
+
 // ---------------------------------------------------------------- shared memory layout
 // Per CTA: [log table 512 x 16 B][K(s) 33 doubles] then per warp:
-//   state   k * SA * W * 16 B   E(l, slot, w) at ((l*SA + slot)*W + w)*16
-//   rec     SA * 16 B           per slot (shared by the warp's workers): the warp's running
-//                               best BIC of the slot's child, the table index of (child,
-//                               F without the warp and free variables), lm = (1 << v) - 1
-//   bm      SA * 4 B            the mask of that running best
-//   wbb/wbm 32 * 12 B           the warp's running best per child (kept across items)
-//   slotof  32 B                variable -> slot
+//   state   k * k * W * 16 B   free-slot state E(l, f, w) at ((l*k + f)*W + w)*16
+//   rec     SA * 16 B          per slot (shared by the warp's workers): the warp's running
+//                              best BIC of the slot's child, the table index of (child,
+//                              F without the warp and free variables), lm = (1 << v) - 1
+//   bm      SA * 4 B           the mask of that running best (directly after rec)
+//   wbb/wbm 32 * 12 B          the warp's running best per child (kept across items)
 struct WalkLayout {
-    int state, scratch, bm, wbb, wbm, slotof, per_warp;
+    int state, rec, bm, wbb, wbm, per_warp;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline WalkLayout walk_layout(int m, int k, int SA, int W)
+__host__ __device__ inline WalkLayout walk_layout(int k, int SA)
 {
     WalkLayout L;
     int o = 0;
     L.state = o;
-    o += al16(k * SA * W * 16);
-    L.scratch = o;
+    o += al16(k * k * kW * 16);
+    L.rec = o;
     L.bm = o + SA * 16;
     o += al16(SA * 20);
     L.wbb = o;
     o += 32 * 8;
     L.wbm = o;
     o += 32 * 4;
-    L.slotof = o;
-    o += 32;
     L.per_warp = al16(o);
     return L;
 }
@@ -68,12 +163,18 @@ constexpr int kWalkHead = 8192 + 272;   // log table + K(s) table
 
 size_t walk_cta_smem(int m, int k, int SA, int g, int lw)
 {
-    return (size_t)kWalkHead + ((size_t)1 << g) * (size_t)walk_layout(m, k, SA, 1 << lw).per_warp;
+    (void)m;
+    (void)lw;
+    return (size_t)kWalkHead + ((size_t)1 << g) * (size_t)walk_layout(k, SA).per_warp;
 }
 
-// user id of seed-tree level l (plan.h hv_id): top ids first, the gang ids last
-__device__ __forceinline__ int hv_of(int l, int m, int gs, int fv0) { return l < gs ? m - 1 - l : fv0 - 1 - (l - gs); }
-
+// TMEM columns a CTA allocates: a warp's back state is k rows x JB slots x 4 columns
+int walk_tmem_cols(int k, int jbmax)
+{
+    int need = k * jbmax * 4, c = 32;
+    while (c < need) c <<= 1;
+    return c;
+}
 
 // Predicated stores that stay predicated (no branch around them, so the
 // entries of a step remain one basic block the scheduler can interleave).
@@ -89,137 +190,59 @@ __device__ __forceinline__ void sts_pair_if(unsigned a, double x, double u, doub
                  "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(a), "d"(x), "d"(u), "r"(a + rs), "d"(y), "r"((unsigned)q)
                  : "memory");
 }
-
-// Givens coefficients without the rank-deficiency guard: in the walk, b is the
-// diagonal entry r_{i+1,i+1} of the pivot column, nonzero for full-rank data
-// (checked at create, G26), so h2 > 0.
-__device__ __forceinline__ void givens_fr(double a, double b, double& c, double& s, double& h)
+__device__ __forceinline__ double2 lds2(unsigned a)
 {
-    const double h2 = fma(a, a, b * b);
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h2));
-    double e = fma(-h2, y * y, 1.0);
-    y = fma(0.5 * y, e, y);
-    e = fma(-h2, y * y, 1.0);
-    y = fma(0.5 * y, e, y);
-    c = a * y;
-    s = b * y;
-    h = h2 * y;
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
 }
 
-// Per-step values of a lane (entries e = h + PP j of the step's list: the free
-// slots after the prefix, in position order, then the back slots).
-struct StepV {
-    unsigned bi;          // shared address of (row i, slot 0, worker w) of the walk state
-    unsigned bb0;         // shared address of the lane's first back entry: bi + (kb + h) * CSb
-    unsigned rb0;         // record address of the lane's first back entry: rec + (kb + h) * 16
-    unsigned rf;          // record array base (free entries: rf + f * 16)
-    int RS;               // bytes between rows i and i+1
-    int nvalid;           // entries j < nvalid exist for this lane
-    int nfj;              // entries j < nfj are free slots (from the nibble list)
-    uint32_t nl, nh;      // the free-list nibbles shifted to this lane's first entry
-    uint32_t ab0;         // absent >> (kb + h): bit PP j = back entry j's variable is in F
-    uint32_t X, X1;       // free part of the prefix set | this worker's warp-variable bits, and >> 1
-    double c, sg;         // this step's rotation
-    double Kw;            // BIC constant of |S|
-    int seed0;            // seed pseudo-step with i = -1 (RSS = U_0)
+// Per-lane constants of the current item.
+struct LaneC {
+    unsigned sbase;   // shared address of the free state (row 0, slot 0, worker w)
+    unsigned recb;    // shared address of rec[slot 0]
+    unsigned recB;    // shared address of the record of back slot h: rec[k + h]
+    unsigned bmb;     // shared address of bm[slot 0]
+    uint32_t tb;      // TMEM address of (this warp's lane quarter, column 0)
+    uint32_t bval;    // bit j: back entry j (slot k + 4j + h) holds a family of this worker
+    uint32_t w;       // worker id = its warp-variable bits
+    uint32_t Fw;      // the worker's F (user ids)
+    int fh0;          // this part's first free-list entry: (h - NB) mod 4
+    int live;         // w < 2^p
+    int h;
+    int RS;           // bytes between free rows l and l+1
+    int fv0;          // user id of free slot 0
+    double mhalf_n;
+    const double* KCw;   // K(|S|) = KCw[i + 1] (K shifted by the worker's d)
+    unsigned lnt;        // shared address of the log table
+    double* out_rss;
+    double* out_bic;
 };
 
-// Record address of a free entry from its state address (same slot index; the
-// state's slot stride is W*16 bytes, the records' 16 bytes).
-__device__ __forceinline__ unsigned rec_of(const StepV& v, unsigned sa) { return v.rf + ((sa - v.bi) >> 3); }
-
-constexpr int kMaxE = 16;   // list entries per lane and step (PP * kMaxE >= 32 > m - 1)
-
-// state address of entry j (free entries from the nibble list, back entries at fixed strides)
-template <int PP, int CSB>
-__device__ __forceinline__ unsigned entry_addr(const StepV& v, int j)
+// phase C of a step: ln RSS, BIC (a9), the two table stores (a10) and the
+// running-best candidates; new bests (rare) are resolved warp-serially (a11, G14)
+template <int NE, bool HR, bool HB>
+__device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const unsigned* ra, const bool* okv,
+                                        double Kw, uint32_t X, uint32_t S)
 {
-    constexpr int JF = 8 / PP;                               // free entries only for e < nf <= k - 1 <= 8
-    const unsigned back = v.bb0 + j * (PP * CSB);
-    if (j < JF) {
-        const int sh = 4 * PP * j;                           // nibble of entry e = h + PP j
-        const unsigned f = ((sh < 32 ? v.nl >> (sh & 31) : v.nh >> ((sh - 32) & 31)) & 15u);
-        return j < v.nfj ? v.bi + f * CSB : back;
-    }
-    return back;
-}
-
-// One lockstep step of a lane over its NE = ceil(L / PP) entries:
-//   phase A  the GRC's rotation of rows i, i+1 of every entry's column and the
-//            new suffix sum U_{i+1} = U_{i+2} + R'_{i+1}^2 (a7, a8), or the seed
-//            pseudo-step's read of U_{i+1};
-//   pivot    Y (now at position i): E_i = (h, 0), R_{i+1} = 0;
-//   givens   the next step's rotation from its pivot column (overlaps phase C);
-//   phase C  ln RSS, BIC (a9), the two table stores (a10), running-best
-//            candidates; new bests (rare) resolved at the end (a11, G14).
-template <bool SEED, int NE, int PP, int CSB, bool HR, bool HB>
-__device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
-                                          double* out_bic, bool pivot, unsigned pcol, double hh, bool has_next,
-                                          unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
-                                          unsigned rec_sh, unsigned bm_sh)
-{
-    constexpr int NA = NE > 0 ? NE : 1;                       // (NE = 0: an empty list, e.g. the last seed step)
-    double rs[NA];
-    unsigned ad[NA];
-    {
-        double2 a0[NA], a1[NA];
-#pragma unroll
-        for (int j = 0; j < NE; ++j) {
-            ad[j] = entry_addr<PP, CSB>(v, j);
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a0[j].x), "=d"(a0[j].y) : "r"(ad[j]));
-            if (!SEED)
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a1[j].x), "=d"(a1[j].y) : "r"(ad[j] + v.RS));
-        }
-#pragma unroll
-        for (int j = 0; j < NE; ++j) {
-            if (SEED) {
-                rs[j] = v.seed0 ? fma(a0[j].x, a0[j].x, a0[j].y) : a0[j].y;   // U_0 or U_{i+1}
-            } else {
-                const double xa = fma(v.c, a0[j].x, v.sg * a1[j].x), ya = fma(v.c, a1[j].x, -v.sg * a0[j].x);
-                const double ra = fma(ya, ya, a1[j].y);
-                rs[j] = ra;
-                sts_pair_if(ad[j], xa, ra, ya, v.RS, j < v.nvalid);
-            }
-        }
-    }
-    if (!SEED && pivot) sts_pair_if(pcol, hh, 0.0, 0.0, v.RS, true);
-    __syncwarp();
-    {
-        // unconditional (no branch: the chain interleaves with phase C); without a next
-        // GRC the table points at a valid slot and the result is unused
-        double a, b;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(ncol));
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(ncol + v.RS));
-        if (!has_next) {
-            a = 0.0;
-            b = 1.0;
-        }
-        givens_fr(a, b, cn, sn, hn);
-    }
     const double PINF = __longlong_as_double(0x7ff0000000000000LL);
-    constexpr int JF = 8 / PP;
+    const uint32_t X1 = X >> 1;
     uint32_t upd = 0;
-    double bics[NA];
+    double bics[NE > 0 ? NE : 1];
 #pragma unroll
-    for (int j = 0; j < NE; ++j) {
-        const double rss = rs[j];
-        const double lnr = fast_ln9(rss, lntab);
-        const double bic = fma(mhalf_n, lnr, v.Kw);
+    for (int e = 0; e < NE; ++e) {
+        const double rss = rs[e];
+        const double lnr = fast_ln9s(rss, L.lnt);
+        const double bic = fma(L.mhalf_n, lnr, Kw);
         const bool tiny = rss <= 1e-300;                             // G13: BIC = +inf, fixed on the rare path
-        bics[j] = bic;
-        const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
-        double bb, rr;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(bb), "=d"(rr) : "r"(ra));
-        const uint32_t idx = (uint32_t)__double2loint(rr);          // table index of (child, F_w)
-        const uint32_t lm = (uint32_t)__double2hiint(rr);           // (1 << child) - 1
-        const uint32_t ix = idx + ((v.X & lm) | (v.X1 & ~lm));       // + compress(T | w-bits, child)
-        bool ok = j < v.nvalid;
-        if (j < JF) ok = ok && (j < v.nfj || !((v.ab0 >> (PP * j)) & 1u));
-        else ok = ok && !((v.ab0 >> (PP * j)) & 1u);
-        if (HR) stg_cs_if(out_rss + ix, rss, ok);
-        if (HB) stg_cs_if(out_bic + ix, bic, ok);
-        upd |= (ok && (bic >= bb || tiny)) ? (1u << j) : 0u;
+        bics[e] = bic;
+        const double2 rr = lds2(ra[e]);
+        const uint32_t idx = (uint32_t)__double2loint(rr.y);        // table index of (child, F_w)
+        const uint32_t lm = (uint32_t)__double2hiint(rr.y);         // (1 << child) - 1
+        const uint32_t ix = idx + ((X & lm) | (X1 & ~lm));           // + compress(T | w-bits, child)
+        if (HR) stg_cs_if(L.out_rss + ix, rss, okv[e]);
+        if (HB) stg_cs_if(L.out_bic + ix, bic, okv[e]);
+        upd |= (okv[e] && (bic >= rr.x || tiny)) ? (1u << e) : 0u;
     }
     unsigned bal = __ballot_sync(FULLMASK, upd != 0);
     while (bal) {
@@ -229,24 +252,25 @@ __device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, 
         bal &= bal - 1;
         if ((int)(threadIdx.x & 31) == l) {
 #pragma unroll
-            for (int j = 0; j < NE; ++j) {
-                if ((upd >> j) & 1u) {
-                    const unsigned ra = (j < JF) ? rec_of(v, ad[j]) : v.rb0 + j * (PP * 16);
-                    const unsigned ma = bm_sh + ((ra - rec_sh) >> 2);   // bm[slot] beside rec[slot]
-                    if (rs[j] <= 1e-300) {
+            for (int e = 0; e < NE; ++e) {
+                if ((upd >> e) & 1u) {
+                    const unsigned a = ra[e];
+                    const unsigned ma = L.bmb + ((a - L.recb) >> 2);   // bm[slot] beside rec[slot]
+                    double b = bics[e];
+                    if (rs[e] <= 1e-300) {
                         // a perfect fit (G13): BIC = +inf, stored over the finite value written above
-                        bics[j] = PINF;
+                        b = PINF;
                         double rr;
-                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rr) : "r"(ra + 8));
+                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rr) : "r"(a + 8));
                         const uint32_t idx = (uint32_t)__double2loint(rr), lm = (uint32_t)__double2hiint(rr);
-                        if (HB) out_bic[idx + ((v.X & lm) | (v.X1 & ~lm))] = PINF;
+                        if (HB) L.out_bic[idx + ((X & lm) | (X1 & ~lm))] = PINF;
                     }
                     double cb;
                     uint32_t cm;
-                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ra));
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(a));
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(ma));
-                    if (tie_better(bics[j], S, cb, cm)) {
-                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(ra), "d"(bics[j]) : "memory");
+                    if (tie_better(b, S, cb, cm)) {
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(b) : "memory");
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
                     }
                 }
@@ -256,58 +280,251 @@ __device__ __forceinline__ void walk_step(const StepV& v, const double2* lntab, 
     }
 }
 
-// NE-dispatch of the step body (NE = entries per lane, at most 32 / PP).
-template <bool SEED, int PP, int CSB, bool HR, bool HB, int NE>
-__device__ __forceinline__ void step_ne(const StepV& v, const double2* lntab, double mhalf_n, double* out_rss,
-                                        double* out_bic, bool pv, unsigned pcol, double hh, bool has_next,
-                                        unsigned ncol, double& cn, double& sn, double& hn, uint32_t S,
-                                        unsigned rec_sh, unsigned bm_sh)
+// The free-list entries of this lane at step record q: slots and validity.
+template <int NFE>
+__device__ __forceinline__ void free_entries(const LaneC& L, uint32_t nib, int nf, unsigned* slot, bool* ok)
 {
-    if constexpr (NE * PP <= 32)
-        walk_step<SEED, NE, PP, CSB, HR, HB>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn,
-                                             hn, S, rec_sh, bm_sh);
+    const uint32_t nl = nib >> (4 * L.fh0);
+#pragma unroll
+    for (int j = 0; j < NFE; ++j) {
+        slot[j] = (nl >> (16 * j)) & 15u;
+        ok[j] = L.live && (L.fh0 + 4 * j < nf);
+    }
 }
 
-template <int LW, bool WORLD1, bool HR, bool HB>
-__global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ TravParams P)
+// Seed pseudo-step (reading G11: the seed prefixes {free 0..j-1}, i = j - 1):
+// RSS = U_{i+1} = E_i.y, or U_0 = R_0^2 + E_0.y for the empty prefix; no rotation.
+template <int JB, int NFE, bool HR, bool HB>
+__device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
 {
-    constexpr int W = 1 << LW;
-    constexpr int PP = 32 / W;                  // lanes (parts) per worker
+    constexpr int NE = JB + NFE;
+    const uint32_t fl = q.w;
+    const int nf = (int)(fl & 31u);
+    const int i = (int)((fl >> 8) & 31u) - 1;
+    const bool s0 = i < 0;
+    const unsigned bi = L.sbase + q.x;   // row max(i, 0)
+    double rs[NE > 0 ? NE : 1];
+    unsigned ra[NE > 0 ? NE : 1];
+    bool okv[NE > 0 ? NE : 1];
+    if constexpr (JB > 0) {
+        uint32_t rb[4 * JB];
+        tm_wait_st();
+        tm_ld<4 * JB>(L.tb + (uint32_t)((s0 ? 0 : i) * JB * 4), rb);
+        tm_wait_ld<4 * JB>(rb);
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            const double R = tm_f64(rb + 4 * j), U = tm_f64(rb + 4 * j + 2);
+            rs[j] = s0 ? fma(R, R, U) : U;
+            ra[j] = L.recB + 64 * j;
+            okv[j] = (L.bval >> j) & 1u;
+        }
+    }
+    unsigned sl[NFE > 0 ? NFE : 1];
+    bool fo[NFE > 0 ? NFE : 1];
+    free_entries<NFE>(L, q.z, nf, sl, fo);
+#pragma unroll
+    for (int j = 0; j < NFE; ++j) {
+        const double2 a = lds2(bi + sl[j] * kCS);
+        rs[JB + j] = s0 ? fma(a.x, a.x, a.y) : a.y;
+        ra[JB + j] = L.recb + sl[j] * 16;
+        okv[JB + j] = fo[j];
+    }
+    const uint32_t Tsh = (fl >> 17) << L.fv0;
+    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.w, L.Fw | Tsh);
+}
+
+// One lockstep GRC step of a lane (a7-a11):
+//   phase A  the rotation of rows i, i+1 of every entry's column with this step's
+//            (c, s) and the new suffix sum U_{i+1} = U_{i+2} + R'_{i+1}^2: back
+//            entries in TMEM (one ld / st of the contiguous rows), free entries in
+//            shared memory; the pivot Y (now at position i): E_i = (h, 0), R_{i+1} = 0;
+//   givens   the next step's rotation from its pivot column (overlaps phase C);
+//   phase C  harvest().
+template <int JB, int NFE, bool HR, bool HB>
+__device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& c, double& sg, double& hh)
+{
+    constexpr int NE = JB + NFE;
+    const uint32_t fl = q.w;
+    const int nf = (int)(fl & 31u);
+    const int i = (int)((fl >> 8) & 31u) - 1;
+    const unsigned bi = L.sbase + q.x;
+    const int RS = L.RS;
+    double rs[NE];
+    unsigned ra[NE];
+    bool okv[NE];
+    unsigned sl[NFE > 0 ? NFE : 1];
+    bool fo[NFE > 0 ? NFE : 1];
+    free_entries<NFE>(L, q.z, nf, sl, fo);
+    double2 f0[NFE > 0 ? NFE : 1], f1[NFE > 0 ? NFE : 1];
+    if constexpr (JB > 0) {
+        uint32_t rb[8 * JB];
+        const uint32_t tcol = L.tb + (uint32_t)(i * JB * 4);
+        tm_wait_st();
+        tm_ld<8 * JB>(tcol, rb);
+#pragma unroll
+        for (int j = 0; j < NFE; ++j) {
+            f0[j] = lds2(bi + sl[j] * kCS);
+            f1[j] = lds2(bi + sl[j] * kCS + RS);
+        }
+        tm_wait_ld<8 * JB>(rb);
+#pragma unroll
+        for (int j = 0; j < JB; ++j) {
+            uint32_t* r0 = rb + 4 * j;            // row i:   (R_i, U_{i+1})
+            uint32_t* r1 = rb + 4 * JB + 4 * j;   // row i+1: (R_{i+1}, U_{i+2})
+            const double x = tm_f64(r0), y = tm_f64(r1), u2 = tm_f64(r1 + 2);
+            const double xa = fma(c, x, sg * y), ya = fma(c, y, -sg * x);
+            const double ru = fma(ya, ya, u2);
+            tm_put(r0, xa);
+            tm_put(r0 + 2, ru);
+            tm_put(r1, ya);
+            rs[j] = ru;
+            ra[j] = L.recB + 64 * j;
+            okv[j] = (L.bval >> j) & 1u;
+        }
+        tm_st<8 * JB>(tcol, rb);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NFE; ++j) {
+            f0[j] = lds2(bi + sl[j] * kCS);
+            f1[j] = lds2(bi + sl[j] * kCS + RS);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NFE; ++j) {
+        const double xa = fma(c, f0[j].x, sg * f1[j].x), ya = fma(c, f1[j].x, -sg * f0[j].x);
+        const double ru = fma(ya, ya, f1[j].y);
+        sts_pair_if(bi + sl[j] * kCS, xa, ru, ya, RS, fo[j]);
+        rs[JB + j] = ru;
+        ra[JB + j] = L.recb + sl[j] * 16;
+        okv[JB + j] = fo[j];
+    }
+    if (L.h == 0) sts_pair_if(bi + ((fl >> 13) & 15u) * kCS, hh, 0.0, 0.0, RS, true);   // pivot Y
+    __syncwarp();
+    {
+        // the next step's rotation, unconditionally (no branch: the chain interleaves with
+        // phase C); without a next GRC the table points at a valid slot and the result is unused
+        double a, b;
+        const unsigned ncol = L.sbase + q.y;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(ncol));
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(ncol + RS));
+        if (!((fl >> 7) & 1u)) {
+            a = 0.0;
+            b = 1.0;
+        }
+        givens_fr(a, b, c, sg, hh);
+    }
+    const uint32_t Tsh = (fl >> 17) << L.fv0;
+    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.w, L.Fw | Tsh);
+}
+
+// One item (gang) of a warp with JB back entries per lane: fill the lane's TMEM
+// rows from the seed block, the k + 1 seed pseudo-steps, then Upsilon(k).
+template <int JB, bool HR, bool HB>
+__device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* src, int k, int SA, int NB,
+                                       const uint4* __restrict__ wsteps, int nsteps)
+{
+    if constexpr (JB > 0) {
+        // back slot b = 4j + h of worker w, row l: seed block [w][l][slot] at ((w k + l) SA + k + b) * 16
+        const unsigned char* bs = src + ((size_t)(L.w * k) * SA + k + L.h) * 16;
+        for (int l = 0; l < k; l += 2) {
+            uint32_t v0[4 * JB], v1[4 * JB];
+#pragma unroll
+            for (int j = 0; j < JB; ++j) {
+                const bool ok = L.live && (4 * j + L.h < NB);
+                uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+                if (ok) {
+                    a = __ldg((const uint4*)(bs + ((size_t)l * SA + 4 * j) * 16));
+                    if (l + 1 < k) b = __ldg((const uint4*)(bs + ((size_t)(l + 1) * SA + 4 * j) * 16));
+                }
+                v0[4 * j] = a.x; v0[4 * j + 1] = a.y; v0[4 * j + 2] = a.z; v0[4 * j + 3] = a.w;
+                v1[4 * j] = b.x; v1[4 * j + 1] = b.y; v1[4 * j + 2] = b.z; v1[4 * j + 3] = b.w;
+            }
+            tm_st<4 * JB>(L.tb + (uint32_t)(l * JB * 4), v0);
+            if (l + 1 < k) tm_st<4 * JB>(L.tb + (uint32_t)((l + 1) * JB * 4), v1);
+        }
+    }
+    // a6-a11: the k + 1 seed pseudo-steps, then d + Upsilon(k), in lockstep
+    uint4 r0 = __ldg(wsteps);
+    for (int t = 0; t <= k; ++t) {
+        const uint4 q = r0;
+        r0 = __ldg(wsteps + t + 1);
+        const int nfe = ((int)(q.w & 31u) + 3) >> 2;
+        if (nfe == 0) seed_step<JB, 0, HR, HB>(L, q);
+        else if (nfe == 1) seed_step<JB, 1, HR, HB>(L, q);
+        else seed_step<JB, 2, HR, HB>(L, q);
+    }
+    double c = 1.0, sg = 0.0, hh = 0.0;
+    {
+        // the first GRC's rotation (the last seed record points at its pivot column)
+        const uint4 q = __ldg(wsteps + k);
+        double a = 0.0, b = 1.0;
+        if ((q.w >> 7) & 1u) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(L.sbase + q.y));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(L.sbase + q.y + L.RS));
+        }
+        givens_fr(a, b, c, sg, hh);
+    }
+    for (int t = k + 1; t < nsteps; ++t) {
+        const uint4 q = r0;
+        if (t + 1 < nsteps) r0 = __ldg(wsteps + t + 1);
+        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB>(L, q, c, sg, hh);
+        else grc_step<JB, 1, HR, HB>(L, q, c, sg, hh);
+    }
+    tm_wait_st();
+}
+
+template <bool HR, bool HB, int JBMAX>
+__global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __grid_constant__ TravParams P)
+{
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_item;
+    __shared__ uint32_t s_item, s_taddr;
     double2* const lntab = (double2*)smem;
     double* const KC = (double*)(smem + 8192);
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     for (int j = tid; j < 512; j += blockDim.x) lntab[j] = P.lntab9[j];
     for (int j = tid; j < 33; j += blockDim.x) KC[j] = P.Kc[j];
+    if (wib == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&s_taddr)),
+                     "r"(P.tm_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g, SA = P.S_alloc;
     const int fv0 = p + g;                      // user id of free slot 0
     const int gs = bh - g;                      // gang levels are gs..bh-1
     const int G = 1 << g;
-    const WalkLayout Ly = walk_layout(m, k, SA, W);
+    const WalkLayout Ly = walk_layout(k, SA);
     unsigned char* const wb = smem + kWalkHead + wib * Ly.per_warp;
     unsigned char* const st = wb + Ly.state;
-    unsigned char* const recb = wb + Ly.scratch;            // rec[slot], 16 B
-    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);           // bm[slot]
-    static_assert(W == 8, "rec_of assumes a state slot stride of 8 x 16 B");
+    unsigned char* const recb = wb + Ly.rec;
+    uint32_t* const bm = (uint32_t*)(wb + Ly.bm);
     double* const wbb = (double*)(wb + Ly.wbb);
     uint32_t* const wbm = (uint32_t*)(wb + Ly.wbm);
-    const int w = lane & (W - 1), h = lane >> LW;
+    const int w = lane & (kW - 1), h = lane >> 3;
     const double NINF = -__longlong_as_double(0x7ff0000000000000LL);
     wbb[lane] = NINF;
     wbm[lane] = 0xffffffffu;
-    const int shb = WORLD1 ? m - 1 : m - P.r;   // child block = v << shb entries
-    const int RS = SA * W * 16;                 // bytes between free rows l and l+1 of a slot
-    constexpr int CSb = W * 16;                 // bytes between slots (state and rec)
+    const int shb = P.world1 ? m - 1 : m - P.r;   // child block = v << shb entries
     const int nw = P.nw;
-    double* const out_rss = P.out_rss;
-    double* const out_bic = P.out_bic;
-    const double mhalf_n = P.mhalf_n;
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);     // state of (row 0, slot 0, w)
-    const unsigned rbase = (unsigned)__cvta_generic_to_shared(recb);            // rec[slot 0]
-    const unsigned recb_sh = (unsigned)__cvta_generic_to_shared(recb);
-    const unsigned bm_sh = (unsigned)__cvta_generic_to_shared(bm);
-    const int nsteps = P.nsteps;                // kernel parameters the step loop needs, in registers
+    LaneC L;
+    L.sbase = (unsigned)__cvta_generic_to_shared(st + w * 16);
+    L.recb = (unsigned)__cvta_generic_to_shared(recb);
+    L.recB = L.recb + (unsigned)(k + h) * 16u;
+    L.bmb = (unsigned)__cvta_generic_to_shared(bm);
+    L.tb = s_taddr + ((uint32_t)(wib * 32) << 16);
+    L.w = (uint32_t)w;
+    L.live = w < nw;
+    L.h = h;
+    L.RS = k * kW * 16;
+    L.fv0 = fv0;
+    L.mhalf_n = P.mhalf_n;
+    L.lnt = (unsigned)__cvta_generic_to_shared(lntab);
+    L.out_rss = P.out_rss;
+    L.out_bic = P.out_bic;
+    const int nsteps = P.nsteps;
     const uint4* const wsteps = P.wsteps;
     __syncthreads();
 
@@ -324,20 +541,22 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
             if ((pack >> l) & 1u) Fhi |= 1u << hv_of(l, m, gs, fv0);
             else ++nB;
         }
-        const int Sw = k + p + nB;              // walk slots of this warp: free, warp vars, back set
+        const int NB = p + nB;                  // back slots: warp vars, then the back set
+        const int Sw = k + NB;                  // walk slots: free, warp vars, back set
 
         // ---- a5: this warp's seeds (seed kernel): worker-major blocks [w][row l][slot] of
-        //      16 B E pairs, transposed into the interleaved state [l][slot][w] (cp.async)
+        //      16 B E pairs; the free slots go to shared memory [l][f][w] (cp.async), the
+        //      back slots to TMEM (walk_item)
+        const unsigned char* src = P.seeds + ((size_t)(item - P.item_begin) * G + wib) * (size_t)(k * SA * kW * 16);
         {
-            const unsigned char* src =
-                P.seeds + ((size_t)(item - P.item_begin) * G + wib) * (size_t)(k * RS);
-            const unsigned dst = sbase - w * 16;
-            for (int r = 0; r < nw * k; ++r) {          // (worker, row) pairs; lane = slot
-                const int ww = r / k, l = r - ww * k;
-                if (lane < Sw)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((l * SA + lane) * W + ww) * 16),
-                                 "l"(src + ((size_t)(ww * k + l) * SA + lane) * 16));
-            }
+            const unsigned dst = L.sbase - w * 16;
+            const int kk = k * k;
+            for (int ww = 0; ww < nw; ++ww)
+                for (int ls = lane; ls < kk; ls += 32) {
+                    const int l = ls / k, f = ls - l * k;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((l * k + f) * kW + ww) * 16),
+                                 "l"(src + ((size_t)(ww * k + l) * SA + f) * 16));
+                }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         // slot -> variable: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
@@ -361,96 +580,47 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         if (lane < Sw) {
             const int v = slotvar;
             const uint32_t lm = (1u << v) - 1u;
-            const uint32_t idx = (uint32_t)((long long)v << shb) + block_offset<WORLD1>(P, Fhi, Fhi >> 1, lm);
+            const uint32_t off = P.world1 ? block_offset<true>(P, Fhi, Fhi >> 1, lm)
+                                          : block_offset<false>(P, Fhi, Fhi >> 1, lm);
+            const uint32_t idx = (uint32_t)((long long)v << shb) + off;
             unsigned char* r = recb + lane * 16;
             *(double*)r = wbb[v];
             *(uint32_t*)(r + 8) = idx;
             *(uint32_t*)(r + 12) = lm;
             bm[lane] = wbm[v];
         }
+        L.Fw = Fhi | (uint32_t)w;               // warp variable j (user id j) in F iff bit j of w
+        L.KCw = KC + __popc(L.Fw);
+        L.fh0 = (h - NB) & 3;
+        {
+            // back entry j = slot k + 4j + h: exists for b < NB; absent for this worker
+            // when it is warp variable b in F (b < p, bit b of w)
+            uint32_t bv = 0;
+            for (int j = 0; j < 8; ++j) {
+                const int b = 4 * j + h;
+                if (L.live && b < NB && !(b < p && ((w >> b) & 1))) bv |= 1u << j;
+            }
+            L.bval = bv;
+        }
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
 
-        // ---- a6-a11: the walk, k+1 seed pseudo-steps then d + Upsilon(k), in lockstep
-        const uint32_t Fw = Fhi | (uint32_t)w;  // warp variable j (user id j) in F iff bit j of w
-        const int dw = __popc(Fw);
-        const uint32_t absent = (w < nw) ? ((uint32_t)w << k) : 0xffffffffu;
-        const int NB = Sw - k;
-        double c = 1.0, sg = 0.0, hh = 0.0;
-        const unsigned sb_h = sbase + h * CSb;              // + kbCS: the lane's first back entry
-        const unsigned rb_h = rbase + h * 16;
-        const uint32_t ab_h = absent >> h;
-        const double* const KCw = KC + dw;                  // K(|S|) = KC[dw + i + 1]
-        const int nv_h = (w < nw) ? NB + (PP - 1) - h : -64; // entries: nvalid = (nf + nv_h) / PP (absent workers: none)
-        const int nfj_h = (PP - 1) - h;                      // free entries: nfj = (nf + nfj_h) / PP
-        uint4 r0 = __ldg(wsteps);
-        for (int t = 0; t < nsteps; ++t) {
-            const uint4 q = r0;
-            if (t + 1 < nsteps) r0 = __ldg(wsteps + t + 1);
-            const uint32_t fl = q.w;
-            const int nf = (int)(fl & 31u);
-            const int L = nf + NB;
-            const uint32_t Tsh = (fl >> 17) << fv0;              // the free part of the prefix set
-            const uint32_t S = Fw | Tsh;
-            StepV v;
-            v.bi = sbase + q.x;
-            const unsigned kbcs = (unsigned)(k - nf) * CSb;
-            v.bb0 = sb_h + q.x + kbcs;
-            v.rf = rbase;
-            v.rb0 = rb_h + (unsigned)(k - nf) * 16;
-            v.RS = RS;
-            v.nvalid = (nf + nv_h) >> (5 - LW);               // / PP (arithmetic: negative = none)
-            v.nfj = (nf + nfj_h) >> (5 - LW);
-            v.nl = q.z >> (4 * h);
-            v.nh = 0;
-            v.ab0 = ab_h >> (k - nf);
-            v.X = Tsh | (uint32_t)w;
-            v.X1 = v.X >> 1;
-            v.c = c;
-            v.sg = sg;
-            v.Kw = KCw[(fl >> 8) & 31u];                          // read-only table: plain load
-            v.seed0 = (fl >> 6) & 1u;
-            const bool seed = (fl >> 5) & 1u;
-            const bool has_next = (fl >> 7) & 1u;
-            const unsigned ncol = sbase + q.y;
-            const unsigned pcol = v.bi + ((fl >> 13) & 15u) * CSb;
-            const bool pv = h == 0;
-            const int ne = (L + PP - 1) >> (5 - LW);
-            double cn = c, sn = sg, hn = hh;
-#define BN_STEP(SEEDV, NEV)                                                                                   \
-    step_ne<SEEDV, PP, CSb, HR, HB, NEV>(v, lntab, mhalf_n, out_rss, out_bic, pv, pcol, hh, has_next, ncol, cn, sn, \
-                                         hn, S, recb_sh, bm_sh)
-#define BN_SWITCH(SEEDV)                                                                                      \
-    switch (ne) {                                                                                             \
-        case 0: BN_STEP(SEEDV, 0); break;                                                                     \
-        case 1: BN_STEP(SEEDV, 1); break;                                                                     \
-        case 2: BN_STEP(SEEDV, 2); break;                                                                     \
-        case 3: BN_STEP(SEEDV, 3); break;                                                                     \
-        case 4: BN_STEP(SEEDV, 4); break;                                                                     \
-        case 5: BN_STEP(SEEDV, 5); break;                                                                     \
-        case 6: BN_STEP(SEEDV, 6); break;                                                                     \
-        case 7: BN_STEP(SEEDV, 7); break;                                                                     \
-        case 8: BN_STEP(SEEDV, 8); break;                                                                     \
-        case 9: BN_STEP(SEEDV, 9); break;                                                                     \
-        case 10: BN_STEP(SEEDV, 10); break;                                                                   \
-        case 11: BN_STEP(SEEDV, 11); break;                                                                   \
-        case 12: BN_STEP(SEEDV, 12); break;                                                                   \
-        case 13: BN_STEP(SEEDV, 13); break;                                                                   \
-        case 14: BN_STEP(SEEDV, 14); break;                                                                   \
-        case 15: BN_STEP(SEEDV, 15); break;                                                                   \
-        default: BN_STEP(SEEDV, 16); break;                                                                   \
-    }
-            if (seed) {
-                BN_SWITCH(true)
-            } else {
-                BN_SWITCH(false)
-            }
-#undef BN_SWITCH
-#undef BN_STEP
-            c = cn;
-            sg = sn;
-            hh = hn;
-            // the gang's warps write the two halves of each 256 B region: keep them in step
+        const int JB = (NB + 3) >> 2;
+        switch (JB) {
+            case 0: walk_item<0, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 1: walk_item<1, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 2: walk_item<2, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 3: walk_item<3, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
+            default:
+                if constexpr (JBMAX <= 4) {
+                    walk_item<4, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                } else {
+                    if (JB == 4) walk_item<4, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                    else if (JB == 5) walk_item<5, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                    else if (JB == 6) walk_item<6, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                    else walk_item<7, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                }
+                break;
         }
         __syncwarp();
         // the per-slot records are the warp's per-child bests (a11)
@@ -466,276 +636,77 @@ __global__ void __launch_bounds__(128, 1) walk_kernel(const __grid_constant__ Tr
         P.part_bic[row * m + lane] = wbb[lane];
         P.part_mask[row * m + lane] = wbm[lane];
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (wib == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "r"(P.tm_cols));
 }
 
-// ---------------------------------------------------------------- a5: the seed kernel
-// One warp per pack (item, warp of the gang): the pack's node at tree depth L1
-// (tree_level_kernel), the remaining tree levels, then the W workers' seeds
-// along a Gray path over the warp variables, each converted into walk state
-// (E pairs of the free rows + suffix sums) and written to the pack's block of
-// `seeds`.  Separate from the walk so that its serial GRC chains run at high
-// occupancy.
-//
-// The node lives in a square array A[row position][physical column] and each
-// lane owns one physical column (its variable never changes) and tracks the
-// column's position: a GRC at positions J, J+1 rotates rows
-// J, J+1 of every column at a position >= J and exchanges the two positions --
-// no data moves for the swap itself.
-__host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw) { return (size_t)k * S_alloc * (16u << lw); }
-
-// GRC at positions J, J+1 on the square node (lane = physical column, pos = its position).
-__device__ __forceinline__ void grc_cols(double* A, int SA, int J, int lane, int& pos)
+// Dynamic shared memory of a launch: the layout, padded so that no more CTAs
+// share an SM than its 512 TMEM columns hold (a CTA beyond that would wait in
+// tcgen05.alloc).
+static size_t walk_launch_smem(const TravParams& P)
 {
-    const int Y = __ffs(__ballot_sync(FULLMASK, pos == J + 1)) - 1;   // the column at position J+1
-    const double a = A[J * SA + Y], b = A[(J + 1) * SA + Y];
-    double c, s, h;
-    givens_fr(a, b, c, s, h);
-    const bool live = pos < 32;                                        // lanes past the node's columns idle
-    double* const p0 = A + J * SA + (live ? lane : 0);
-    const double x = p0[0], y = p0[SA];
-    __syncwarp();
-    const bool isY = lane == Y;
-    const double xn = isY ? h : fma(c, x, s * y);
-    const double yn = isY ? 0.0 : fma(c, y, -s * x);
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(p0);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q st.shared.f64 [%0], %1;\n\t"
-                 "@q st.shared.f64 [%2], %3;\n\t}" ::"r"(sa), "d"(xn), "r"(sa + SA * 8), "d"(yn),
-                 "r"((unsigned)(live && pos >= J))
-                 : "memory");
-    __syncwarp();
-    pos = pos == J ? J + 1 : (pos == J + 1 ? J : pos);
+    size_t smem = walk_cta_smem(P.m, P.k, P.S_alloc, P.g, P.lw);
+    const int occ_tm = 512 / P.tm_cols;
+    const size_t cap = (size_t)233472 / (size_t)(occ_tm + 1);   // 228 KB per SM / (occ + 1)
+    if (smem + 1024 <= cap) smem = cap - 1024 + 16;
+    return smem;
 }
 
-// Seed -> walk state of one worker, written to its part of a worker-major seed
-// block ([row l][slot] of 16 B E pairs, row stride SA*16): the columns at
-// positions >= og = [free block (k) | back columns].  Rows are processed
-// bottom-up in lockstep (suffix sums of squares by addition; rows below the
-// free block form the tail), so each row's stores are contiguous.
-__device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, int og, int k, int SA, int lane, int pos,
-                                            int slot, unsigned char* wblk)
-{
-    const bool mine = pos >= og && pos < sn;
-    double acc = 0.0;
-    const double* pa = A + (sn - 1) * SAq + lane;
-    int r = sn - 1;
-    // the tail: rows below the free block only add to the suffix sum
-    for (; r >= og + k; --r, pa -= SAq) {
-        const double x = (mine && r <= pos) ? *pa : 0.0;
-        acc = fma(x, x, acc);
-    }
-    // the free rows og..og+k-1: E_l = (R_l, U_{l+1}), l = r - og
-    double2* pw = (double2*)(wblk + (size_t)slot * 16) + (size_t)(r - og) * SA;
-    for (; r >= og; --r, pa -= SAq, pw -= SA) {
-        const double x = (mine && r <= pos) ? *pa : 0.0;
-        if (mine) *pw = make_double2(x, acc);
-        acc = fma(x, x, acc);
-    }
-}
-
-// The seed tree's nodes at depth L1, all in one launch: one warp per node
-// derives it from the root R directly (the same GRC sequence the level-by-level
-// tree applies: a level's variable in F stays at the front and is dropped, one
-// not in F is bubbled behind the remaining tree levels, the warp variables and
-// the free block).  Output: m x m row-major, top-left sn x sn in position order.
-__global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restrict__ root, double* __restrict__ nodes,
-                                                          int m, int L1, int bh, int p, int k)
-{
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int SAq = m | 1;
-    double* const A = (double*)smem + (size_t)wib * m * SAq;
-    const uint32_t nid = blockIdx.x * (blockDim.x >> 5) + wib;
-    if (nid >= (1u << L1)) return;
-    if (lane < m)
-        for (int r = 0; r < m; ++r) A[r * SAq + lane] = root[r * m + lane];
-    __syncwarp();
-    int pos = lane < m ? lane : 1 << 20;
-    int org = 0;
-    for (int l = 0; l < L1; ++l) {
-        if ((nid >> l) & 1u) {
-            ++org;
-            continue;
-        }
-        const int T = (bh - l - 1) + p + k;
-        for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
-    }
-    // write the node in position order, without the dropped front
-    const int sn = m - org;
-    double* const dst = nodes + (size_t)nid * m * m;
-    if (pos < 32 && pos >= org) {
-        const int cq = pos - org;
-        for (int r = org; r < m; ++r) dst[(r - org) * m + cq] = A[r * SAq + lane];
-    }
-    (void)sn;
-}
-
-cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
-                               cudaStream_t st)
-{
-    if (L1 <= 0) return cudaSuccess;
-    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
-    const unsigned n = 1u << L1;
-    cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    tree_direct_kernel<<<(n + 3) / 4, 128, smem, st>>>(root, nodes, m, L1, bh, p, k);
-    return cudaGetLastError();
-}
-
-template <int LW>
-__global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedParams P)
-{
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int m = P.m, k = P.k, p = P.p, bh = P.bh, g = P.g;
-    const int fv0 = p + g, gs = bh - g, G = 1 << g;
-    const int SAq = m | 1;
-    double* const A = (double*)smem + (size_t)wib * m * SAq;
-    const int npk = (P.item_end - P.item_begin) * G;
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
-        const int item = P.item_begin + q / G, gw = q % G;
-        int c = 0;
-        while (c + 1 < P.nclass && item >= P.cls_end[c]) ++c;
-        const int SA = P.cls_SA[c];
-        unsigned char* const blk =
-            P.seeds + P.cls_off[c] + ((size_t)(item - P.cls_begin[c]) * G + gw) * seed_block_bytes(k, SA, LW);
-        const uint32_t pack = P.packs[item] | ((uint32_t)gw << gs);
-        // the node at depth L1: sn x sn, row-major (stride m) in global memory
-        const uint32_t nid = pack & ((1u << P.L1) - 1u);
-        const int sn = m - __popc(nid);
-        {
-            const double* src = P.nodes + (size_t)nid * m * m;
-            if (lane < sn)
-                for (int r = 0; r < sn; ++r) {
-                    const unsigned sa = (unsigned)__cvta_generic_to_shared(A + r * SAq + lane);
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + lane));
-                }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-        }
-        // the lane's physical column: its position (initially the column index) and variable,
-        // node order [hv[L1..bh-1], warp vars p-1..0, free, back set (ascending id)]
-        int pos = lane < sn ? lane : 1 << 20;
-        int myvar = -1;
-        {
-            const int nlev = bh - P.L1;
-            const int qq = lane;
-            if (qq < nlev) myvar = hv_of(P.L1 + qq, m, gs, fv0);
-            else if (qq < nlev + p) myvar = p - 1 - (qq - nlev);
-            else if (qq < nlev + p + k) myvar = fv0 + (qq - nlev - p);
-            else if (qq < sn) {
-                int cc = qq - nlev - p - k;
-                for (int l = P.L1 - 1; l >= 0; --l)
-                    if (!((pack >> l) & 1u)) {
-                        if (cc == 0) { myvar = hv_of(l, m, gs, fv0); break; }
-                        --cc;
-                    }
-            }
-        }
-        // the column's walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
-        int slot = 0;
-        if (myvar >= 0) {
-            if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
-            else if (myvar < p) slot = k + myvar;
-            else {
-                int cnt = 0;                           // back variables with a smaller id (not in F)
-                for (int l = bh - 1; l >= 0; --l)
-                    if (!((pack >> l) & 1u) && hv_of(l, m, gs, fv0) < myvar) ++cnt;
-                slot = k + p + cnt;
-            }
-        }
-        // remaining tree levels: F -> the leading position joins the front (dropped),
-        // B -> bubble it behind the remaining tree levels, the warp variables and the free block
-        int org = 0;
-        for (int l = P.L1; l < bh; ++l) {
-            if ((pack >> l) & 1u) {
-                ++org;
-                continue;
-            }
-            const int T = (bh - l - 1) + p + k;
-            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
-        }
-        // Gray path over the warp variables: start with all of them in F (front
-        // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
-        // variable j across the free block and the j lower warp variables
-        const size_t wsz = (size_t)k * SA * 16;      // one worker's part of the block
-        int wcur = P.nw - 1;
-        snapshot_sq(A, SAq, sn, org + p, k, SA, lane, pos, slot, blk + wcur * wsz);
-        for (int i = 1; i < P.nw; ++i) {
-            const int j = __ffs(i) - 1;
-            const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
-            const int d = k + j;
-            if ((wcur >> j) & 1) {
-                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
-            } else {
-                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
-            }
-            wcur ^= 1 << j;
-            snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SA, lane, pos, slot, blk + wcur * wsz);
-        }
-        __syncwarp();
-    }
-}
-
-cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
-{
-    const int m = P.m;
-    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
-    const int npk = (P.item_end - P.item_begin) << P.g;
-    if (npk <= 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min((npk + 3) / 4, sms * 16);
-    if (P.lw != 3) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(seed_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    seed_kernel<3><<<grid, 128, smem, st>>>(P);
-    return cudaGetLastError();
-}
-
-template <int LW, bool W1, bool HR, bool HB>
+template <bool HR, bool HB, int JBMAX>
 static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 {
-    const size_t smem = walk_cta_smem(P.m, P.k, P.S_alloc, P.g, LW);
-    auto f = walk_kernel<LW, W1, HR, HB>;
+    const size_t smem = walk_launch_smem(P);
+    auto f = walk_kernel<HR, HB, JBMAX>;
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     f<<<grid, 32 << P.g, smem, st>>>(P);
     return cudaGetLastError();
 }
 
-template <int LW>
-static cudaError_t launch_lw(const TravParams& P, int grid, cudaStream_t st)
+template <int JBMAX>
+static cudaError_t launch_jb(const TravParams& P, int grid, cudaStream_t st)
 {
-    const int key = (P.world1 ? 4 : 0) | (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
+    const int key = (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
     switch (key) {
-        case 7: return launch_w<LW, true, true, true>(P, grid, st);
-        case 6: return launch_w<LW, true, true, false>(P, grid, st);
-        case 5: return launch_w<LW, true, false, true>(P, grid, st);
-        case 4: return launch_w<LW, true, false, false>(P, grid, st);
-        case 3: return launch_w<LW, false, true, true>(P, grid, st);
-        case 2: return launch_w<LW, false, true, false>(P, grid, st);
-        case 1: return launch_w<LW, false, false, true>(P, grid, st);
-        default: return launch_w<LW, false, false, false>(P, grid, st);
+        case 3: return launch_w<true, true, JBMAX>(P, grid, st);
+        case 2: return launch_w<true, false, JBMAX>(P, grid, st);
+        case 1: return launch_w<false, true, JBMAX>(P, grid, st);
+        default: return launch_w<false, false, JBMAX>(P, grid, st);
     }
 }
 
 cudaError_t launch_walk(const TravParams& P, int grid, cudaStream_t st)
 {
-    if (P.lw != 3) return cudaErrorInvalidValue;   // 8 workers per warp (plan.h kPackBits)
-    return launch_lw<3>(P, grid, st);
+    if (P.lw != 3 || P.k > 8 || P.jbmax > 7) return cudaErrorInvalidValue;   // 8 workers per warp, k <= 8
+    return P.jbmax <= 4 ? launch_jb<4>(P, grid, st) : launch_jb<7>(P, grid, st);
 }
 
-int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int world1, int lw)
+int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int jbmax)
 {
-    const size_t smem = walk_cta_smem(m, k, S_alloc, g, lw);
-    int n = 0;
-    if (lw != 3) return 0;
-    auto f = world1 ? walk_kernel<3, true, true, true> : walk_kernel<3, false, true, true>;
+    // computed from the limits directly: cudaOccupancyMaxActiveBlocksPerMultiprocessor
+    // reports 1 CTA per SM for this kernel (measured on B200, CUDA 12.9), although the
+    // SM runs 4 (ncu launch__occupancy_limit_*)
+    TravParams P{};
+    P.m = m; P.k = k; P.S_alloc = S_alloc; P.g = g; P.lw = 3; P.jbmax = jbmax;
+    P.tm_cols = walk_tmem_cols(k, jbmax);
+    const size_t smem = walk_launch_smem(P);
+    auto f = jbmax <= 4 ? walk_kernel<true, true, 4> : walk_kernel<true, true, 7>;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 32 << g, smem) != cudaSuccess) return 0;
-    return n;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 0;
+    int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+    const int threads = 32 << g;
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = regs_sm / (regs_warp * (threads / 32));
+    const int by_smem = (int)((size_t)smem_sm / (smem + fa.sharedSizeBytes + 1024));
+    const int by_thr = thr_sm / threads;
+    return std::max(0, std::min(std::min(by_regs, by_smem), std::min(by_thr, 512 / P.tm_cols)));
 }
 
 }  // namespace bnr

@@ -49,7 +49,7 @@ def test_index_matches_oracle(bn):
         assert bn.bnreg_index(m, v, S) == oracle.index(m, v, S)
 
 
-@pytest.mark.parametrize("m,k", [(8, 4), (12, 5), (16, 8), (20, 8), (28, 8), (24, 9)])
+@pytest.mark.parametrize("m,k", [(8, 4), (12, 5), (16, 8), (20, 8), (28, 8), (24, 7)])
 def test_plan_partition(bn, m, k):
     """Packs x 2^p workers enumerate every Alg.2 worker (every front set of the
     pinned variables) exactly once; world ranks split packs disjointly with
@@ -118,6 +118,7 @@ def test_best_merge(bn):
 
 
 def test_walk_rejects_large_k(bn):
-    """The walk kernel's step list of free slots is one u32 of nibbles: k <= 9."""
+    """The walk kernel takes k <= 8 free variables (a step's free list is one u32 of
+    nibbles, at most 2 entries per lane)."""
     with pytest.raises(bn.BnregError):
-        bn.bnreg_plan_query(24, 1000, bn.options(free_vars=10))
+        bn.bnreg_plan_query(24, 1000, bn.options(free_vars=9))
