@@ -32,6 +32,10 @@
 #include "kernels.h"
 #include "device.cuh"
 
+#ifndef BNREG_GANG_SYNC
+#define BNREG_GANG_SYNC 1
+#endif
+
 namespace bnr {
 
 constexpr int kW = 8;          // lockstep workers per warp
@@ -444,14 +448,19 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
         }
     }
     // a6-a11: the k + 1 seed pseudo-steps, then d + Upsilon(k), in lockstep
+    // step records are prefetched one step ahead; the empty asm pins the prefetched
+    // registers behind the step body (else the compiler copies them right after
+    // the load and waits for it)
     uint4 r0 = __ldg(wsteps);
     for (int t = 0; t <= k; ++t) {
         const uint4 q = r0;
-        r0 = __ldg(wsteps + t + 1);
+        uint4 nx = __ldg(wsteps + t + 1);
         const int nfe = ((int)(q.w & 31u) + 3) >> 2;
         if (nfe == 0) seed_step<JB, 0, HR, HB>(L, q);
         else if (nfe == 1) seed_step<JB, 1, HR, HB>(L, q);
         else seed_step<JB, 2, HR, HB>(L, q);
+        asm volatile("" : "+r"(nx.x), "+r"(nx.y), "+r"(nx.z), "+r"(nx.w));
+        r0 = nx;
     }
     double c = 1.0, sg = 0.0, hh = 0.0;
     {
@@ -466,9 +475,14 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
     }
     for (int t = k + 1; t < nsteps; ++t) {
         const uint4 q = r0;
-        if (t + 1 < nsteps) r0 = __ldg(wsteps + t + 1);
+        uint4 nx = __ldg(wsteps + t + 1);   // (the device table ends with a pad record)
         if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB>(L, q, c, sg, hh);
         else grc_step<JB, 1, HR, HB>(L, q, c, sg, hh);
+        asm volatile("" : "+r"(nx.x), "+r"(nx.y), "+r"(nx.z), "+r"(nx.w));
+        r0 = nx;
+#if BNREG_GANG_SYNC > 0
+        if ((t & (BNREG_GANG_SYNC - 1)) == 0) asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+#endif
     }
     tm_wait_st();
 }
