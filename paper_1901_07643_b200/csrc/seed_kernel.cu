@@ -175,16 +175,17 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
                     }
             }
         }
-        // the column's walk slot: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        // the column's walk slot: [free 0..k-1 | warp vars 0..p-1 | gang vars 0..g-1 |
+        // tree back set ascending id]; a warp or gang variable in F keeps its (unused) slot
         int slot = 0;
         if (myvar >= 0) {
             if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
-            else if (myvar < p) slot = k + myvar;
+            else if (myvar < fv0) slot = k + myvar;
             else {
-                int cnt = 0;                           // back variables with a smaller id (not in F)
-                for (int l = bh - 1; l >= 0; --l)
+                int cnt = 0;                           // tree back variables with a smaller id (not in F)
+                for (int l = gs - 1; l >= 0; --l)
                     if (!((pack >> l) & 1u) && hv_of(l, m, gs, fv0) < myvar) ++cnt;
-                slot = k + p + cnt;
+                slot = k + fv0 + cnt;
             }
         }
         // remaining tree levels: F -> the leading position joins the front (dropped),

@@ -33,7 +33,7 @@
 #include "device.cuh"
 
 #ifndef BNREG_GANG_SYNC
-#define BNREG_GANG_SYNC 1
+#define BNREG_GANG_SYNC 2
 #endif
 
 namespace bnr {
@@ -210,6 +210,7 @@ struct LaneC {
     uint32_t tb;      // TMEM address of (this warp's lane quarter, column 0)
     uint32_t bval;    // bit j: back entry j (slot k + 4j + h) holds a family of this worker
     uint32_t w;       // worker id = its warp-variable bits
+    uint32_t Xw;      // the worker's warp and gang variables in F (user-id bits)
     uint32_t Fw;      // the worker's F (user ids)
     int fh0;          // this part's first free-list entry: (h - NB) mod 4
     int live;         // w < 2^p
@@ -334,7 +335,7 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
         okv[JB + j] = fo[j];
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
-    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.w, L.Fw | Tsh);
+    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One lockstep GRC step of a lane (a7-a11):
@@ -418,7 +419,10 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
         givens_fr(a, b, c, sg, hh);
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
-    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.w, L.Fw | Tsh);
+#if BNREG_GANG_SYNC == 2
+    asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");   // the gang's stores of this step start together
+#endif
+    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One item (gang) of a warp with JB back entries per lane: fill the lane's TMEM
@@ -480,8 +484,8 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
         else grc_step<JB, 1, HR, HB>(L, q, c, sg, hh);
         asm volatile("" : "+r"(nx.x), "+r"(nx.y), "+r"(nx.z), "+r"(nx.w));
         r0 = nx;
-#if BNREG_GANG_SYNC > 0
-        if ((t & (BNREG_GANG_SYNC - 1)) == 0) asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+#if BNREG_GANG_SYNC == 1
+        asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
 #endif
     }
     tm_wait_st();
@@ -538,6 +542,13 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     L.lnt = (unsigned)__cvta_generic_to_shared(lntab);
     L.out_rss = P.out_rss;
     L.out_bic = P.out_bic;
+    {
+        // the worker's warp and gang variables in F (user-id bits): w, and gang slot wib
+        // bit j = seed-tree level gs + j = gang variable fv0 - 1 - j (plan.h hv_id)
+        uint32_t x = (uint32_t)w;
+        for (int j = 0; j < g; ++j) x |= ((uint32_t)(wib >> j) & 1u) << (fv0 - 1 - j);
+        L.Xw = x;
+    }
     const int nsteps = P.nsteps;
     const uint4* const wsteps = P.wsteps;
     __syncthreads();
@@ -548,15 +559,18 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         const int item = P.item_begin + (int)s_item;
         __syncthreads();
         if (item >= P.item_end) break;
-        const uint32_t pack = P.packs[item] | ((uint32_t)wib << gs);
-        uint32_t Fhi = 0;                       // tree/gang variables in F (user ids)
-        int nB = 0;
-        for (int l = 0; l < bh; ++l) {
-            if ((pack >> l) & 1u) Fhi |= 1u << hv_of(l, m, gs, fv0);
-            else ++nB;
+        const uint32_t pack = P.packs[item];    // the gang's tree levels (gang bits 0)
+        uint32_t Ft = 0;                        // tree variables in F (user ids)
+        int nBt = 0;
+        for (int l = 0; l < gs; ++l) {
+            if ((pack >> l) & 1u) Ft |= 1u << hv_of(l, m, gs, fv0);
+            else ++nBt;
         }
-        const int NB = p + nB;                  // back slots: warp vars, then the back set
-        const int Sw = k + NB;                  // walk slots: free, warp vars, back set
+        // back slots [warp vars | gang vars | tree back set]: the same list in every warp of
+        // the gang (a warp or gang variable in a worker's F keeps its slot, absent), so the
+        // gang's warps run identical steps and store each child's 256 B region together
+        const int NB = fv0 + nBt;
+        const int Sw = k + NB;                  // walk slots: free, back
 
         // ---- a5: this warp's seeds (seed kernel): worker-major blocks [w][row l][slot] of
         //      16 B E pairs; the free slots go to shared memory [l][f][w] (cp.async), the
@@ -573,15 +587,15 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
                 }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        // slot -> variable: [free 0..k-1 | warp vars 0..p-1 | back set ascending id]
+        // slot -> variable: [free 0..k-1 | warp vars 0..p-1 | gang vars | tree back set ascending id]
         int slotvar = -1;
         if (lane < Sw) {
             const int s = lane;
             if (s < k) slotvar = fv0 + s;
-            else if (s < k + p) slotvar = s - k;
+            else if (s < k + fv0) slotvar = s - k;
             else {
-                int c = s - k - p;
-                for (int l = bh - 1; l >= 0; --l)
+                int c = s - k - fv0;
+                for (int l = gs - 1; l >= 0; --l)
                     if (!((pack >> l) & 1u)) {
                         if (c == 0) { slotvar = hv_of(l, m, gs, fv0); break; }
                         --c;
@@ -590,12 +604,12 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         }
         // per-slot records: the warp's running best of the slot's child (from the warp's
         // best so far: only families that beat it take the update path), the table index
-        // of (child v, F without the warp and free variables) and lm
+        // of (child v, F without the warp, gang and free variables) and lm
         if (lane < Sw) {
             const int v = slotvar;
             const uint32_t lm = (1u << v) - 1u;
-            const uint32_t off = P.world1 ? block_offset<true>(P, Fhi, Fhi >> 1, lm)
-                                          : block_offset<false>(P, Fhi, Fhi >> 1, lm);
+            const uint32_t off = P.world1 ? block_offset<true>(P, Ft, Ft >> 1, lm)
+                                          : block_offset<false>(P, Ft, Ft >> 1, lm);
             const uint32_t idx = (uint32_t)((long long)v << shb) + off;
             unsigned char* r = recb + lane * 16;
             *(double*)r = wbb[v];
@@ -603,16 +617,16 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
             *(uint32_t*)(r + 12) = lm;
             bm[lane] = wbm[v];
         }
-        L.Fw = Fhi | (uint32_t)w;               // warp variable j (user id j) in F iff bit j of w
+        L.Fw = Ft | L.Xw;                       // the worker's F: tree, gang and warp variables
         L.KCw = KC + __popc(L.Fw);
         L.fh0 = (h - NB) & 3;
         {
             // back entry j = slot k + 4j + h: exists for b < NB; absent for this worker
-            // when it is warp variable b in F (b < p, bit b of w)
+            // when it is warp or gang variable b (b < fv0) in F
             uint32_t bv = 0;
             for (int j = 0; j < 8; ++j) {
                 const int b = 4 * j + h;
-                if (L.live && b < NB && !(b < p && ((w >> b) & 1))) bv |= 1u << j;
+                if (L.live && b < NB && !(b < fv0 && ((L.Xw >> b) & 1u))) bv |= 1u << j;
             }
             L.bval = bv;
         }
