@@ -257,7 +257,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
                 all.insert(all.end(), tb.begin(), tb.end());
             }
             if (!all.empty()) {
-                all.push_back(WalkStep{});   // pad: the walk kernel prefetches one record past a table
+                for (int j = 0; j < 32; ++j) all.push_back(WalkStep{});   // pad: the walk kernel loads 32-record windows
                 CKH(cudaMalloc(&h->d_wsteps, all.size() * sizeof(WalkStep)));
                 CKH(cudaMemcpy(h->d_wsteps, all.data(), all.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
             }

@@ -452,38 +452,41 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
         }
     }
     // a6-a11: the k + 1 seed pseudo-steps, then d + Upsilon(k), in lockstep
-    // step records are prefetched one step ahead; the empty asm pins the prefetched
-    // registers behind the step body (else the compiler copies them right after
-    // the load and waits for it)
-    uint4 r0 = __ldg(wsteps);
+    // step records: lane l holds record t0 + l of the current 32-step window (one
+    // coalesced load per 32 steps), a step's record is shuffled from lane t - t0
+    uint4 win = make_uint4(0, 0, 0, 0);
+    const int lane = (int)(threadIdx.x & 31);
+    auto record = [&](int t) {
+        if ((t & 31) == 0) win = __ldg(wsteps + t + lane);   // (the device table is padded to whole windows)
+        const int s = t & 31;
+        return make_uint4(__shfl_sync(FULLMASK, win.x, s), __shfl_sync(FULLMASK, win.y, s),
+                          __shfl_sync(FULLMASK, win.z, s), __shfl_sync(FULLMASK, win.w, s));
+    };
+    win = __ldg(wsteps + lane);
+    uint4 qk = make_uint4(0, 0, 0, 0);
     for (int t = 0; t <= k; ++t) {
-        const uint4 q = r0;
-        uint4 nx = __ldg(wsteps + t + 1);
+        const uint4 q = t ? record(t) : make_uint4(__shfl_sync(FULLMASK, win.x, 0), __shfl_sync(FULLMASK, win.y, 0),
+                                                   __shfl_sync(FULLMASK, win.z, 0), __shfl_sync(FULLMASK, win.w, 0));
+        qk = q;
         const int nfe = ((int)(q.w & 31u) + 3) >> 2;
         if (nfe == 0) seed_step<JB, 0, HR, HB>(L, q);
         else if (nfe == 1) seed_step<JB, 1, HR, HB>(L, q);
         else seed_step<JB, 2, HR, HB>(L, q);
-        asm volatile("" : "+r"(nx.x), "+r"(nx.y), "+r"(nx.z), "+r"(nx.w));
-        r0 = nx;
     }
     double c = 1.0, sg = 0.0, hh = 0.0;
     {
         // the first GRC's rotation (the last seed record points at its pivot column)
-        const uint4 q = __ldg(wsteps + k);
         double a = 0.0, b = 1.0;
-        if ((q.w >> 7) & 1u) {
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(L.sbase + q.y));
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(L.sbase + q.y + L.RS));
+        if ((qk.w >> 7) & 1u) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(L.sbase + qk.y));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(L.sbase + qk.y + L.RS));
         }
         givens_fr(a, b, c, sg, hh);
     }
     for (int t = k + 1; t < nsteps; ++t) {
-        const uint4 q = r0;
-        uint4 nx = __ldg(wsteps + t + 1);   // (the device table ends with a pad record)
+        const uint4 q = record(t);
         if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB>(L, q, c, sg, hh);
         else grc_step<JB, 1, HR, HB>(L, q, c, sg, hh);
-        asm volatile("" : "+r"(nx.x), "+r"(nx.y), "+r"(nx.z), "+r"(nx.w));
-        r0 = nx;
 #if BNREG_GANG_SYNC == 1
         asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
 #endif
