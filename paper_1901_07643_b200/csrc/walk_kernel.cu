@@ -194,6 +194,12 @@ __device__ __forceinline__ void sts_pair_if(unsigned a, double x, double u, doub
                  "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(a), "d"(x), "d"(u), "r"(a + rs), "d"(y), "r"((unsigned)q)
                  : "memory");
 }
+__device__ __forceinline__ double lds1(unsigned a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ double2 lds2(unsigned a)
 {
     double2 v;
@@ -360,7 +366,8 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
     unsigned sl[NFE > 0 ? NFE : 1];
     bool fo[NFE > 0 ? NFE : 1];
     free_entries<NFE>(L, q.z, nf, sl, fo);
-    double2 f0[NFE > 0 ? NFE : 1], f1[NFE > 0 ? NFE : 1];
+    double f0[NFE > 0 ? NFE : 1];
+    double2 f1[NFE > 0 ? NFE : 1];
     if constexpr (JB > 0) {
         uint32_t rb[8 * JB];
         const uint32_t tcol = L.tb + (uint32_t)(i * JB * 4);
@@ -368,7 +375,7 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
         tm_ld<8 * JB>(tcol, rb);
 #pragma unroll
         for (int j = 0; j < NFE; ++j) {
-            f0[j] = lds2(bi + sl[j] * kCS);
+            f0[j] = lds1(bi + sl[j] * kCS);
             f1[j] = lds2(bi + sl[j] * kCS + RS);
         }
         tm_wait_ld<8 * JB>(rb);
@@ -390,13 +397,13 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
     } else {
 #pragma unroll
         for (int j = 0; j < NFE; ++j) {
-            f0[j] = lds2(bi + sl[j] * kCS);
+            f0[j] = lds1(bi + sl[j] * kCS);
             f1[j] = lds2(bi + sl[j] * kCS + RS);
         }
     }
 #pragma unroll
     for (int j = 0; j < NFE; ++j) {
-        const double xa = fma(c, f0[j].x, sg * f1[j].x), ya = fma(c, f1[j].x, -sg * f0[j].x);
+        const double xa = fma(c, f0[j], sg * f1[j].x), ya = fma(c, f1[j].x, -sg * f0[j]);
         const double ru = fma(ya, ya, f1[j].y);
         sts_pair_if(bi + sl[j] * kCS, xa, ru, ya, RS, fo[j]);
         rs[JB + j] = ru;
