@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--wpc", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--layout", default="pairs", choices=["pairs", "tables"],
+                    help="pairs: one table of 16 B (RSS, BIC) records (bnreg_run_pairs, the north star's "
+                         "128-bit stores); tables: separate RSS and BIC tables (bnreg_run)")
     ap.add_argument("--outputs", default="both", choices=["both", "rss", "bic", "none"],
                     help="diagnostic: which tables the timed run writes (the metric needs both)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -207,8 +210,13 @@ def bench_ours(args):
     h.set_stream(stream.cuda_stream)
     F = h.num_families()
     total = m << (m - 1)
-    rss = torch.empty(F, dtype=torch.float64, device=dev)
-    bic = torch.empty(F, dtype=torch.float64, device=dev)
+    pairs = args.layout == "pairs" and args.outputs == "both"
+    if pairs:
+        tab = torch.empty((F, 2), dtype=torch.float64, device=dev)
+        rss = bic = None
+    else:
+        rss = torch.empty(F, dtype=torch.float64, device=dev)
+        bic = torch.empty(F, dtype=torch.float64, device=dev)
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)       # column-major n x m
     Rt = torch.empty(m * m, dtype=torch.float64, device=dev)
     bm_d = torch.empty(m, dtype=torch.int32, device=dev)
@@ -242,14 +250,20 @@ def bench_ours(args):
         if rank == 0:
             h.load(Xd)
         broadcast_root()
-        h.run_async(out_r, out_b, bm_d, bb_d)
+        if pairs:
+            h.run_pairs_async(tab, bm_d, bb_d)
+        else:
+            h.run_async(out_r, out_b, bm_d, bb_d)
         gather_best()
 
     def step_e2e():
         if rank == 0:
             h.load(Xpin_np)                      # H2D of X from pinned host memory
         broadcast_root()
-        bm, bb = h.run(rss, bic)                 # D2H of the per-child best
+        if pairs:
+            bm, bb = h.run_pairs(tab)            # D2H of the per-child best
+        else:
+            bm, bb = h.run(rss, bic)
         if world > 1:
             bm_d.copy_(torch.from_numpy(bm.view(np.int32)))
             bb_d.copy_(torch.from_numpy(bb))
@@ -320,6 +334,8 @@ def bench_ours(args):
                           "seed": args.seed if args.seed is not None else 1000 * args.config + 1,
                           "families": total, "k": plan["k"], "pinned": plan["b"], "tree_levels_global": plan["L1"],
                           "packs": plan["npacks"], "parallelism": f"lattice-sharded x{world}",
+                          "layout": ("(RSS, BIC) 16 B records, one table (bnreg_run_pairs)" if pairs else
+                                     "separate RSS and BIC tables (bnreg_run)"),
                           "l2": "outputs (16 B/family, %.1f GB) >> L2 126 MB: every step evicts L2" % (
                               BYTES_PER_FAMILY * total / 1e9)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,

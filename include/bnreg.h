@@ -102,6 +102,16 @@ bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* b
 bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask_dev,
                              double* best_bic_dev);
 
+/* The fused hot path writing one 16 B record per family (the north star's
+ * 128-bit stores): out_pairs is a caller-owned DEVICE buffer of
+ * 2 * bnreg_num_families(h) doubles, 16-byte aligned; family i's RSS is
+ * out_pairs[2i] and its BIC out_pairs[2i + 1] (same index as the separate
+ * tables).  best_mask / best_bic as in bnreg_run (HOST). */
+bnreg_status bnreg_run_pairs(bnreg_t* h, double* out_pairs, uint32_t* best_mask, double* best_bic);
+
+/* As bnreg_run_pairs, asynchronous on the handle's stream; DEVICE best arrays. */
+bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* best_mask_dev, double* best_bic_dev);
+
 /* The north-star calls: the RSS table alone / the BIC table alone. */
 bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
 bnreg_status bnreg_bic(bnreg_t* h, double* out);

@@ -24,7 +24,8 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
-           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_all_rss", "bnreg_bic",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async",
+           "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
            "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_last_error", "bnreg_destroy"]
@@ -70,6 +71,8 @@ def lib():
         "bnreg_local_index": ([H, i64], i64),
         "bnreg_run": ([H, P, P, P, P], i32),
         "bnreg_run_async": ([H, P, P, P, P], i32),
+        "bnreg_run_pairs": ([H, P, P, P], i32),
+        "bnreg_run_pairs_async": ([H, P, P, P], i32),
         "bnreg_all_rss": ([H, P], i32),
         "bnreg_bic": ([H, P], i32),
         "bnreg_set_stream": ([H, P], i32),
@@ -210,6 +213,17 @@ class Bnreg:
         _check(lib().bnreg_run(self._h, _dptr(out_rss), _dptr(out_bic),
                                _hptr(bm) if best else None, _hptr(bb) if best else None))
         return bm, bb
+
+    def run_pairs(self, out_pairs, best=True):
+        """bnreg_run_pairs: one device table of (RSS, BIC) 16 B records -> (best_mask, best_bic) host."""
+        bm = np.zeros(self.m, dtype=np.uint32)
+        bb = np.zeros(self.m)
+        _check(lib().bnreg_run_pairs(self._h, _dptr(out_pairs), _hptr(bm) if best else None,
+                                     _hptr(bb) if best else None))
+        return bm, bb
+
+    def run_pairs_async(self, out_pairs, best_mask_dev=None, best_bic_dev=None):
+        _check(lib().bnreg_run_pairs_async(self._h, _dptr(out_pairs), _dptr(best_mask_dev), _dptr(best_bic_dev)))
 
     def run_async(self, out_rss=None, out_bic=None, best_mask_dev=None, best_bic_dev=None):
         _check(lib().bnreg_run_async(self._h, _dptr(out_rss), _dptr(out_bic), _dptr(best_mask_dev),

@@ -1,6 +1,7 @@
 // bnreg_api.cu -- the C ABI (include/bnreg.h): argument checks, device state,
 // host plan (plan.h) and the launch sequence of the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -443,8 +444,11 @@ static void shard_ranges_of(const Plan& P, int64_t* count, int64_t* starts, int6
     }
 }
 
-static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev)
+static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev,
+                             double* out_pairs = nullptr)
 {
+    if (out_pairs && (reinterpret_cast<uintptr_t>(out_pairs) & 15u))
+        return fail(BNREG_E_INVAL, "out_pairs must be 16-byte aligned");
     if (!h) return fail(BNREG_E_INVAL, "NULL handle");
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded (bnreg_load / bnreg_root_received first)");
     const Plan& P = h->plan;
@@ -471,7 +475,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     if (const char* dbg = getenv("BNREG_DEBUG_SCHED_LEN")) sched_len = std::min(sched_len, atoi(dbg));  // profiling aid
     T.nsteps = P.k + 1 + sched_len;
     T.packs = h->d_packs;
-    T.out_rss = out_rss; T.out_bic = out_bic;
+    T.out_rss = out_rss; T.out_bic = out_bic; T.out_pairs = out_pairs;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
     T.lntab9 = h->d_lntab9;
@@ -530,9 +534,10 @@ static bnreg_status collect_timing(bnreg_t* h)
     return BNREG_OK;
 }
 
-bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask, double* best_bic)
+static bnreg_status run_sync(bnreg_t* h, double* out_rss, double* out_bic, double* out_pairs, uint32_t* best_mask,
+                             double* best_bic)
 {
-    bnreg_status s = run_impl(h, out_rss, out_bic, nullptr, nullptr);
+    bnreg_status s = run_impl(h, out_rss, out_bic, nullptr, nullptr, out_pairs);
     if (s != BNREG_OK) return s;
     const int m = h->plan.m;
     if (best_mask)
@@ -542,6 +547,26 @@ bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* b
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaGetLastError());
     return collect_timing(h);
+}
+
+bnreg_status bnreg_run(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* best_mask, double* best_bic)
+{
+    return run_sync(h, out_rss, out_bic, nullptr, best_mask, best_bic);
+}
+
+bnreg_status bnreg_run_pairs(bnreg_t* h, double* out_pairs, uint32_t* best_mask, double* best_bic)
+{
+    if (!out_pairs) return fail(BNREG_E_INVAL, "out_pairs is NULL");
+    return run_sync(h, nullptr, nullptr, out_pairs, best_mask, best_bic);
+}
+
+bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* bm_dev, double* bb_dev)
+{
+    if (!out_pairs) return fail(BNREG_E_INVAL, "out_pairs is NULL");
+    bnreg_status s = run_impl(h, nullptr, nullptr, bm_dev, bb_dev, out_pairs);
+    if (s != BNREG_OK) return s;
+    if (h->timing) return collect_timing(h);
+    return BNREG_OK;
 }
 
 bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint32_t* bm_dev, double* bb_dev)

@@ -18,6 +18,7 @@ struct TravParams {
     unsigned int* counter;      // this launch's work-queue counter (zeroed before the launches)
     double* out_rss;            // rank-local RSS table (device) or nullptr
     double* out_bic;            // rank-local BIC table (device) or nullptr
+    double* out_pairs;          // rank-local (RSS, BIC) record table (device, 16 B per family) or nullptr
     double* part_bic;           // [warps of all launches][m] per-warp best BIC
     uint32_t* part_mask;        // [warps of all launches][m] per-warp best mask
     double mhalf_n;             // -n/2

@@ -182,6 +182,11 @@ int walk_tmem_cols(int k, int jbmax)
 
 // Predicated stores that stay predicated (no branch around them, so the
 // entries of a step remain one basic block the scheduler can interleave).
+__device__ __forceinline__ void stg2_cs_if(double* p, double a, double b, bool q)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.global.cs.v2.f64 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "d"(a), "d"(b), "r"((unsigned)q));
+}
 __device__ __forceinline__ void stg_cs_if(double* p, double v, bool q)
 {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
@@ -228,11 +233,12 @@ struct LaneC {
     unsigned lnt;        // shared address of the log table
     double* out_rss;
     double* out_bic;
+    double* out_pairs;
 };
 
 // phase C of a step: ln RSS, BIC (a9), the two table stores (a10) and the
 // running-best candidates; new bests (rare) are resolved warp-serially (a11, G14)
-template <int NE, bool HR, bool HB>
+template <int NE, bool HR, bool HB, bool HP>
 __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const unsigned* ra, const bool* okv,
                                         double Kw, uint32_t X, uint32_t S)
 {
@@ -253,6 +259,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
         const uint32_t ix = idx + ((X & lm) | (X1 & ~lm));           // + compress(T | w-bits, child)
         if (HR) stg_cs_if(L.out_rss + ix, rss, okv[e]);
         if (HB) stg_cs_if(L.out_bic + ix, bic, okv[e]);
+        if (HP) stg2_cs_if(L.out_pairs + 2 * (size_t)ix, rss, bic, okv[e]);
         upd |= (okv[e] && (bic >= rr.x || tiny)) ? (1u << e) : 0u;
     }
     unsigned bal = __ballot_sync(FULLMASK, upd != 0);
@@ -275,6 +282,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
                         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rr) : "r"(a + 8));
                         const uint32_t idx = (uint32_t)__double2loint(rr), lm = (uint32_t)__double2hiint(rr);
                         if (HB) L.out_bic[idx + ((X & lm) | (X1 & ~lm))] = PINF;
+                        if (HP) L.out_pairs[2 * (size_t)(idx + ((X & lm) | (X1 & ~lm))) + 1] = PINF;
                     }
                     double cb;
                     uint32_t cm;
@@ -305,7 +313,7 @@ __device__ __forceinline__ void free_entries(const LaneC& L, uint32_t nib, int n
 
 // Seed pseudo-step (reading G11: the seed prefixes {free 0..j-1}, i = j - 1):
 // RSS = U_{i+1} = E_i.y, or U_0 = R_0^2 + E_0.y for the empty prefix; no rotation.
-template <int JB, int NFE, bool HR, bool HB>
+template <int JB, int NFE, bool HR, bool HB, bool HP>
 __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
 {
     constexpr int NE = JB + NFE;
@@ -341,7 +349,7 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
         okv[JB + j] = fo[j];
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
-    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
+    harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One lockstep GRC step of a lane (a7-a11):
@@ -351,7 +359,7 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
 //            shared memory; the pivot Y (now at position i): E_i = (h, 0), R_{i+1} = 0;
 //   givens   the next step's rotation from its pivot column (overlaps phase C);
 //   phase C  harvest().
-template <int JB, int NFE, bool HR, bool HB>
+template <int JB, int NFE, bool HR, bool HB, bool HP>
 __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& c, double& sg, double& hh)
 {
     constexpr int NE = JB + NFE;
@@ -429,12 +437,12 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
 #if BNREG_GANG_SYNC == 2
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");   // the gang's stores of this step start together
 #endif
-    harvest<NE, HR, HB>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
+    harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One item (gang) of a warp with JB back entries per lane: fill the lane's TMEM
 // rows from the seed block, the k + 1 seed pseudo-steps, then Upsilon(k).
-template <int JB, bool HR, bool HB>
+template <int JB, bool HR, bool HB, bool HP>
 __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* src, int k, int SA, int NB,
                                        const uint4* __restrict__ wsteps, int nsteps)
 {
@@ -476,9 +484,9 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
                                                    __shfl_sync(FULLMASK, win.z, 0), __shfl_sync(FULLMASK, win.w, 0));
         qk = q;
         const int nfe = ((int)(q.w & 31u) + 3) >> 2;
-        if (nfe == 0) seed_step<JB, 0, HR, HB>(L, q);
-        else if (nfe == 1) seed_step<JB, 1, HR, HB>(L, q);
-        else seed_step<JB, 2, HR, HB>(L, q);
+        if (nfe == 0) seed_step<JB, 0, HR, HB, HP>(L, q);
+        else if (nfe == 1) seed_step<JB, 1, HR, HB, HP>(L, q);
+        else seed_step<JB, 2, HR, HB, HP>(L, q);
     }
     double c = 1.0, sg = 0.0, hh = 0.0;
     {
@@ -492,8 +500,8 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
     }
     for (int t = k + 1; t < nsteps; ++t) {
         const uint4 q = record(t);
-        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB>(L, q, c, sg, hh);
-        else grc_step<JB, 1, HR, HB>(L, q, c, sg, hh);
+        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB, HP>(L, q, c, sg, hh);
+        else grc_step<JB, 1, HR, HB, HP>(L, q, c, sg, hh);
 #if BNREG_GANG_SYNC == 1
         asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
 #endif
@@ -501,7 +509,7 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
     tm_wait_st();
 }
 
-template <bool HR, bool HB, int JBMAX>
+template <bool HR, bool HB, bool HP, int JBMAX>
 __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __grid_constant__ TravParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -552,6 +560,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     L.lnt = (unsigned)__cvta_generic_to_shared(lntab);
     L.out_rss = P.out_rss;
     L.out_bic = P.out_bic;
+    L.out_pairs = P.out_pairs;
     {
         // the worker's warp and gang variables in F (user-id bits): w, and gang slot wib
         // bit j = seed-tree level gs + j = gang variable fv0 - 1 - j (plan.h hv_id)
@@ -645,18 +654,18 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
 
         const int JB = (NB + 3) >> 2;
         switch (JB) {
-            case 0: walk_item<0, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 1: walk_item<1, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 2: walk_item<2, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 3: walk_item<3, HR, HB>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 0: walk_item<0, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 1: walk_item<1, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 2: walk_item<2, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 3: walk_item<3, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
             default:
                 if constexpr (JBMAX <= 4) {
-                    walk_item<4, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                    walk_item<4, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
                 } else {
-                    if (JB == 4) walk_item<4, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
-                    else if (JB == 5) walk_item<5, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
-                    else if (JB == 6) walk_item<6, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
-                    else walk_item<7, HR, HB>(L, src, k, SA, NB, wsteps, nsteps);
+                    if (JB == 4) walk_item<4, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
+                    else if (JB == 5) walk_item<5, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
+                    else if (JB == 6) walk_item<6, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
+                    else walk_item<7, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
                 }
                 break;
         }
@@ -692,11 +701,11 @@ static size_t walk_launch_smem(const TravParams& P)
     return smem;
 }
 
-template <bool HR, bool HB, int JBMAX>
+template <bool HR, bool HB, bool HP, int JBMAX>
 static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 {
     const size_t smem = walk_launch_smem(P);
-    auto f = walk_kernel<HR, HB, JBMAX>;
+    auto f = walk_kernel<HR, HB, HP, JBMAX>;
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     f<<<grid, 32 << P.g, smem, st>>>(P);
@@ -706,12 +715,13 @@ static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 template <int JBMAX>
 static cudaError_t launch_jb(const TravParams& P, int grid, cudaStream_t st)
 {
+    if (P.out_pairs) return launch_w<false, false, true, JBMAX>(P, grid, st);
     const int key = (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
     switch (key) {
-        case 3: return launch_w<true, true, JBMAX>(P, grid, st);
-        case 2: return launch_w<true, false, JBMAX>(P, grid, st);
-        case 1: return launch_w<false, true, JBMAX>(P, grid, st);
-        default: return launch_w<false, false, JBMAX>(P, grid, st);
+        case 3: return launch_w<true, true, false, JBMAX>(P, grid, st);
+        case 2: return launch_w<true, false, false, JBMAX>(P, grid, st);
+        case 1: return launch_w<false, true, false, JBMAX>(P, grid, st);
+        default: return launch_w<false, false, false, JBMAX>(P, grid, st);
     }
 }
 
@@ -730,7 +740,7 @@ int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int jbmax)
     P.m = m; P.k = k; P.S_alloc = S_alloc; P.g = g; P.lw = 3; P.jbmax = jbmax;
     P.tm_cols = walk_tmem_cols(k, jbmax);
     const size_t smem = walk_launch_smem(P);
-    auto f = jbmax <= 4 ? walk_kernel<true, true, 4> : walk_kernel<true, true, 7>;
+    auto f = jbmax <= 4 ? walk_kernel<true, true, false, 4> : walk_kernel<true, true, false, 7>;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 0;

@@ -38,8 +38,10 @@ def _bic(rss, n, ks):
     return -(n / 2) * np.log(rss / n) - (n / 2) * (1 + np.log(2 * np.pi)) - (ks / 2) * np.log(n)
 
 
-def _run_full(cfg):
-    """The bench configuration: default options, tables on the device."""
+def _run_full(cfg, pairs):
+    """The bench configuration: default options, tables on the device; pairs=True
+    is the bench's layout (bnreg_run_pairs: one table of (RSS, BIC) records), the
+    RSS and BIC columns are strided views of it."""
     import torch
     import paper_1901_07643_b200 as bn
     X = datagen.config_data(cfg)
@@ -47,10 +49,16 @@ def _run_full(cfg):
     h = bn.Bnreg.create(X)
     F = h.num_families()
     assert F == m << (m - 1)
-    rss = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
-    bic = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
-    torch.cuda.synchronize()      # the NaN fills run on torch's stream, the handle on its own
-    bm, bb = h.run(rss, bic)
+    if pairs:
+        t = torch.full((F, 2), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()  # the NaN fill runs on torch's stream, the handle on its own
+        bm, bb = h.run_pairs(t)
+        rss, bic = t[:, 0], t[:, 1]
+    else:
+        rss = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+        bic = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()  # the NaN fills run on torch's stream, the handle on its own
+        bm, bb = h.run(rss, bic)
     torch.cuda.synchronize()
     plan = bn.bnreg_plan_query(m, n)
     h.close()
@@ -70,9 +78,9 @@ def _gather(t, idx):
     return t[torch.from_numpy(np.asarray(idx, dtype=np.int64)).cuda()].cpu().numpy()
 
 
-def _check(cfg, n_uniform, n_chain):
+def _check(cfg, n_uniform, n_chain, pairs=False):
     import torch
-    X, rss, bic, bm, bb, plan = _run_full(cfg)
+    X, rss, bic, bm, bb, plan = _run_full(cfg, pairs)
     n, m = X.shape
     Xc = oracle.centre(X)
     # every entry written, every value finite and positive
@@ -147,8 +155,7 @@ def _check(cfg, n_uniform, n_chain):
     k2 = np.array([bin(int(s)).count("1") for s in S2])
     assert np.abs(b_s - _bic(r_s, n, k2)).max() <= BIC_ATOL
     # the reported best = the maximum of each child's BIC block
-    blk = bic.view(m, 1 << (m - 1))
-    mx = blk.max(dim=1).values.cpu().numpy()
+    mx = np.array([bic[v << (m - 1):(v + 1) << (m - 1)].max().item() for v in range(m)])
     np.testing.assert_array_equal(mx, bb)
     for v in range(m):
         assert _gather(bic, [oracle.index(m, v, int(bm[v]))])[0] == bb[v]
@@ -160,9 +167,13 @@ def test_cfg4_full_size():
     _check(4, 20000, 100000)
 
 
+def test_cfg4_full_size_pairs():
+    _check(4, 20000, 100000, pairs=True)
+
+
 def test_cfg5_full_size():
     import torch
     free, total = torch.cuda.mem_get_info()
     if free < 64e9:
         pytest.skip("cfg5 needs 60 GB of device memory for its tables")
-    _check(5, 5000, 100000)
+    _check(5, 5000, 100000, pairs=True)   # the bench layout

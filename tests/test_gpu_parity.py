@@ -31,11 +31,11 @@ def _bn():
     return bn
 
 
-def _check_full(X, opt=None, o2=False, threads=0):
+def _check_full(X, opt=None, o2=False, threads=0, pairs=False):
     from gpu_util import run_tables
     Xc = oracle.centre(X)
     n, m = X.shape
-    rss, bic, bm, bb, h = run_tables(X, opt)
+    rss, bic, bm, bb, h = run_tables(X, opt, pairs=pairs)
     assert not np.isnan(rss).any(), f"{np.isnan(rss).sum()} RSS entries never written"
     assert not np.isnan(bic).any(), f"{np.isnan(bic).sum()} BIC entries never written"
     if o2:
@@ -77,6 +77,33 @@ def test_cfg1_full_all_k(k):
     bn = _bn()
     X = datagen.config_data(1)
     _check_full(X, bn.options(free_vars=k))
+
+
+@pytest.mark.parametrize("k", [8, 3, 2])
+def test_cfg1_pairs(k):
+    """bnreg_run_pairs (one table of 16 B (RSS, BIC) records, the bench's layout)
+    on cfg1: same parity bar."""
+    bn = _bn()
+    X = datagen.config_data(1)
+    _check_full(X, bn.options(free_vars=k), pairs=True)
+
+
+def test_cfg2_pairs():
+    X = datagen.config_data(2)
+    _check_full(X, pairs=True)
+
+
+def test_pairs_rejects_misaligned():
+    import torch
+    bn = _bn()
+    X = datagen.config_data(1)
+    h = bn.Bnreg.create(X)
+    t = torch.zeros(2 * h.num_families() + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(bn.BnregError):
+        h.run_pairs(t.data_ptr() + 8)
+    with pytest.raises(bn.BnregError):
+        h.run_pairs(None)
+    h.close()
 
 
 @pytest.mark.parametrize("lw", [0, 1, 2, 5])
