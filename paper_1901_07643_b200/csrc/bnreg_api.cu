@@ -478,6 +478,9 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.out_rss = out_rss; T.out_bic = out_bic; T.out_pairs = out_pairs;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
+    // RSS <= 1e-300 (or 0, or subnormal: the fast log then returns ~-709) has ln RSS <= -690.77,
+    // so its BIC >= (n/2) 690.77 + K(32) (K decreases in |S|); 1 below that for rounding
+    T.tiny_bic = (double)P.n / 2.0 * 690.7755278982137 + P.bic_const[32] - 1.0;
     T.lntab9 = h->d_lntab9;
     T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];

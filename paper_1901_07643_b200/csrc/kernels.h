@@ -22,6 +22,7 @@ struct TravParams {
     double* part_bic;           // [warps of all launches][m] per-warp best BIC
     uint32_t* part_mask;        // [warps of all launches][m] per-warp best mask
     double mhalf_n;             // -n/2
+    double tiny_bic;            // lower bound of the BIC (fast log) of any RSS <= 1e-300 (G13 candidates)
     const double2* lntab9;      // fast-log table (512 x (r_j, -ln r_j))
     double Kc[33];              // BIC constant per parent-set size
     int r;                      // rank-selector bits (world > 1)

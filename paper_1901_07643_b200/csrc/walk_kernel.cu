@@ -138,10 +138,12 @@ __device__ __forceinline__ void tm_put(uint32_t* r, double x)
 //   rec     SA * 16 B          per slot (shared by the warp's workers): the warp's running
 //                              best BIC of the slot's child, the table index of (child,
 //                              F without the warp and free variables), lm = (1 << v) - 1
-//   bm      SA * 4 B           the mask of that running best (directly after rec)
+//   bb      SA * 8 B           the running best BIC of the slot's child (rec holds the candidate
+//                              threshold min(best, tiny_bic))
+//   bm      SA * 4 B           the mask of that running best
 //   wbb/wbm 32 * 12 B          the warp's running best per child (kept across items)
 struct WalkLayout {
-    int state, rec, bm, wbb, wbm, per_warp;
+    int state, rec, bb, bm, wbb, wbm, per_warp;
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -153,8 +155,9 @@ __host__ __device__ inline WalkLayout walk_layout(int k, int SA)
     L.state = o;
     o += al16(k * k * kW * 16);
     L.rec = o;
-    L.bm = o + SA * 16;
-    o += al16(SA * 20);
+    L.bb = o + SA * 16;
+    L.bm = o + SA * 24;
+    o += al16(SA * 28);
     L.wbb = o;
     o += 32 * 8;
     L.wbm = o;
@@ -218,6 +221,8 @@ struct LaneC {
     unsigned recb;    // shared address of rec[slot 0]
     unsigned recB;    // shared address of the record of back slot h: rec[k + h]
     unsigned bmb;     // shared address of bm[slot 0]
+    unsigned bbb;     // shared address of bb[slot 0]
+    double tiny_bic;  // a lower bound of the BIC of any RSS <= 1e-300 (G13)
     uint32_t tb;      // TMEM address of (this warp's lane quarter, column 0)
     uint32_t bval;    // bit j: back entry j (slot k + 4j + h) holds a family of this worker
     uint32_t w;       // worker id = its warp-variable bits
@@ -251,7 +256,6 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
         const double rss = rs[e];
         const double lnr = fast_ln9s(rss, L.lnt);
         const double bic = fma(L.mhalf_n, lnr, Kw);
-        const bool tiny = rss <= 1e-300;                             // G13: BIC = +inf, fixed on the rare path
         bics[e] = bic;
         const double2 rr = lds2(ra[e]);
         const uint32_t idx = (uint32_t)__double2loint(rr.y);        // table index of (child, F_w)
@@ -260,7 +264,9 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
         if (HR) stg_cs_if(L.out_rss + ix, rss, okv[e]);
         if (HB) stg_cs_if(L.out_bic + ix, bic, okv[e]);
         if (HP) stg2_cs_if(L.out_pairs + 2 * (size_t)ix, rss, bic, okv[e]);
-        upd |= (okv[e] && (bic >= rr.x || tiny)) ? (1u << e) : 0u;
+        // candidate: BIC >= the slot's threshold min(running best, tiny_bic); a perfect fit
+        // (RSS <= 1e-300, G13: BIC = +inf, fixed on the rare path) has BIC >= tiny_bic
+        upd |= (okv[e] && bic >= rr.x) ? (1u << e) : 0u;
     }
     unsigned bal = __ballot_sync(FULLMASK, upd != 0);
     while (bal) {
@@ -273,7 +279,8 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
             for (int e = 0; e < NE; ++e) {
                 if ((upd >> e) & 1u) {
                     const unsigned a = ra[e];
-                    const unsigned ma = L.bmb + ((a - L.recb) >> 2);   // bm[slot] beside rec[slot]
+                    const unsigned ma = L.bmb + ((a - L.recb) >> 2);   // bm[slot]
+                    const unsigned ba = L.bbb + ((a - L.recb) >> 1);   // bb[slot]
                     double b = bics[e];
                     if (rs[e] <= 1e-300) {
                         // a perfect fit (G13): BIC = +inf, stored over the finite value written above
@@ -286,11 +293,12 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
                     }
                     double cb;
                     uint32_t cm;
-                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(a));
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cb) : "r"(ba));
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cm) : "r"(ma));
                     if (tie_better(b, S, cb, cm)) {
-                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(b) : "memory");
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(ba), "d"(b) : "memory");
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(fmin(b, L.tiny_bic)) : "memory");
                     }
                 }
             }
@@ -537,6 +545,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     unsigned char* const st = wb + Ly.state;
     unsigned char* const recb = wb + Ly.rec;
     uint32_t* const bm = (uint32_t*)(wb + Ly.bm);
+    double* const bbv = (double*)(wb + Ly.bb);
     double* const wbb = (double*)(wb + Ly.wbb);
     uint32_t* const wbm = (uint32_t*)(wb + Ly.wbm);
     const int w = lane & (kW - 1), h = lane >> 3;
@@ -550,6 +559,8 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     L.recb = (unsigned)__cvta_generic_to_shared(recb);
     L.recB = L.recb + (unsigned)(k + h) * 16u;
     L.bmb = (unsigned)__cvta_generic_to_shared(bm);
+    L.bbb = (unsigned)__cvta_generic_to_shared(bbv);
+    L.tiny_bic = P.tiny_bic;
     L.tb = s_taddr + ((uint32_t)(wib * 32) << 16);
     L.w = (uint32_t)w;
     L.live = w < nw;
@@ -631,7 +642,8 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
                                           : block_offset<false>(P, Ft, Ft >> 1, lm);
             const uint32_t idx = (uint32_t)((long long)v << shb) + off;
             unsigned char* r = recb + lane * 16;
-            *(double*)r = wbb[v];
+            *(double*)r = fmin(wbb[v], P.tiny_bic);
+            bbv[lane] = wbb[v];
             *(uint32_t*)(r + 8) = idx;
             *(uint32_t*)(r + 12) = lm;
             bm[lane] = wbm[v];
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         __syncwarp();
         // the per-slot records are the warp's per-child bests (a11)
         if (lane < Sw) {
-            wbb[slotvar] = *(const double*)(recb + lane * 16);
+            wbb[slotvar] = bbv[lane];
             wbm[slotvar] = bm[lane];
         }
         __syncwarp();

@@ -278,3 +278,21 @@ def test_tree_direct_matches_level_by_level():
     finally:
         del os.environ["BNREG_TREE_LEVELS"]
     assert np.array_equal(r1, r2) and np.array_equal(b1, b2) and np.array_equal(m1, m2)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+def test_perfect_fit_scale_g13(pairs):
+    """Reading G13: RSS <= 1e-300 -> BIC = +inf.  cfg1 scaled by 1e-152 passes the
+    (relative) rank check while every RSS is ~1e-302, so every family takes the
+    +inf path (the candidate threshold min(best, tiny_bic) of the walk); every
+    child's best is then the empty set (G14: equal BIC -> smaller |S|)."""
+    from gpu_util import run_tables
+    X = datagen.config_data(1) * 1e-152
+    n, m = X.shape
+    rss, bic, bm, bb, h = run_tables(X, pairs=pairs)
+    ref, _ = oracle.table(oracle.centre(X), want_bic=False)
+    assert (ref <= 1e-300).all()
+    assert (np.abs(rss - ref) / ref).max() <= RSS_RTOL
+    assert np.isposinf(bic).all()
+    assert bm.tolist() == [0] * m and np.isposinf(bb).all()
+    h.close()
