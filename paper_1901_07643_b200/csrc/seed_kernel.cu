@@ -182,10 +182,11 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
             if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
             else if (myvar < fv0) slot = k + myvar;
             else {
-                int cnt = 0;                           // tree back variables with a smaller id (not in F)
-                for (int l = gs - 1; l >= 0; --l)
-                    if (!((pack >> l) & 1u) && hv_of(l, m, gs, fv0) < myvar) ++cnt;
-                slot = k + fv0 + cnt;
+                // tree back variables with a smaller id: tree level l < gs is user id m - 1 - l
+                // (plan.h hv_id), so the back set's id mask is the bit-reversed free levels
+                const uint32_t lv = ~pack & ((1u << gs) - 1u);
+                const uint32_t bmask = (uint32_t)(__brev(lv) >> (32 - m));
+                slot = k + fv0 + __popc(bmask & ((1u << myvar) - 1u));
             }
         }
         // remaining tree levels: F -> the leading position joins the front (dropped),
