@@ -112,6 +112,14 @@ bnreg_status bnreg_run_pairs(bnreg_t* h, double* out_pairs, uint32_t* best_mask,
 /* As bnreg_run_pairs, asynchronous on the handle's stream; DEVICE best arrays. */
 bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* best_mask_dev, double* best_bic_dev);
 
+/* The score the BIC table / record column and the per-child best hold (SURVEY.md §8(f)
+ * NEXT 4): BNREG_SCORE_BIC (default; reading G5), BNREG_SCORE_AIC
+ * (loglik - |S|, higher is better), BNREG_SCORE_LOGLIK (loglik = -(n/2) ln(RSS/n)
+ * - (n/2)(1 + ln 2pi)).  +inf for RSS <= 1e-300 in every score (G13).  Applies to
+ * later runs; BNREG_E_INVAL for another value. */
+enum { BNREG_SCORE_BIC = 0, BNREG_SCORE_AIC = 1, BNREG_SCORE_LOGLIK = 2 };
+bnreg_status bnreg_set_score(bnreg_t* h, int32_t score);
+
 /* The north-star calls: the RSS table alone / the BIC table alone. */
 bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
 bnreg_status bnreg_bic(bnreg_t* h, double* out);

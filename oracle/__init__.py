@@ -63,6 +63,8 @@ def lib():
         L.oracle_rss_reduced.restype = dbl
         L.oracle_bic.argtypes = [dbl, i64, i32]
         L.oracle_bic.restype = dbl
+        L.oracle_score.argtypes = [dbl, i64, i32, i32]
+        L.oracle_score.restype = dbl
         L.oracle_table.argtypes = [P, i64, i32, P, P, i32]
         L.oracle_table.restype = None
         L.oracle_rss_indices.argtypes = [P, i64, i32, P, i64, P, i32]
@@ -137,6 +139,19 @@ def rss_reduced(R0, child: int, mask: int) -> float:
 
 def bic(rss_value: float, n: int, k: int) -> float:
     return lib().oracle_bic(float(rss_value), n, k)
+
+
+SCORE_BIC, SCORE_AIC, SCORE_LL = 0, 1, 2
+
+
+def score(rss_value: float, n: int, k: int, kind: int) -> float:
+    """oracle_score: BIC (0), AIC as loglik - k (1), log-likelihood (2); SURVEY §8(f) NEXT 4."""
+    return lib().oracle_score(float(rss_value), n, k, kind)
+
+
+def score_array(rss_arr, n: int, ks, kind: int):
+    f = lib().oracle_score
+    return np.array([f(float(r), n, int(k), kind) for r, k in zip(rss_arr, ks)])
 
 
 def bic_array(rss_arr, n: int, ks):

@@ -229,6 +229,20 @@ ORACLE_API double oracle_bic(double rss, int64_t n, int k)
     return -(dn / 2.0) * log(rss / dn) - (dn / 2.0) * (1.0 + log(2.0 * M_PI)) - ((double)k / 2.0) * log(dn);
 }
 
+/* ---- other decomposable Gaussian scores -----
+ * score 0 = BIC (as oracle_bic), 1 = AIC in the same "higher is better" scale
+ * (loglik - k), 2 = the maximised log-likelihood
+ * loglik = -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi); +inf for RSS <= 1e-300 (G13). */
+ORACLE_API double oracle_score(double rss, int64_t n, int k, int score)
+{
+    if (rss <= 1e-300) return INFINITY;
+    double dn = (double)n;
+    double ll = -(dn / 2.0) * log(rss / dn) - (dn / 2.0) * (1.0 + log(2.0 * M_PI));
+    if (score == 1) return ll - (double)k;
+    if (score == 2) return ll;
+    return ll - ((double)k / 2.0) * log(dn);
+}
+
 static int popc32(uint32_t x) { return __builtin_popcount(x); }
 
 /* ---- O1 over the whole table ------------------------------------------- */

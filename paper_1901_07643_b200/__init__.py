@@ -19,12 +19,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbnreg.so")
 
 OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE = range(7)
+SCORE_BIC, SCORE_AIC, SCORE_LOGLIK = 0, 1, 2
 _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNREG_E_NOMEM",
           5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
-           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
@@ -72,6 +73,7 @@ def lib():
         "bnreg_run": ([H, P, P, P, P], i32),
         "bnreg_run_async": ([H, P, P, P, P], i32),
         "bnreg_run_pairs": ([H, P, P, P], i32),
+        "bnreg_set_score": ([H, i32], i32),
         "bnreg_run_pairs_async": ([H, P, P, P], i32),
         "bnreg_all_rss": ([H, P], i32),
         "bnreg_bic": ([H, P], i32),
@@ -213,6 +215,10 @@ class Bnreg:
         _check(lib().bnreg_run(self._h, _dptr(out_rss), _dptr(out_bic),
                                _hptr(bm) if best else None, _hptr(bb) if best else None))
         return bm, bb
+
+    def set_score(self, score: int):
+        """bnreg_set_score: SCORE_BIC (default), SCORE_AIC or SCORE_LOGLIK for later runs."""
+        _check(lib().bnreg_set_score(self._h, score))
 
     def run_pairs(self, out_pairs, best=True):
         """bnreg_run_pairs: one device table of (RSS, BIC) 16 B records -> (best_mask, best_bic) host."""

@@ -72,6 +72,7 @@ struct bnreg {
     std::vector<WalkClass> classes;
     int nparts = 0;                // rows of d_part_bic / d_part_mask
     unsigned* d_counters = nullptr;
+    int score = 0;                     // BNREG_SCORE_*
     uint4* d_wsteps = nullptr;     // per-class walk step tables (plan.h WalkStep)
     unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
@@ -478,12 +479,14 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.out_rss = out_rss; T.out_bic = out_bic; T.out_pairs = out_pairs;
     T.part_bic = h->d_part_bic; T.part_mask = h->d_part_mask;
     T.mhalf_n = P.mhalf_n;
+    double K[33];
+    score_constants(P.n, h->score, K);
     // RSS <= 1e-300 (or 0, or subnormal: the fast log then returns ~-709) has ln RSS <= -690.77,
-    // so its BIC >= (n/2) 690.77 + K(32) (K decreases in |S|); 1 below that for rounding
-    T.tiny_bic = (double)P.n / 2.0 * 690.7755278982137 + P.bic_const[32] - 1.0;
+    // so its score >= (n/2) 690.77 + K(32) (K is non-increasing in |S|); 1 below that for rounding
+    T.tiny_bic = (double)P.n / 2.0 * 690.7755278982137 + K[32] - 1.0;
     T.lntab9 = h->d_lntab9;
     T.world1 = P.world == 1 ? 1 : 0;
-    for (int s = 0; s <= 32; ++s) T.Kc[s] = P.bic_const[s];
+    for (int s = 0; s <= 32; ++s) T.Kc[s] = K[s];
     T.r = P.r;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
     CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
@@ -577,6 +580,14 @@ bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint3
     bnreg_status s = run_impl(h, out_rss, out_bic, bm_dev, bb_dev);
     if (s != BNREG_OK) return s;
     if (h->timing) return collect_timing(h);   // timing needs the events: synchronises
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_set_score(bnreg_t* h, int32_t score)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (score < 0 || score > 2) return fail(BNREG_E_INVAL, "score must be BNREG_SCORE_BIC, _AIC or _LOGLIK");
+    h->score = score;
     return BNREG_OK;
 }
 

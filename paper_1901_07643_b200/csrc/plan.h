@@ -297,6 +297,20 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     return P;
 }
 
+// The score epilogue is score = -(n/2) ln RSS + K(|S|) for every decomposable Gaussian
+// score: loglik = -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi),
+// BIC (score 0, reading G5) = loglik - (s/2) ln n, AIC (1) = loglik - s, log-likelihood (2).
+inline void score_constants(int64_t n, int score, double* K33)
+{
+    const long double nn = (long double)n;
+    const long double l2pi = logl(2.0L * 3.14159265358979323846264338327950288L);
+    for (int s = 0; s <= 32; ++s) {
+        const long double ll = (nn / 2) * logl(nn) - (nn / 2) * (1.0L + l2pi);
+        const long double pen = score == 1 ? (long double)s : score == 2 ? 0.0L : ((long double)s / 2) * logl(nn);
+        K33[s] = (double)(ll - pen);
+    }
+}
+
 // Global flat index (SPEC.md:179 / D6): child 2^(m-1) + compress(mask, child).
 inline int64_t family_index(int m, int child, uint32_t mask)
 {

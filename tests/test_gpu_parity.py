@@ -296,3 +296,47 @@ def test_perfect_fit_scale_g13(pairs):
     assert np.isposinf(bic).all()
     assert bm.tolist() == [0] * m and np.isposinf(bb).all()
     h.close()
+
+
+@pytest.mark.parametrize("score", [1, 2])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_other_scores(score, pairs):
+    """bnreg_set_score: AIC (loglik - |S|) and the log-likelihood
+    as the score epilogue, element by element against oracle_score on cfg1 and cfg2
+    (absolute 1e-6 as for BIC), per-child argmax exact (G14); the log-likelihood best
+    is the full parent set."""
+    import torch
+    bn = _bn()
+    for cfg in (1, 2):
+        X = datagen.config_data(cfg)
+        n, m = X.shape
+        h = bn.Bnreg.create(X)
+        h.set_score(score)
+        F = h.num_families()
+        if pairs:
+            t = torch.full((F, 2), float("nan"), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            bm, bb = h.run_pairs(t)
+            torch.cuda.synchronize()
+            rss, sc = t[:, 0].cpu().numpy(), t[:, 1].cpu().numpy()
+        else:
+            r = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+            b = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            bm, bb = h.run(r, b)
+            torch.cuda.synchronize()
+            rss, sc = r.cpu().numpy(), b.cpu().numpy()
+        ref, _ = oracle.table(oracle.centre(X), want_bic=False)
+        assert (np.abs(rss - ref) / ref).max() <= RSS_RTOL
+        _, S = oracle.masks_of(m, np.arange(F))
+        ks = np.array([bin(int(s)).count("1") for s in S])
+        ref_sc = oracle.score_array(ref, n, ks, score)
+        assert np.abs(sc - ref_sc).max() <= BIC_ATOL
+        om, ob = oracle.best(ref_sc, m)
+        assert np.array_equal(bm, om)
+        np.testing.assert_allclose(bb, ob, atol=BIC_ATOL)
+        if score == 2:
+            assert [int(x) for x in bm] == [((1 << m) - 1) & ~(1 << v) for v in range(m)]
+        with pytest.raises(bn.BnregError):
+            h.set_score(3)
+        h.close()

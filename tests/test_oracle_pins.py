@@ -286,3 +286,36 @@ def test_permutation_invariance():
         ov = perm[v]
         oS = sum(1 << perm[u] for u in range(m) if (S >> u) & 1)
         assert r2[idx] == pytest.approx(r1[oracle.index(m, ov, oS)], rel=1e-12)
+
+
+def test_other_scores_spec_value_and_penalties():
+    """the maximised Gaussian log-likelihood
+    of SPEC's example (n=50, rss=50) is -25(1 + ln 2 pi) = -70.946926660 whatever |S|;
+    AIC (loglik - k) and BIC (loglik - (k/2) ln n) subtract their per-parameter penalties;
+    every score is +inf for RSS <= 1e-300 (G13); BIC agrees with oracle_bic."""
+    for k in (0, 1, 3, 7):
+        ll = oracle.score(50.0, 50, k, oracle.SCORE_LL)
+        assert ll == pytest.approx(-70.946926660, abs=1e-9)
+        assert oracle.score(50.0, 50, k, oracle.SCORE_AIC) == pytest.approx(ll - k, abs=1e-12)
+        assert oracle.score(50.0, 50, k, oracle.SCORE_BIC) == pytest.approx(ll - k / 2 * math.log(50), abs=1e-12)
+        assert oracle.score(50.0, 50, k, oracle.SCORE_BIC) == oracle.bic(50.0, 50, k)
+    for kind in (oracle.SCORE_BIC, oracle.SCORE_AIC, oracle.SCORE_LL):
+        assert math.isinf(oracle.score(1e-301, 50, 2, kind))
+
+
+def test_loglik_best_is_the_full_parent_set():
+    """Without a penalty the best set is V minus the child: RSS is non-increasing in S
+    (strictly for generic data), so the log-likelihood argmax is the full set -- on the
+    golden m=3 table (exact rationals, tests/golden/m3_table.json) and on cfg1."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "m3_table.json")))
+    X = np.array(g["rows"], dtype=float)
+    for Xr in (X, datagen.config_data(1)):
+        n, m = Xr.shape
+        rss, _ = oracle.table(oracle.centre(Xr), want_bic=False)
+        _, S = oracle.masks_of(m, np.arange(m << (m - 1)))
+        ks = np.array([bin(int(s)).count("1") for s in S])
+        ll = oracle.score_array(rss, n, ks, oracle.SCORE_LL)
+        bm, _ = oracle.best(ll, m)
+        assert [int(b) for b in bm] == [((1 << m) - 1) & ~(1 << v) for v in range(m)]
