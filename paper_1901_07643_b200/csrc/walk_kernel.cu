@@ -32,8 +32,10 @@
 #include "kernels.h"
 #include "device.cuh"
 
-#ifndef BNREG_GANG_SYNC
-#define BNREG_GANG_SYNC 2
+#ifndef BNREG_SYNC_EVERY
+#define BNREG_SYNC_EVERY 16  // (RSS, BIC) records: gang barrier every this many steps (a power of two;
+                             // measured at cfg5: 1 13.0 ms, 4 12.45, 16 12.3, 64 12.7, none 13.7); the
+                             // two-table layout's 64 B pieces need it every step (16: 20.3 vs 15.2 ms)
 #endif
 
 namespace bnr {
@@ -368,7 +370,7 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
 //   givens   the next step's rotation from its pivot column (overlaps phase C);
 //   phase C  harvest().
 template <int JB, int NFE, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& c, double& sg, double& hh)
+__device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& c, double& sg, double& hh, bool sync)
 {
     constexpr int NE = JB + NFE;
     const uint32_t fl = q.w;
@@ -442,9 +444,9 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
         givens_fr(a, b, c, sg, hh);
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
-#if BNREG_GANG_SYNC == 2
-    asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");   // the gang's stores of this step start together
-#endif
+    // the gang's stores start together (DRAM write combining of the 4 warps' parts of each
+    // region) every BNREG_SYNC_EVERY steps: the barrier costs more than the last bit of combining
+    if (sync) asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
     harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
@@ -506,13 +508,11 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
         }
         givens_fr(a, b, c, sg, hh);
     }
+    constexpr int kSync = HP ? BNREG_SYNC_EVERY : 1;
     for (int t = k + 1; t < nsteps; ++t) {
         const uint4 q = record(t);
-        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB, HP>(L, q, c, sg, hh);
-        else grc_step<JB, 1, HR, HB, HP>(L, q, c, sg, hh);
-#if BNREG_GANG_SYNC == 1
-        asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
-#endif
+        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB, HP>(L, q, c, sg, hh, (t & (kSync - 1)) == 0);
+        else grc_step<JB, 1, HR, HB, HP>(L, q, c, sg, hh, (t & (kSync - 1)) == 0);
     }
     tm_wait_st();
 }
