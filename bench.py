@@ -206,7 +206,11 @@ def bench_ours(args):
     opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, warps_per_cta=args.wpc)
     h = bn.Bnreg(n, m, opt)
     plan = bn.bnreg_plan_query(m, n, opt)
-    stream = torch.cuda.current_stream(dev)
+    # one explicit (non-legacy) stream for torch and the handle: the timing events are
+    # recorded on the stream the kernels run on (the legacy default stream would make
+    # bnreg_set_stream fall back to the handle's own stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     h.set_stream(stream.cuda_stream)
     F = h.num_families()
     total = m << (m - 1)

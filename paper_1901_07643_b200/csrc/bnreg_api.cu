@@ -19,6 +19,26 @@ using namespace bnr;
 
 static thread_local std::string g_err;
 
+// Wait for the stream by polling: cudaStreamSynchronize under the default
+// "auto" schedule may yield the host thread, and its wake-up costs ~1 ms per
+// synchronous call (measured: tools/e2e_probe.py); the calls that wait are
+// short and the caller asked to block anyway.
+static cudaError_t stream_wait(cudaStream_t st)
+{
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaErrorNotReady) return e;
+    }
+}
+static cudaError_t event_wait(cudaEvent_t ev)
+{
+    for (;;) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e != cudaErrorNotReady) return e;
+    }
+}
+
+
 static bnreg_status fail(bnreg_status s, const std::string& msg)
 {
     g_err = msg;
@@ -332,7 +352,7 @@ bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
     CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
     int status = 0;
     CK(cudaMemcpyAsync(&status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h->stream));
     h->loaded = false;
     if (status & 2) return fail(BNREG_E_NONFINITE, "X contains NaN or Inf");
     if (status & 4) return fail(BNREG_E_RANK, "data is rank deficient (|r_jj| <= 1e-12 max column norm)");
@@ -346,7 +366,7 @@ bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev)
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
     const int m = h->plan.m;
     CK(cudaMemcpyAsync(R_dev, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h->stream));
     return BNREG_OK;
 }
 
@@ -355,7 +375,7 @@ bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev)
     if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
     const int m = h->plan.m;
     CK(cudaMemcpyAsync(h->d_root, R_dev, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h->stream));
     h->loaded = true;
     return BNREG_OK;
 }
@@ -366,7 +386,7 @@ bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host)
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
     const int m = h->plan.m;
     if (R_host) {
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h->stream));
         CK(cudaMemcpy(R_host, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost));
     }
     if (order_host)
@@ -529,7 +549,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
 static bnreg_status collect_timing(bnreg_t* h)
 {
     if (!h->timing) return BNREG_OK;
-    CK(cudaEventSynchronize(h->ev[3]));
+    CK(event_wait(h->ev[3]));
     float a = 0, b = 0, c = 0, d = 0;
     CK(cudaEventElapsedTime(&a, h->ev[0], h->ev[3]));
     CK(cudaEventElapsedTime(&b, h->ev[0], h->ev[1]));
@@ -550,7 +570,7 @@ static bnreg_status run_sync(bnreg_t* h, double* out_rss, double* out_bic, doubl
         CK(cudaMemcpyAsync(best_mask, h->d_best_mask, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
     if (best_bic)
         CK(cudaMemcpyAsync(best_bic, h->d_best_bic, m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h->stream));
     CK(cudaGetLastError());
     return collect_timing(h);
 }
@@ -635,7 +655,7 @@ bnreg_status bnreg_debug_ln(bnreg_t* h, const double* x_dev, double* out_dev, in
 {
     if (!h || (!x_dev && count > 0) || (!out_dev && count > 0)) return fail(BNREG_E_INVAL, "NULL argument");
     CK(launch_debug_ln(x_dev, out_dev, count, h->d_lntab9, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h->stream));
     return BNREG_OK;
 }
 
