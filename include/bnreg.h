@@ -120,6 +120,16 @@ bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* best
 enum { BNREG_SCORE_BIC = 0, BNREG_SCORE_AIC = 1, BNREG_SCORE_LOGLIK = 2 };
 bnreg_status bnreg_set_score(bnreg_t* h, int32_t score);
 
+/* Least-squares coefficients ("solve the regression equations"; SURVEY.md
+ * §8(f) NEXT 1) of each child's regression on one parent set per child, from the
+ * root R (X~ = Q0 R0: the regression of R0[:,v] on R0[:,S]).  masks: HOST, m
+ * entries (bit v of masks[v] is ignored), or NULL for the per-child best sets of
+ * the last run.  beta: HOST, m*m doubles, row-major: beta[v*m + u] is the
+ * coefficient of parent u in child v's regression on the centred data, 0 for u
+ * outside the set.  Synchronous.  BNREG_E_STATE before data is loaded (or, with
+ * masks NULL, before a run). */
+bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta);
+
 /* The north-star calls: the RSS table alone / the BIC table alone. */
 bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
 bnreg_status bnreg_bic(bnreg_t* h, double* out);

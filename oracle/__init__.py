@@ -144,6 +144,21 @@ def bic(rss_value: float, n: int, k: int) -> float:
 SCORE_BIC, SCORE_AIC, SCORE_LL = 0, 1, 2
 
 
+def coefficients(Xc, child: int, mask: int):
+    """Least-squares coefficients of child on the parent set `mask` ("solve
+    the regression equations for each family"): the plain
+    definition on the centred data, argmin_b ||x_v - X_S b||, by numpy's lstsq
+    (a library primitive).  Returns a length-m vector (0 outside the set)."""
+    Xc = np.asarray(Xc, dtype=np.float64)
+    m = Xc.shape[1]
+    S = [u for u in range(m) if (mask >> u) & 1 and u != child]
+    beta = np.zeros(m)
+    if S:
+        b, *_ = np.linalg.lstsq(Xc[:, S], Xc[:, child], rcond=None)
+        beta[S] = b
+    return beta
+
+
 def score(rss_value: float, n: int, k: int, kind: int) -> float:
     """oracle_score: BIC (0), AIC as loglik - k (1), log-likelihood (2); SURVEY §8(f) NEXT 4."""
     return lib().oracle_score(float(rss_value), n, k, kind)

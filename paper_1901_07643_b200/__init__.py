@@ -25,7 +25,7 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
-           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
@@ -74,6 +74,7 @@ def lib():
         "bnreg_run_async": ([H, P, P, P, P], i32),
         "bnreg_run_pairs": ([H, P, P, P], i32),
         "bnreg_set_score": ([H, i32], i32),
+        "bnreg_coefficients": ([H, P, P], i32),
         "bnreg_run_pairs_async": ([H, P, P, P], i32),
         "bnreg_all_rss": ([H, P], i32),
         "bnreg_bic": ([H, P], i32),
@@ -215,6 +216,14 @@ class Bnreg:
         _check(lib().bnreg_run(self._h, _dptr(out_rss), _dptr(out_bic),
                                _hptr(bm) if best else None, _hptr(bb) if best else None))
         return bm, bb
+
+    def coefficients(self, masks=None) -> np.ndarray:
+        """bnreg_coefficients: least-squares coefficients of each child on masks[child] (None:
+        the last run's per-child best sets) -> m x m array, beta[v, u] for parent u of child v."""
+        beta = np.zeros((self.m, self.m))
+        mk = None if masks is None else np.ascontiguousarray(masks, dtype=np.uint32)
+        _check(lib().bnreg_coefficients(self._h, _hptr(mk) if mk is not None else None, _hptr(beta)))
+        return beta
 
     def set_score(self, score: int):
         """bnreg_set_score: SCORE_BIC (default), SCORE_AIC or SCORE_LOGLIK for later runs."""

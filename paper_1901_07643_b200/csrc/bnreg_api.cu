@@ -93,6 +93,9 @@ struct bnreg {
     int nparts = 0;                // rows of d_part_bic / d_part_mask
     unsigned* d_counters = nullptr;
     int score = 0;                     // BNREG_SCORE_*
+    bool ran = false;                  // a run wrote d_best_mask
+    double* d_coef = nullptr;          // bnreg_coefficients output (m*m)
+    uint32_t* d_cmask = nullptr;       // bnreg_coefficients input masks
     uint4* d_wsteps = nullptr;     // per-class walk step tables (plan.h WalkStep)
     unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
@@ -115,7 +118,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds};
+                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -543,6 +546,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->nparts, P.m,
                           bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask, st));
     if (h->timing) CK(cudaEventRecord(h->ev[3], st));
+    h->ran = true;
     return BNREG_OK;
 }
 
@@ -600,6 +604,27 @@ bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint3
     bnreg_status s = run_impl(h, out_rss, out_bic, bm_dev, bb_dev);
     if (s != BNREG_OK) return s;
     if (h->timing) return collect_timing(h);   // timing needs the events: synchronises
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta)
+{
+    if (!h || !beta) return fail(BNREG_E_INVAL, "NULL handle or beta");
+    if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
+    if (!masks && !h->ran) return fail(BNREG_E_STATE, "no run yet: pass the parent sets");
+    const int m = h->plan.m;
+    if (!h->d_coef) {
+        CK(cudaMalloc(&h->d_coef, (size_t)m * m * sizeof(double)));
+        CK(cudaMalloc(&h->d_cmask, (size_t)m * sizeof(uint32_t)));
+    }
+    const uint32_t* dm = h->d_best_mask;
+    if (masks) {
+        CK(cudaMemcpyAsync(h->d_cmask, masks, (size_t)m * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
+        dm = h->d_cmask;
+    }
+    CK(launch_coefficients(h->d_root, h->d_order, m, dm, h->d_coef, h->stream));
+    CK(cudaMemcpyAsync(beta, h->d_coef, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(stream_wait(h->stream));
     return BNREG_OK;
 }
 

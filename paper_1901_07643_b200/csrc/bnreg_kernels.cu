@@ -325,4 +325,70 @@ cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- coefficients
+// The least-squares coefficients of child v on parent set S ("solve the
+// regression equations"), from the root R: X~ = Q0 R0 with Q0 orthonormal, so the
+// regression of x~_v on X~_S is that of R0[:, v] on R0[:, S].  One warp per child,
+// lane = row of the m x (|S| + 1) matrix [R0[:, S] | R0[:, v]] (columns by ascending
+// user id): Householder QR, then back-substitution on the |S| x |S| triangle.
+__global__ void __launch_bounds__(32) coef_kernel(const double* __restrict__ R, const int* __restrict__ order, int m,
+                                                  const uint32_t* __restrict__ masks, double* __restrict__ beta)
+{
+    __shared__ double M[32 * 33];          // column-major, ld 32
+    __shared__ int cols[32];
+    const int v = blockIdx.x, lane = threadIdx.x;
+    const uint32_t S = masks[v] & ~(1u << v);
+    // position of user id u in the root order
+    int k = 0;
+    if (lane == 0) {
+        for (int u = 0; u < m; ++u)
+            if ((S >> u) & 1u) cols[k++] = u;
+        cols[k] = v;
+    }
+    __syncwarp();
+    k = __popc(S);
+    for (int j = 0; j <= k; ++j) {
+        const int u = cols[j];
+        int pu = 0;
+        for (int c = 0; c < m; ++c)
+            if (order[c] == u) pu = c;
+        M[j * 32 + lane] = lane < m ? R[(size_t)lane * m + pu] : 0.0;
+    }
+    __syncwarp();
+    for (int j = 0; j < k; ++j) {
+        const double xj = M[j * 32 + lane];
+        const double x = lane >= j ? xj : 0.0;
+        const double nrm2 = warp_sum(x * x);
+        const double x0 = __shfl_sync(FULLMASK, xj, j);
+        const double alpha = x0 > 0.0 ? -sqrt(nrm2) : sqrt(nrm2);
+        const double vr = lane == j ? x0 - alpha : x;          // Householder vector (rows >= j)
+        const double vn2 = nrm2 - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+        for (int c = j + 1; c <= k; ++c) {
+            const double mc = M[c * 32 + lane];
+            const double d = warp_sum(vr * mc);
+            if (lane >= j && vn2 > 0.0) M[c * 32 + lane] = mc - 2.0 * vr * d / vn2;
+        }
+        __syncwarp();
+        if (lane == j) M[j * 32 + j] = alpha;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        double b[32];
+        for (int i = k - 1; i >= 0; --i) {
+            double t = M[k * 32 + i];
+            for (int c = i + 1; c < k; ++c) t -= M[c * 32 + i] * b[c];
+            b[i] = t / M[i * 32 + i];
+        }
+        for (int u = 0; u < m; ++u) beta[(size_t)v * m + u] = 0.0;
+        for (int i = 0; i < k; ++i) beta[(size_t)v * m + cols[i]] = b[i];
+    }
+}
+
+cudaError_t launch_coefficients(const double* R, const int* order, int m, const uint32_t* masks, double* beta,
+                                cudaStream_t st)
+{
+    coef_kernel<<<m, 32, 0, st>>>(R, order, m, masks, beta);
+    return cudaGetLastError();
+}
+
 }  // namespace bnr

@@ -73,6 +73,9 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st);
 
+// least-squares coefficients of every child on masks[child] from the root R (one warp per child)
+cudaError_t launch_coefficients(const double* R, const int* order, int m, const uint32_t* masks, double* beta,
+                                cudaStream_t st);
 cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2* tab, cudaStream_t st);
 
 }  // namespace bnr

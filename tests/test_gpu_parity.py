@@ -340,3 +340,30 @@ def test_other_scores(score, pairs):
         with pytest.raises(bn.BnregError):
             h.set_score(3)
         h.close()
+
+
+def test_coefficients_against_oracle():
+    """bnreg_coefficients: the per-child best sets of the last run
+    and random sets on cfg1, cfg2 and the near-collinear cfg3, against oracle.coefficients
+    (lstsq on the centred data); relative 1e-8 of the coefficient scale (cfg3: 1e-5, its
+    pair is ill-conditioned, kappa ~ 5e7)."""
+    import torch
+    bn = _bn()
+    rng = np.random.default_rng(11)
+    for cfg, tol in ((1, 1e-8), (2, 1e-8), (3, 1e-5)):
+        X = datagen.config_data(cfg)
+        n, m = X.shape
+        Xc = oracle.centre(X)
+        h = bn.Bnreg.create(X)
+        with pytest.raises(bn.BnregError):
+            h.coefficients()                      # no run yet
+        bm, _ = h.run_pairs(torch.empty((h.num_families(), 2), dtype=torch.float64, device="cuda"))
+        torch.cuda.synchronize()
+        sets = [bm.astype(np.uint32), rng.integers(0, 1 << m, size=m, dtype=np.int64).astype(np.uint32)]
+        for i, masks in enumerate(sets):
+            beta = h.coefficients(None if i == 0 else masks)
+            for v in range(m):
+                ref = oracle.coefficients(Xc, v, int(masks[v]) & ~(1 << v))
+                scale = max(1.0, np.abs(ref).max())
+                assert np.abs(beta[v] - ref).max() <= tol * scale, (cfg, v)
+        h.close()

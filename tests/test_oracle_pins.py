@@ -319,3 +319,29 @@ def test_loglik_best_is_the_full_parent_set():
         ll = oracle.score_array(rss, n, ks, oracle.SCORE_LL)
         bm, _ = oracle.best(ll, m)
         assert [int(b) for b in bm] == [((1 << m) - 1) & ~(1 << v) for v in range(m)]
+
+
+def test_coefficients_exact_and_planted():
+    """oracle.coefficients against exact rational normal equations
+    on the golden m=3 data (beta = G_SS^-1 G_Sv, G the centred Gram [[10,11,9],[11,34,5],
+    [9,5,10]]: A on {B,C} -> (65/315, 251/315), whose residual G_AA - G_AS beta is the
+    golden table's RSS(A|{B,C}) = 176/315) and a planted zero-noise relation
+    x2 = 1.5 x0 - 2 x1 recovered exactly."""
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "m3_table.json")))
+    X = np.array(g["rows"], dtype=float)
+    Xc = oracle.centre(X)
+    G = [[Fraction(10), Fraction(11), Fraction(9)], [Fraction(11), Fraction(34), Fraction(5)],
+         [Fraction(9), Fraction(5), Fraction(10)]]
+    # A | {B, C}: solve [[34, 5], [5, 10]] b = [11, 9]
+    det = G[1][1] * G[2][2] - G[1][2] * G[2][1]
+    b1 = (G[2][2] * G[1][0] - G[1][2] * G[2][0]) / det
+    b2 = (G[1][1] * G[2][0] - G[2][1] * G[1][0]) / det
+    assert (b1, b2) == (Fraction(65, 315), Fraction(251, 315))
+    assert G[0][0] - G[0][1] * b1 - G[0][2] * b2 == Fraction(176, 315)
+    beta = oracle.coefficients(Xc, 0, 0b110)
+    assert beta[0] == 0 and abs(beta[1] - float(b1)) < 1e-13 and abs(beta[2] - float(b2)) < 1e-13
+    rng = np.random.default_rng(3)
+    Z = rng.standard_normal((50, 4))
+    Z[:, 2] = 1.5 * Z[:, 0] - 2.0 * Z[:, 1]
+    bz = oracle.coefficients(oracle.centre(Z), 2, 0b11)
+    np.testing.assert_allclose(bz, [1.5, -2.0, 0.0, 0.0], atol=1e-12)
