@@ -120,6 +120,19 @@ bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* best
 enum { BNREG_SCORE_BIC = 0, BNREG_SCORE_AIC = 1, BNREG_SCORE_LOGLIK = 2 };
 bnreg_status bnreg_set_score(bnreg_t* h, int32_t score);
 
+/* Best parent set within every candidate set (the step after
+ * the score table in exact structure search): for every child v and
+ * candidate set C (entry i = bnreg_index(m, v, C)), best_score[i] = the maximum over
+ * S subset of C of the score of (v, S) and best_mask[i] = that S (user ids; G14
+ * tie-break: larger score, then smaller |S|, then smaller mask).  scores: DEVICE, the
+ * score column of a run on this handle: the BIC table (stride 1) or the record
+ * table's column (out_pairs + 1, stride 2).  best_score / best_mask: DEVICE,
+ * bnreg_num_families entries each (best_score may alias scores when stride == 1).
+ * Single rank only (world 1: a child's candidate lattice is not split).
+ * Asynchronous on the handle's stream. */
+bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride, double* best_score,
+                                uint32_t* best_mask);
+
 /* Least-squares coefficients ("solve the regression equations"; SURVEY.md
  * §8(f) NEXT 1) of each child's regression on one parent set per child, from the
  * root R (X~ = Q0 R0: the regression of R0[:,v] on R0[:,S]).  masks: HOST, m

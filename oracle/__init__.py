@@ -144,6 +144,71 @@ def bic(rss_value: float, n: int, k: int) -> float:
 SCORE_BIC, SCORE_AIC, SCORE_LL = 0, 1, 2
 
 
+def _user_mask(c: int, v: int) -> int:
+    lo = c & ((1 << v) - 1)
+    return lo | ((c >> v) << (v + 1))
+
+
+def _g14_better(s1, S1, s2, S2) -> bool:
+    """G14: larger score, then smaller |S|, then smaller mask."""
+    if s1 != s2:
+        return s1 > s2
+    p1, p2 = bin(S1).count("1"), bin(S2).count("1")
+    return p1 < p2 if p1 != p2 else S1 < S2
+
+
+def best_subsets_brute(scores, m: int):
+    """SURVEY §8(f) NEXT 3, the plain definition (small m only): for every child v and
+    candidate set C (table index of (v, C)), the best score over all S subset of C and
+    that S (user ids), G14 tie-break.  Enumerates the subsets of every C."""
+    scores = np.asarray(scores, dtype=np.float64)
+    F = m << (m - 1)
+    out_s = np.empty(F)
+    out_m = np.empty(F, dtype=np.uint32)
+    for v in range(m):
+        for c in range(1 << (m - 1)):
+            bs, bm = None, None
+            sub = c
+            while True:
+                sc = scores[(v << (m - 1)) + sub]
+                S = _user_mask(sub, v)
+                if bs is None or _g14_better(sc, S, bs, bm):
+                    bs, bm = sc, S
+                if sub == 0:
+                    break
+                sub = (sub - 1) & c
+            out_s[(v << (m - 1)) + c] = bs
+            out_m[(v << (m - 1)) + c] = bm
+    return out_s, out_m
+
+
+def best_subsets(scores, m: int):
+    """The same by the subset-max recursion bps(v, C) = best(score(v, C), bps(v, C - {u}))
+    taken one bit at a time (Silander & Myllymaki's step), vectorised; pinned against
+    best_subsets_brute.  Compressed masks keep the order and popcount of user masks, so
+    G14 compares them directly."""
+    scores = np.asarray(scores, dtype=np.float64)
+    nb = m - 1
+    out_s = scores.reshape(m, 1 << nb).copy()
+    c = np.tile(np.arange(1 << nb, dtype=np.int64), (m, 1))
+    pop = np.vectorize(lambda x: bin(int(x)).count("1"))
+    popc = pop(np.arange(1 << nb)).astype(np.int64)
+    for b in range(nb):
+        idx = np.arange(1 << nb)
+        hi = idx[(idx >> b) & 1 == 1]
+        lo = hi ^ (1 << b)
+        sj, si = out_s[:, lo], out_s[:, hi]
+        cj, ci = c[:, lo], c[:, hi]
+        pj, pi = popc[cj], popc[ci]
+        better = (sj > si) | ((sj == si) & ((pj < pi) | ((pj == pi) & (cj < ci))))
+        out_s[:, hi] = np.where(better, sj, si)
+        c[:, hi] = np.where(better, cj, ci)
+    v = np.arange(m)[:, None]
+    lm = (np.int64(1) << v) - 1
+    um = (c & lm) | ((c & ~lm) << 1)
+    return out_s.reshape(-1), um.reshape(-1).astype(np.uint32)
+
+
 def coefficients(Xc, child: int, mask: int):
     """Least-squares coefficients of child on the parent set `mask` ("solve
     the regression equations for each family"): the plain

@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu", "walk_kernel.cu", "seed_kernel.cu"]
+SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu", "walk_kernel.cu", "seed_kernel.cu", "bps_kernel.cu"]
 HEADERS = ["plan.h", "kernels.h", "device.cuh"]
 OUT = os.path.join(HERE, "libbnreg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

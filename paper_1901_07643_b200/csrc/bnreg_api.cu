@@ -607,6 +607,18 @@ bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint3
     return BNREG_OK;
 }
 
+bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride, double* best_score,
+                                uint32_t* best_mask)
+{
+    if (!h || !scores || !best_score || !best_mask) return fail(BNREG_E_INVAL, "NULL argument");
+    if (stride < 1) return fail(BNREG_E_INVAL, "stride must be >= 1");
+    if (h->plan.world != 1) return fail(BNREG_E_INVAL, "bnreg_best_subsets needs the whole table (world 1)");
+    if (stride != 1 && (const void*)scores == (const void*)best_score)
+        return fail(BNREG_E_INVAL, "best_score may alias scores only with stride 1");
+    CK(launch_bps(scores, stride, h->plan.m, best_score, best_mask, h->stream));
+    return BNREG_OK;
+}
+
 bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta)
 {
     if (!h || !beta) return fail(BNREG_E_INVAL, "NULL handle or beta");

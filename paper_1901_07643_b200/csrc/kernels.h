@@ -73,6 +73,8 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, cudaStream_t st);
 
+// best parent set within every candidate set (subset-max transform of a score column)
+cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_s, uint32_t* out_m, cudaStream_t st);
 // least-squares coefficients of every child on masks[child] from the root R (one warp per child)
 cudaError_t launch_coefficients(const double* R, const int* order, int m, const uint32_t* masks, double* beta,
                                 cudaStream_t st);

@@ -177,3 +177,41 @@ def test_cfg5_full_size():
     if free < 64e9:
         pytest.skip("cfg5 needs 60 GB of device memory for its tables")
     _check(5, 5000, 100000, pairs=True)   # the bench layout
+
+
+def test_cfg4_best_subsets_sampled():
+    """bnreg_best_subsets at cfg4's full size (23 mask bits: the low tile and two high
+    groups), in place over the record table's BIC column copy: for sampled candidate
+    sets of up to 9 variables, the maximum over their subsets by enumeration of the
+    GPU's own scores (G14), and for every child the full set = the run's best."""
+    import torch
+    import paper_1901_07643_b200 as bn
+    X = datagen.config_data(4)
+    n, m = X.shape
+    h = bn.Bnreg.create(X)
+    F = h.num_families()
+    t = torch.empty((F, 2), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    best_m, best_b = h.run_pairs(t)
+    bs = torch.empty(F, dtype=torch.float64, device="cuda")
+    bmk = torch.empty(F, dtype=torch.int32, device="cuda")
+    h.best_subsets(t.data_ptr() + 8, 2, bs, bmk)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(24)
+    for v in range(m):
+        i = oracle.index(m, v, ((1 << m) - 1) & ~(1 << v))
+        assert _gather(bmk, [i]).view(np.uint32)[0] == best_m[v] and _gather(bs, [i])[0] == best_b[v]
+    for _ in range(300):
+        v = int(rng.integers(0, m))
+        others = [u for u in range(m) if u != v]
+        C = [others[j] for j in rng.choice(m - 1, size=int(rng.integers(0, 10)), replace=False)]
+        subs = [sum(1 << C[q] for q in range(len(C)) if (s >> q) & 1) for s in range(1 << len(C))]
+        idx = [oracle.index(m, v, S) for S in subs]
+        scs = _gather(t[:, 1], idx)
+        bsc, bS = None, None
+        for sc, S in zip(scs, subs):
+            if bsc is None or oracle._g14_better(sc, S, bsc, bS):
+                bsc, bS = sc, S
+        i = oracle.index(m, v, sum(1 << u for u in C))
+        assert _gather(bs, [i])[0] == bsc and _gather(bmk, [i]).view(np.uint32)[0] == bS
+    h.close()

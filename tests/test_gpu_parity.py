@@ -367,3 +367,60 @@ def test_coefficients_against_oracle():
                 scale = max(1.0, np.abs(ref).max())
                 assert np.abs(beta[v] - ref).max() <= tol * scale, (cfg, v)
         h.close()
+
+
+def _bps_run(cfg, layout):
+    import torch
+    bn = _bn()
+    X = datagen.config_data(cfg)
+    n, m = X.shape
+    h = bn.Bnreg.create(X)
+    F = h.num_families()
+    bs = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+    bmk = torch.zeros(F, dtype=torch.int32, device="cuda")
+    if layout == "pairs":
+        t = torch.empty((F, 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        best_m, best_b = h.run_pairs(t)
+        h.best_subsets(t.data_ptr() + 8, 2, bs, bmk)
+        sc = t[:, 1]
+    else:
+        sc = torch.empty(F, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        best_m, best_b = h.run(None, sc)
+        scores = sc.clone()
+        h.best_subsets(sc, 1, sc, bmk)                 # in place over the BIC table
+        sc, bs = scores, sc
+    torch.cuda.synchronize()
+    out = (sc.cpu().numpy(), bs.cpu().numpy(), bmk.cpu().numpy().view(np.uint32), best_m, best_b, m)
+    h.close()
+    return out
+
+
+@pytest.mark.parametrize("cfg,layout", [(1, "pairs"), (2, "pairs"), (2, "tables")])
+def test_best_subsets(cfg, layout):
+    """bnreg_best_subsets on the GPU's own score column, exactly:
+    cfg1 against the plain enumeration of every candidate set's subsets, cfg2 (15 mask
+    bits: the low tile and a high group) against the subset-max recursion of the
+    oracle, both layouts (the two-table one in place); the full candidate set gives the
+    run's per-child best."""
+    sc, bs, bmk, best_m, best_b, m = _bps_run(cfg, layout)
+    ref = oracle.best_subsets_brute(sc, m) if cfg == 1 else oracle.best_subsets(sc, m)
+    np.testing.assert_array_equal(bs, ref[0])
+    np.testing.assert_array_equal(bmk, ref[1])
+    for v in range(m):
+        i = oracle.index(m, v, ((1 << m) - 1) & ~(1 << v))
+        assert bmk[i] == best_m[v] and bs[i] == best_b[v]
+
+
+def test_best_subsets_errors():
+    import torch
+    bn = _bn()
+    h = bn.Bnreg.create(datagen.config_data(1))
+    t = torch.empty(h.num_families(), dtype=torch.float64, device="cuda")
+    k = torch.empty(h.num_families(), dtype=torch.int32, device="cuda")
+    with pytest.raises(bn.BnregError):
+        h.best_subsets(t, 0, t, k)
+    with pytest.raises(bn.BnregError):
+        h.best_subsets(t, 2, t, k)                     # aliasing needs stride 1
+    h.close()

@@ -345,3 +345,27 @@ def test_coefficients_exact_and_planted():
     Z[:, 2] = 1.5 * Z[:, 0] - 2.0 * Z[:, 1]
     bz = oracle.coefficients(oracle.centre(Z), 2, 0b11)
     np.testing.assert_allclose(bz, [1.5, -2.0, 0.0, 0.0], atol=1e-12)
+
+
+def test_best_subsets_golden_and_brute():
+    """best parent set within a candidate set.  On the golden m=3
+    table: B's best within {C} is the empty set (BIC(B|C) = -12.50 <
+    BIC(B|{}) = -11.89), A's within {B} is {B}, every child's within V-v is its overall
+    best; and the subset-max recursion equals the plain enumeration on random tables
+    (with ties: rounded scores) at m = 4..8."""
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "m3_table.json")))
+    m = 3
+    sc = np.array([e["bic"] for e in sorted(g["table"], key=lambda e: e["idx"])])
+    s, mk = oracle.best_subsets(sc, m)
+    B = 1
+    assert mk[oracle.index(m, B, 0b100)] == 0 and s[oracle.index(m, B, 0b100)] == pytest.approx(-11.886999196479)
+    assert mk[oracle.index(m, 0, 0b010)] == 0b010
+    for v in range(m):
+        assert mk[oracle.index(m, v, 0b111 & ~(1 << v))] == g["best"][str(v)]
+    rng = np.random.default_rng(5)
+    for m in range(4, 9):
+        t = np.round(rng.standard_normal(m << (m - 1)), 1)        # many exact ties: G14 decides
+        a = oracle.best_subsets(t, m)
+        b = oracle.best_subsets_brute(t, m)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
