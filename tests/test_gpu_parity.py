@@ -122,6 +122,17 @@ def test_small_random(m, k, seed):
     _check_full(X, bn.options(free_vars=k))
 
 
+@pytest.mark.parametrize("m,k", [(2, 2), (3, 2), (3, 3), (4, 2), (4, 3), (4, 4), (7, 2), (11, 8)])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_edge_shapes(m, k, pairs):
+    """Edge shapes: the smallest m (no pinned variable, one worker), k = m, k = 2 (the
+    shortest schedule), no gang or warp variables (G < 4, fewer than 8 workers per warp),
+    and the minimum n = m + 1, in both layouts."""
+    bn = _bn()
+    X = datagen.gaussian(m + 1, m, seed=40 + m * 10 + k, offset=-2.0)
+    _check_full(X, bn.options(free_vars=k), pairs=pairs)
+
+
 def test_cfg2_full_o1():
     X = datagen.config_data(2)
     _check_full(X)
