@@ -41,7 +41,6 @@
 namespace bnr {
 
 constexpr int kW = 8;          // lockstep workers per warp
-constexpr int kPP = 4;         // lanes (parts) per worker
 constexpr int kCS = kW * 16;   // bytes between free slots of the shared state
 
 // ---------------------------------------------------------------- tensor memory
