@@ -52,12 +52,14 @@ __global__ void __launch_bounds__(256) bps_low_kernel(const double* __restrict__
     __syncthreads();
     for (int b = 0; b < T; ++b) {
         const int bit = 1 << b;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            if (!(i & bit)) continue;
+        for (int q = threadIdx.x; q < n / 2; q += blockDim.x) {
+            const int i = ((q >> b) << (b + 1)) | (q & (bit - 1)) | bit;   // the q-th index with bit b set
             const int j = i ^ bit;
-            if (bps_better(s[j], c[j], s[i], c[i])) {
-                s[i] = s[j];
-                c[i] = c[j];
+            const double sj = s[j];
+            const uint32_t cj = c[j];
+            if (bps_better(sj, cj, s[i], c[i])) {
+                s[i] = sj;
+                c[i] = cj;
             }
         }
         __syncthreads();
@@ -93,13 +95,15 @@ __global__ void __launch_bounds__(256) bps_group_kernel(int m, int b0, int G, do
     }
     __syncthreads();
     for (int b = 0; b < G; ++b) {
-        const int bit = 32 << b;                             // group bit b within the tile index
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            if (!(i & bit)) continue;
+        const int tb = 5 + b, bit = 1 << tb;                 // group bit b within the tile index
+        for (int q = threadIdx.x; q < n / 2; q += blockDim.x) {
+            const int i = ((q >> tb) << (tb + 1)) | (q & (bit - 1)) | bit;
             const int j = i ^ bit;
-            if (bps_better(s[j], c[j], s[i], c[i])) {
-                s[i] = s[j];
-                c[i] = c[j];
+            const double sj = s[j];
+            const uint32_t cj = c[j];
+            if (bps_better(sj, cj, s[i], c[i])) {
+                s[i] = sj;
+                c[i] = cj;
             }
         }
         __syncthreads();
