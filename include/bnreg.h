@@ -120,6 +120,15 @@ bnreg_status bnreg_run_pairs_async(bnreg_t* h, double* out_pairs, uint32_t* best
 enum { BNREG_SCORE_BIC = 0, BNREG_SCORE_AIC = 1, BNREG_SCORE_LOGLIK = 2 };
 bnreg_status bnreg_set_score(bnreg_t* h, int32_t score);
 
+/* How bnreg_load factors the centred data:
+ * BNREG_ROOT_TSQR (default): Householder QR of 256-row tiles and a merge tree.
+ * BNREG_ROOT_CHOLESKY: R = chol(X~^T X~), the paper's covariance alternative
+ * (PAPER.md:31): faster, but the Gram matrix squares the condition number, so
+ * ill-conditioned data (cfg3's near-collinear pair) loses accuracy -- a
+ * comparison path.  Applies to later loads; BNREG_E_INVAL for another value. */
+enum { BNREG_ROOT_TSQR = 0, BNREG_ROOT_CHOLESKY = 1 };
+bnreg_status bnreg_set_root_method(bnreg_t* h, int32_t method);
+
 /* Best parent set within every candidate set (the step after
  * the score table in exact structure search): for every child v and
  * candidate set C (entry i = bnreg_index(m, v, C)), best_score[i] = the maximum over

@@ -20,12 +20,13 @@ LIB_PATH = os.path.join(_HERE, "libbnreg.so")
 
 OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE = range(7)
 SCORE_BIC, SCORE_AIC, SCORE_LOGLIK = 0, 1, 2
+ROOT_TSQR, ROOT_CHOLESKY = 0, 1
 _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNREG_E_NOMEM",
           5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
-           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_best_subsets",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_best_subsets", "bnreg_set_root_method",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
@@ -76,6 +77,7 @@ def lib():
         "bnreg_set_score": ([H, i32], i32),
         "bnreg_coefficients": ([H, P, P], i32),
         "bnreg_best_subsets": ([H, P, i64, P, P], i32),
+        "bnreg_set_root_method": ([H, i32], i32),
         "bnreg_run_pairs_async": ([H, P, P, P], i32),
         "bnreg_all_rss": ([H, P], i32),
         "bnreg_bic": ([H, P], i32),
@@ -217,6 +219,10 @@ class Bnreg:
         _check(lib().bnreg_run(self._h, _dptr(out_rss), _dptr(out_bic),
                                _hptr(bm) if best else None, _hptr(bb) if best else None))
         return bm, bb
+
+    def set_root_method(self, method: int):
+        """bnreg_set_root_method: ROOT_TSQR (default) or ROOT_CHOLESKY (Gram + Cholesky) for later loads."""
+        _check(lib().bnreg_set_root_method(self._h, method))
 
     def best_subsets(self, scores, stride: int, best_score, best_mask):
         """bnreg_best_subsets: for every (child, candidate set) the best score over the set's

@@ -93,6 +93,8 @@ struct bnreg {
     int nparts = 0;                // rows of d_part_bic / d_part_mask
     unsigned* d_counters = nullptr;
     int score = 0;                     // BNREG_SCORE_*
+    int root_method = 0;               // BNREG_ROOT_*
+    double* d_gram = nullptr;          // Gram scratch (BNREG_ROOT_CHOLESKY)
     bool ran = false;                  // a run wrote d_best_mask
     double* d_coef = nullptr;          // bnreg_coefficients output (m*m)
     uint32_t* d_cmask = nullptr;       // bnreg_coefficients input masks
@@ -118,7 +120,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask};
+                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -352,7 +354,12 @@ bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
     }
     CK(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
     CK(launch_centre(src, P.n, P.m, h->d_order, h->dXr, h->d_status, h->stream));
-    CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
+    if (h->root_method == 1) {
+        if (!h->d_gram) CK(cudaMalloc(&h->d_gram, (size_t)P.m * P.m * sizeof(double)));
+        CK(launch_gram_chol(h->dXr, P.n, P.m, h->d_gram, h->d_root, h->d_status, h->stream));
+    } else {
+        CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
+    }
     int status = 0;
     CK(cudaMemcpyAsync(&status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(stream_wait(h->stream));
@@ -604,6 +611,14 @@ bnreg_status bnreg_run_async(bnreg_t* h, double* out_rss, double* out_bic, uint3
     bnreg_status s = run_impl(h, out_rss, out_bic, bm_dev, bb_dev);
     if (s != BNREG_OK) return s;
     if (h->timing) return collect_timing(h);   // timing needs the events: synchronises
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_set_root_method(bnreg_t* h, int32_t method)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (method != 0 && method != 1) return fail(BNREG_E_INVAL, "method must be BNREG_ROOT_TSQR or BNREG_ROOT_CHOLESKY");
+    h->root_method = method;
     return BNREG_OK;
 }
 

@@ -391,4 +391,73 @@ cudaError_t launch_coefficients(const double* R, const int* order, int m, const 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- a2 alternative: Gram + Cholesky
+// SURVEY §8(f) NEXT 2, the paper's covariance alternative (it "comes at
+// cost of numerical accuracy"): R = chol(X~^T X~) instead of the TSQR.  Same R up to
+// rounding in exact arithmetic, but the Gram matrix squares the condition number.
+// gram_kernel: one CTA per (i <= j) column pair, G[i][j] = sum_r X~[r][i] X~[r][j].
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xr, int64_t n, int m,
+                                                   double* __restrict__ G)
+{
+    __shared__ double red[8];
+    int p = blockIdx.x, i = 0;
+    while (p >= m - i) { p -= m - i; ++i; }
+    const int j = i + p;
+    const double* a = Xr + (int64_t)i * n;
+    const double* b = Xr + (int64_t)j * n;
+    double s = 0.0;
+    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) s = fma(a[r], b[r], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];   // fixed order
+        G[(size_t)i * m + j] = t;
+        G[(size_t)j * m + i] = t;
+    }
+}
+
+// chol_kernel: one warp, upper Cholesky factor R (row-major, diag > 0) of G in place
+// into Rroot; rank check as the TSQR's (G26), a non-positive pivot is rank deficient.
+__global__ void __launch_bounds__(32) chol_kernel(const double* __restrict__ G, int m, double* __restrict__ R,
+                                                  int* status)
+{
+    __shared__ double A[32 * 33];
+    const int lane = threadIdx.x;
+    for (int r = 0; r < m; ++r)
+        if (lane < m) A[r * 33 + lane] = G[(size_t)r * m + lane];
+    __syncwarp();
+    bool bad = false;
+    double mx = 0.0;
+    for (int c = 0; c < m; ++c) mx = fmax(mx, sqrt(fabs(A[c * 33 + c])));
+    for (int k = 0; k < m; ++k) {
+        const double d = A[k * 33 + k];
+        bad |= !(d > 0.0);
+        const double rkk = d > 0.0 ? sqrt(d) : 0.0;
+        __syncwarp();
+        // row k of R: R[k][j] = A[k][j] / rkk for j > k; trailing update A[i][j] -= R[k][i] R[k][j]
+        if (lane > k && lane < m) A[k * 33 + lane] = rkk > 0.0 ? A[k * 33 + lane] / rkk : 0.0;
+        if (lane == k) A[k * 33 + k] = rkk;
+        __syncwarp();
+        if (lane > k && lane < m)
+            for (int i = k + 1; i <= lane; ++i) A[i * 33 + lane] = fma(-A[k * 33 + i], A[k * 33 + lane], A[i * 33 + lane]);
+        __syncwarp();
+        if (!(rkk > 1e-12 * mx)) bad = true;
+    }
+    if (lane < m)
+        for (int r = 0; r < m; ++r) R[(size_t)r * m + lane] = lane >= r ? A[r * 33 + lane] : 0.0;
+    if (lane == 0 && bad) atomicOr(status, 4);
+}
+
+cudaError_t launch_gram_chol(const double* Xr, int64_t n, int m, double* G, double* Rroot, int* status,
+                             cudaStream_t st)
+{
+    gram_kernel<<<m * (m + 1) / 2, 256, 0, st>>>(Xr, n, m, G);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    chol_kernel<<<1, 32, 0, st>>>(G, m, Rroot, status);
+    return cudaGetLastError();
+}
+
 }  // namespace bnr

@@ -68,6 +68,9 @@ cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_ord
                           double* Xr, int* status, cudaStream_t st);
 cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsigned* counters,
                         int nleaf2, int rb, double* Rroot, int* status, cudaStream_t st);
+// a2 alternative: root R by Cholesky of the Gram matrix (G: m*m scratch)
+cudaError_t launch_gram_chol(const double* Xr, int64_t n, int m, double* G, double* Rroot, int* status,
+                             cudaStream_t st);
 cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
                               cudaStream_t st);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,

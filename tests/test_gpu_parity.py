@@ -435,3 +435,60 @@ def test_best_subsets_errors():
     with pytest.raises(bn.BnregError):
         h.best_subsets(t, 2, t, k)                     # aliasing needs stride 1
     h.close()
+
+
+def test_cholesky_root_comparison():
+    """SURVEY §8(f) NEXT 2, the paper's covariance alternative (it "comes at
+    cost of numerical accuracy"): the root R by Cholesky of the Gram matrix.  On the
+    well-conditioned cfg1 and cfg2 it meets the same parity bar as the QR root; on cfg3
+    (near-collinear pair, kappa(X) ~ 5e7, kappa(G) ~ 1e15) the families that contain both
+    members of the pair lose accuracy by orders of magnitude while the QR root does not."""
+    from gpu_util import run_tables
+    bn = _bn()
+    for cfg in (1, 2):
+        X = datagen.config_data(cfg)
+        Xc = oracle.centre(X)
+        h = bn.Bnreg(*X.shape)
+        h.set_root_method(bn.ROOT_CHOLESKY)
+        h.load(X)
+        import torch
+        t = torch.empty((h.num_families(), 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        h.run_pairs(t)
+        torch.cuda.synchronize()
+        rss = t[:, 0].cpu().numpy()
+        ref, _ = oracle.table(Xc, want_bic=False)
+        assert (np.abs(rss - ref) / ref).max() <= RSS_RTOL
+        with pytest.raises(bn.BnregError):
+            h.set_root_method(2)
+        h.close()
+    meta = {}
+    X = datagen.config_data(3, meta=meta)
+    Xc = oracle.centre(X)
+    n, m = X.shape
+    i, j = meta["pair"]
+    rng = np.random.default_rng(9)
+    idx = []
+    for _ in range(200):
+        v = int(rng.integers(0, m))
+        if v in (i, j):
+            continue
+        S = (int(rng.integers(0, 1 << m)) | (1 << i) | (1 << j)) & ~(1 << v)
+        idx.append(oracle.index(m, v, S))
+    idx = np.array(sorted(set(idx)), dtype=np.int64)
+    ref = oracle.rss_indices(Xc, idx)
+    errs = {}
+    for method in (bn.ROOT_TSQR, bn.ROOT_CHOLESKY):
+        import torch
+        h = bn.Bnreg(n, m)
+        h.set_root_method(method)
+        h.load(X)
+        t = torch.empty((h.num_families(), 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        h.run_pairs(t)
+        torch.cuda.synchronize()
+        got = t[torch.from_numpy(idx).cuda(), 0].cpu().numpy()
+        errs[method] = (np.abs(got - ref) / ref).max()
+        h.close()
+    assert errs[bn.ROOT_TSQR] <= RSS_RTOL
+    assert errs[bn.ROOT_CHOLESKY] >= 1e3 * max(errs[bn.ROOT_TSQR], 1e-15), errs
