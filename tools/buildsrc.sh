@@ -1,4 +1,5 @@
 # build libbnreg.so from an alternative csrc directory: tools/buildsrc.sh NAME SRCDIR [-D...]
 name=$1; S=$2; shift 2
+SRCS=$(python -c "import sys; sys.path.insert(0, 'paper_1901_07643_b200'); import build; print(' '.join('$S/' + s for s in build.SOURCES))")
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -shared "$@" \
-  -I paper_1901_07643_b200/csrc -o tmpvar/lib$name.so $S/bnreg_api.cu $S/bnreg_kernels.cu $S/walk_kernel.cu $S/seed_kernel.cu 2>&1 | grep -i "error" || true
+  -I paper_1901_07643_b200/csrc -o tmpvar/lib$name.so $SRCS 2>&1 | grep -i "error" || true
