@@ -10,8 +10,8 @@
 // the c with bit b set.  HBM-bound: the bits are processed in groups inside
 // shared-memory tiles, one read and one write of the (score, mask) table per group:
 //   * low group (bits 0..T-1, T <= 12): a tile = 2^T consecutive entries;
-//   * higher groups of <= 8 bits: a tile = 32 consecutive entries (bits 0..4, one
-//     coalesced 256 B row of scores) x the 2^G combinations of the group's bits.
+//   * higher groups of <= 8 bits: a tile = 2^LO consecutive entries (coalesced rows,
+//     LO >= 5 and LO + G >= 12 where the bits allow) x the 2^G settings of the group.
 // The last pass writes user-id masks (bit v inserted).
 #include <cstdint>
 #include <algorithm>
@@ -33,7 +33,7 @@ __device__ __forceinline__ uint32_t user_mask(uint32_t c, int v)
 }
 
 // bits 0..T-1: one CTA per (child, tile of 2^T consecutive entries)
-__global__ void __launch_bounds__(256) bps_low_kernel(const double* __restrict__ sc_in, int64_t stride, int m, int T,
+__global__ void __launch_bounds__(512) bps_low_kernel(const double* __restrict__ sc_in, int64_t stride, int m, int T,
                                                       double* __restrict__ out_s, uint32_t* __restrict__ out_m,
                                                       int final_pass)
 {
@@ -70,32 +70,32 @@ __global__ void __launch_bounds__(256) bps_low_kernel(const double* __restrict__
     }
 }
 
-// bits b0..b0+G-1 (b0 >= 5): one CTA per (child, setting of the other bits above bit 4);
-// tile = 32 consecutive entries x 2^G group combinations
-__global__ void __launch_bounds__(256) bps_group_kernel(int m, int b0, int G, double* __restrict__ s_io,
+// bits b0..b0+G-1: one CTA per (child, setting of the bits outside the tile); tile =
+// 2^LO consecutive entries (bits 0..LO-1, LO <= b0, coalesced rows) x the 2^G settings
+// of the group's bits
+__global__ void __launch_bounds__(512) bps_group_kernel(int m, int b0, int G, int LO, double* __restrict__ s_io,
                                                         uint32_t* __restrict__ m_io, int final_pass)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int ng = 1 << G, n = 32 * ng;
+    const int n = 1 << (LO + G);
     double* const s = (double*)smem;
     uint32_t* const c = (uint32_t*)(smem + (size_t)n * 8);
     const int nb = m - 1;                                    // compressed index bits
-    const int rest_bits = nb - 5 - G;                        // bits 5..b0-1 and b0+G..nb-1
+    const int rest_bits = nb - LO - G;                       // bits LO..b0-1 and b0+G..nb-1
     const int v = blockIdx.x >> rest_bits;
     const uint32_t r = blockIdx.x & ((1u << rest_bits) - 1u);
-    // spread the rest index over bits 5..b0-1 (low part) and b0+G.. (high part)
-    const int lowr = b0 - 5;
-    const uint32_t fixed = ((r & ((1u << lowr) - 1u)) << 5) | ((r >> lowr) << (b0 + G));
+    const int lowr = b0 - LO;
+    const uint32_t fixed = ((r & ((1u << lowr) - 1u)) << LO) | ((r >> lowr) << (b0 + G));
+    const uint32_t lom = (1u << LO) - 1u;
     const int64_t row = (int64_t)v << nb;
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int g = e >> 5, lo = e & 31;
-        const uint32_t idx = fixed | ((uint32_t)g << b0) | (uint32_t)lo;
+        const uint32_t idx = fixed | ((uint32_t)(e >> LO) << b0) | ((uint32_t)e & lom);
         s[e] = s_io[row + idx];
         c[e] = m_io[row + idx];
     }
     __syncthreads();
     for (int b = 0; b < G; ++b) {
-        const int tb = 5 + b, bit = 1 << tb;                 // group bit b within the tile index
+        const int tb = LO + b, bit = 1 << tb;                // group bit b within the tile index
         for (int q = threadIdx.x; q < n / 2; q += blockDim.x) {
             const int i = ((q >> tb) << (tb + 1)) | (q & (bit - 1)) | bit;
             const int j = i ^ bit;
@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(256) bps_group_kernel(int m, int b0, int G, do
         __syncthreads();
     }
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int g = e >> 5, lo = e & 31;
-        const uint32_t idx = fixed | ((uint32_t)g << b0) | (uint32_t)lo;
+        const uint32_t idx = fixed | ((uint32_t)(e >> LO) << b0) | ((uint32_t)e & lom);
         s_io[row + idx] = s[e];
         m_io[row + idx] = final_pass ? user_mask(c[e], v) : c[e];
     }
@@ -127,18 +126,19 @@ cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_
         cudaError_t e = cudaFuncSetAttribute(bps_low_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const int grid = m << (nb - T);
-        bps_low_kernel<<<grid, 256, smem, st>>>(scores, stride, m, T, out_s, out_m, low_final ? 1 : 0);
+        bps_low_kernel<<<grid, 512, smem, st>>>(scores, stride, m, T, out_s, out_m, low_final ? 1 : 0);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     for (int b0 = T; b0 < nb;) {
         const int G = std::min(8, nb - b0);
+        const int LO = std::min(b0, std::max(5, 12 - G));    // tiles of >= 4096 entries (96 KB at G = 8)
         const bool last = b0 + G == nb;
-        const size_t smem = (size_t)32 * ((size_t)1 << G) * 12;
+        const size_t smem = ((size_t)1 << (LO + G)) * 12;
         cudaError_t e = cudaFuncSetAttribute(bps_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        const int grid = m << (nb - 5 - G);
-        bps_group_kernel<<<grid, 256, smem, st>>>(m, b0, G, out_s, out_m, last ? 1 : 0);
+        const int grid = m << (nb - LO - G);
+        bps_group_kernel<<<grid, 512, smem, st>>>(m, b0, G, LO, out_s, out_m, last ? 1 : 0);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         b0 += G;
