@@ -95,8 +95,11 @@ __device__ void householder_tile(double* T, int nr, int m, double* sh)
     }
 }
 
-// rbuf: heap-ordered binary tree of R's (slot 1 = root, leaves at nleaf2 + b),
-// each m*m row-major.  counters: nleaf2 zeroed arrival counters (self-resetting).
+// rbuf: the merge tree's R's level by level (leaves first, then ceil(c / F) nodes per
+// level up to the root), each m*m row-major.  counters: one zeroed arrival counter per
+// internal node (self-resetting).  A merge of F children is one Householder QR of
+// their stacked R's (F m x m): fewer sequential levels than a binary tree.
+constexpr int kTsqrFanIn = 8;
 __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr, int64_t n, int m, int rb,
                                                    double* rbuf, unsigned* counters, int nleaf2,
                                                    double* Rroot, int* status)
@@ -115,33 +118,42 @@ __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr
             T[(int64_t)c * nrp + i] = (i < nr) ? Xr[(int64_t)c * n + r0 + i] : 0.0;
     __syncthreads();
     householder_tile(T, nrp, m, sh);
-    int node = nleaf2 + b;
-    double* dst = rbuf + (int64_t)node * m * m;
+    // the merge tree: level 0 = the nl leaves, level l+1 has ceil(c_l / F) nodes; the
+    // last of a node's (up to F) children to arrive stacks their R's and re-factors
+    constexpr int F = kTsqrFanIn;
+    const int nl = (int)((n + rb - 1) / rb);
+    int c_l = nl, off = 0, idx = b;              // this level's size, its first node, our node
+    double* dst = rbuf + (int64_t)(off + idx) * m * m;
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
         int i = e / m, c = e % m;
         dst[e] = (c >= i) ? T[(int64_t)c * nrp + i] : 0.0;
     }
-    while (node > 1) {
+    while (c_l > 1) {
         __threadfence();
         __syncthreads();
-        int parent = node >> 1;
-        if (threadIdx.x == 0) s_old = (int)atomicAdd(&counters[parent], 1u);
+        const int parent = idx / F;
+        const int nch = min(F, c_l - F * parent);
+        const int c_next = (c_l + F - 1) / F;
+        const int poff = off + c_l;              // the next level's first node
+        if (threadIdx.x == 0) s_old = (int)atomicAdd(&counters[poff - nl + parent], 1u);
         __syncthreads();
-        if (s_old == 0) return;                   // first arriver: sibling will merge
-        if (threadIdx.x == 0) counters[parent] = 0u;   // reset for the next launch
-        // second arriver: stack [R_left; R_right] (2m x m) and re-factor
-        const double* Lr = rbuf + (int64_t)(2 * parent) * m * m;
-        const double* Rr = rbuf + (int64_t)(2 * parent + 1) * m * m;
-        int nr2 = 2 * m;
-        for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-            int i = e / m, c = e % m;
-            T[(int64_t)c * nr2 + i] = __ldcg(Lr + e);
-            T[(int64_t)c * nr2 + m + i] = __ldcg(Rr + e);
+        if (s_old < nch - 1) return;             // not the last child: the last one merges
+        if (threadIdx.x == 0) counters[poff - nl + parent] = 0u;   // reset for the next launch
+        // last arriver: stack the children's R's (nch * m x m) and re-factor
+        const int nr2 = nch * m;
+        for (int q = 0; q < nch; ++q) {
+            const double* Rq = rbuf + (int64_t)(off + F * parent + q) * m * m;
+            for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+                int i = e / m, c = e % m;
+                T[(int64_t)c * nr2 + q * m + i] = __ldcg(Rq + e);
+            }
         }
         __syncthreads();
         householder_tile(T, nr2, m, sh);
-        node = parent;
-        dst = rbuf + (int64_t)node * m * m;
+        off = poff;
+        idx = parent;
+        c_l = c_next;
+        dst = rbuf + (int64_t)(off + idx) * m * m;
         for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
             int i = e / m, c = e % m;
             dst[e] = (c >= i) ? T[(int64_t)c * nr2 + i] : 0.0;
@@ -150,7 +162,7 @@ __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr
     }
     // root: sign-normalise rows (diag > 0), rank check (G26)
     __syncthreads();
-    const double* R = rbuf + (int64_t)1 * m * m;
+    const double* R = dst;
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
         int i = e / m, c = e % m;
         double d = __ldcg(R + i * m + i);
@@ -296,12 +308,14 @@ cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_ord
 cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsigned* counters, int nleaf2, int rb,
                         double* Rroot, int* status, cudaStream_t st)
 {
-    int rows = rb > 2 * m ? rb : 2 * m;
+    int rows = rb > kTsqrFanIn * m ? rb : kTsqrFanIn * m;
     if (rows < m) rows = m;
     size_t smem = (size_t)rows * m * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(tsqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tsqr_kernel<<<nleaf2, 256, smem, st>>>(Xr, n, m, rb, rbuf, counters, nleaf2, Rroot, status);
+    const int nl = (int)((n + rb - 1) / rb);
+    (void)nleaf2;
+    tsqr_kernel<<<nl, 256, smem, st>>>(Xr, n, m, rb, rbuf, counters, nleaf2, Rroot, status);
     return cudaGetLastError();
 }
 
