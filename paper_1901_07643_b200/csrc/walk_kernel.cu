@@ -15,8 +15,10 @@
 //     list entry f to part (NB + f) % 4.
 //   * the W workers differ in the W lowest user ids (the "warp variables"), the
 //     CTA's 4 warps in the next 2 ids (the "gang variables"): for every child
-//     and step a CTA writes 32 adjacent entries = 256 B of each table at the same
-//     time (DRAM write combining: profiles/r01_storebench.txt)
+//     and step a CTA's 32 workers own 32 adjacent entries -- 512 B of (RSS, BIC)
+//     records, or 256 B of each separate table; a gang barrier before the harvest
+//     (every step for the tables, every 16th for the records) keeps the warps'
+//     parts of a region close in time (DRAM write combining: tools/gangstore.cu)
 //   * walk state E(l, slot) = (R_l, U_{l+1}) of the k free rows l of a column,
 //     U_l = sum_{r >= l} R_r^2 (+ the rows below the free block); suffix sums
 //     are updated by addition only.  Back slots are statically
