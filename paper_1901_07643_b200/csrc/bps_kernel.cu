@@ -115,30 +115,218 @@ __global__ void __launch_bounds__(512) bps_group_kernel(int m, int b0, int G, in
     }
 }
 
+// ---- register-tiled passes (nb >= 12): each thread keeps 16 entries in registers ----
+// A tile's index bits are split three ways in each of two phases: lane bits (5, the
+// coalesced ones), register bits (4: the entries one thread holds) and warp bits.
+// Register bits are transformed in registers, lane bits (low kernel only) by warp
+// shuffles; between the phases the tile goes through shared memory once so that the
+// remaining bits become register bits.  Shared-memory traffic: one write and one read
+// of (score, mask) per entry, one barrier per tile.
+constexpr int kRegE = 16;
+
+struct Ent {
+    double s[kRegE];
+    uint32_t c[kRegE];
+};
+
+// bit j of the register index, for the first `active` register bits
+__device__ __forceinline__ void reg_pass(Ent& e, int active)
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (j >= active) break;
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            if (!((r >> j) & 1)) continue;
+            const int q = r ^ (1 << j);
+            if (bps_better(e.s[q], e.c[q], e.s[r], e.c[r])) {
+                e.s[r] = e.s[q];
+                e.c[r] = e.c[q];
+            }
+        }
+    }
+}
+
+// bits 0..4 of the lane index
+__device__ __forceinline__ void lane_pass(Ent& e)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const bool upper = (lane >> b) & 1;
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const double so = __shfl_xor_sync(0xffffffffu, e.s[r], 1 << b);
+            const uint32_t co = __shfl_xor_sync(0xffffffffu, e.c[r], 1 << b);
+            if (upper && bps_better(so, co, e.s[r], e.c[r])) {
+                e.s[r] = so;
+                e.c[r] = co;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t scatter4(int r, int p0, int p1, int p2, int p3)
+{
+    return ((uint32_t)(r & 1) << p0) | ((uint32_t)((r >> 1) & 1) << p1) | ((uint32_t)((r >> 2) & 1) << p2) |
+           ((uint32_t)((r >> 3) & 1) << p3);
+}
+
+// bits 0..11 of the compressed index: tile = 4096 consecutive entries, 256 threads.
+// phase A: lane = bits 0..4, registers = bits 5..8, warps = bits 9..11;
+// phase B: lane = bits 0..4, registers = bits 9,10,11 (+5, inactive), warps = bits 6..8.
+__global__ void __launch_bounds__(256) bps_low_reg_kernel(const double* __restrict__ sc_in, int64_t stride, int m,
+                                                          double* __restrict__ out_s, uint32_t* __restrict__ out_m,
+                                                          int final_pass)
+{
+    __shared__ double ts[4096];
+    __shared__ uint32_t tc[4096];
+    const int nb = m - 1;
+    const int tiles = 1 << (nb - 12);
+    const int v = blockIdx.x / tiles;
+    const uint32_t base = (uint32_t)(blockIdx.x % tiles) << 12;
+    const int64_t row = (int64_t)v << nb;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Ent e;
+    {
+        const uint32_t tb = (uint32_t)lane | ((uint32_t)warp << 9);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | ((uint32_t)r << 5);
+            e.s[r] = __ldcs(sc_in + (row + base + t) * stride);
+            e.c[r] = base + t;
+        }
+        reg_pass(e, 4);
+        lane_pass(e);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | ((uint32_t)r << 5);
+            ts[t] = e.s[r];
+            tc[t] = e.c[r];
+        }
+    }
+    __syncthreads();
+    {
+        const uint32_t tb = (uint32_t)lane | ((uint32_t)warp << 6);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | scatter4(r, 9, 10, 11, 5);
+            e.s[r] = ts[t];
+            e.c[r] = tc[t];
+        }
+        reg_pass(e, 3);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | scatter4(r, 9, 10, 11, 5);
+            __stcs(out_s + row + base + t, e.s[r]);
+            __stcs(out_m + row + base + t, final_pass ? user_mask(e.c[r], v) : e.c[r]);
+        }
+    }
+}
+
+// group bits b0..b0+G-1, 4 <= G <= 8: tile = 2^LO consecutive entries x 2^G group
+// settings (LO + G = 12, or LO = 5 at G = 8), tile index t = (g << LO) | row bits,
+// 2^(LO+G-4) threads.  phase A: lane = row bits 0..4, registers = g bits 0..3,
+// warps = g bits 4..G-1 then row bits 5..LO-1; phase B: registers = g bits 4..G-1
+// (the active ones) then g bits 0..7-G, warps = g bits 8-G..3 then row bits 5..LO-1.
+__global__ void __launch_bounds__(512, 2) bps_group_reg_kernel(int m, int b0, int G, int LO, double* __restrict__ s_io,
+                                                            uint32_t* __restrict__ m_io, int final_pass)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = 1 << (LO + G);
+    double* const ts = (double*)smem;
+    uint32_t* const tc = (uint32_t*)(smem + (size_t)n * 8);
+    const int nb = m - 1;
+    const int rest_bits = nb - LO - G;
+    const int v = blockIdx.x >> rest_bits;
+    const uint32_t rr = blockIdx.x & ((1u << rest_bits) - 1u);
+    const int lowr = b0 - LO;
+    const uint32_t fixed = ((rr & ((1u << lowr) - 1u)) << LO) | ((rr >> lowr) << (b0 + G));
+    const int64_t row = (int64_t)v << nb;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = G - 4;                                     // group bits among the warp bits
+    const uint32_t wlo = warp & ((1u << gw) - 1u), whi = warp >> gw;
+    const uint32_t rowbits = lane | (whi << 5);
+    const int64_t gs = (int64_t)1 << b0;                      // index step of one group setting
+    Ent e;
+    // phase A: g = (wlo << 4) | r
+    {
+        const int64_t i0 = row + fixed + rowbits + ((int64_t)wlo << (b0 + 4));
+        const double* ps = s_io + i0;
+        const uint32_t* pm = m_io + i0;
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            e.s[r] = __ldcs(ps);
+            e.c[r] = __ldcs(pm);
+            ps += gs;
+            pm += gs;
+        }
+    }
+    reg_pass(e, 4);
+    {
+        const uint32_t tb = rowbits | (wlo << (LO + 4));
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            ts[tb | ((uint32_t)r << LO)] = e.s[r];
+            tc[tb | ((uint32_t)r << LO)] = e.c[r];
+        }
+    }
+    __syncthreads();
+    // phase B: register bit j < gw is g bit 4 + j, the others g bit j - gw:
+    // g = (wlo << (8 - G)) | (rl << 4) | rh
+    const uint32_t tb = rowbits | (wlo << (LO + 8 - G));
+#pragma unroll
+    for (int r = 0; r < kRegE; ++r) {
+        const uint32_t t = tb | (((uint32_t)r & ((1u << gw) - 1u)) << (LO + 4)) | (((uint32_t)r >> gw) << LO);
+        e.s[r] = ts[t];
+        e.c[r] = tc[t];
+    }
+    reg_pass(e, gw);
+    {
+        const int64_t i0 = row + fixed + rowbits + ((int64_t)wlo << (b0 + 8 - G));
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const int64_t i = i0 + ((int64_t)((((uint32_t)r & ((1u << gw) - 1u)) << 4) | ((uint32_t)r >> gw)) << b0);
+            __stcs(s_io + i, e.s[r]);
+            __stcs(m_io + i, final_pass ? user_mask(e.c[r], v) : e.c[r]);
+        }
+    }
+}
+
 cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_s, uint32_t* out_m, cudaStream_t st)
 {
     if (m < 2 || m > 30) return cudaErrorInvalidValue;
     const int nb = m - 1;
-    const int T = std::min(nb, 12);
-    const bool low_final = T == nb;
-    {
-        const size_t smem = ((size_t)1 << T) * 12;
-        cudaError_t e = cudaFuncSetAttribute(bps_low_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e;
+    if (nb < 12) {                                            // one tile per child: shared-memory passes
+        const size_t smem = ((size_t)1 << nb) * 12;
+        e = cudaFuncSetAttribute(bps_low_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        const int grid = m << (nb - T);
-        bps_low_kernel<<<grid, 512, smem, st>>>(scores, stride, m, T, out_s, out_m, low_final ? 1 : 0);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        bps_low_kernel<<<m, 512, smem, st>>>(scores, stride, m, nb, out_s, out_m, 1);
+        return cudaGetLastError();
     }
-    for (int b0 = T; b0 < nb;) {
-        const int G = std::min(8, nb - b0);
-        const int LO = std::min(b0, std::max(5, 12 - G));    // tiles of >= 4096 entries (96 KB at G = 8)
-        const bool last = b0 + G == nb;
-        const size_t smem = ((size_t)1 << (LO + G)) * 12;
-        cudaError_t e = cudaFuncSetAttribute(bps_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        const int grid = m << (nb - LO - G);
-        bps_group_kernel<<<grid, 512, smem, st>>>(m, b0, G, LO, out_s, out_m, last ? 1 : 0);
+    bps_low_reg_kernel<<<m << (nb - 12), 256, 0, st>>>(scores, stride, m, out_s, out_m, nb == 12 ? 1 : 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int R = nb - 12;                                    // high bits: groups of 4..8 (1..3: one small group)
+    const int ng = R == 0 ? 0 : (R < 4 ? 1 : (R + 7) / 8);
+    for (int g = 0, b0 = 12; g < ng; ++g) {
+        const int G = R / ng + (g < R % ng ? 1 : 0);
+        const bool last = g == ng - 1;
+        if (G < 4) {
+            const int LO = std::min(b0, 12 - G);
+            const size_t smem = ((size_t)1 << (LO + G)) * 12;
+            e = cudaFuncSetAttribute(bps_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            bps_group_kernel<<<m << (nb - LO - G), 512, smem, st>>>(m, b0, G, LO, out_s, out_m, last ? 1 : 0);
+        } else {
+            const int LO = G == 8 ? 5 : 12 - G;
+            const size_t smem = ((size_t)1 << (LO + G)) * 12;
+            e = cudaFuncSetAttribute(bps_group_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            bps_group_reg_kernel<<<m << (nb - LO - G), 1 << (LO + G - 4), smem, st>>>(m, b0, G, LO, out_s, out_m,
+                                                                                      last ? 1 : 0);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         b0 += G;

@@ -409,7 +409,7 @@ def _bps_run(cfg, layout):
     return out
 
 
-@pytest.mark.parametrize("cfg,layout", [(1, "pairs"), (2, "pairs"), (2, "tables")])
+@pytest.mark.parametrize("cfg,layout", [(1, "pairs"), (2, "pairs"), (2, "tables"), (3, "pairs")])
 def test_best_subsets(cfg, layout):
     """bnreg_best_subsets on the GPU's own score column, exactly:
     cfg1 against the plain enumeration of every candidate set's subsets, cfg2 (15 mask
@@ -423,6 +423,32 @@ def test_best_subsets(cfg, layout):
     for v in range(m):
         i = oracle.index(m, v, ((1 << m) - 1) & ~(1 << v))
         assert bmk[i] == best_m[v] and bs[i] == best_b[v]
+
+
+@pytest.mark.parametrize("m", [9, 13, 16, 17, 20, 21])
+def test_best_subsets_ties_pass_shapes(m):
+    """bnreg_best_subsets on a score table full of ties (4 distinct values), so that the
+    G14 tie-break (smaller |S|, then smaller mask) decides most entries, at every pass
+    shape launch_bps uses: one shared-memory tile (m = 9), the register-tiled low pass
+    alone (13) or followed by a small group (16: 3 bits) or by one register-tiled group
+    of 4 / 7 / 8 bits (17, 20, 21; two groups: cfg4 in test_gpu_fullsize), exactly
+    against the oracle's recursion (the scores are an input: any table is a valid one)."""
+    import torch
+    bn = _bn()
+    h = bn.Bnreg.create(datagen.gaussian(4 * m, m, seed=m))
+    F = h.num_families()
+    rng = np.random.default_rng(100 + m)
+    sc = rng.integers(0, 4, F).astype(np.float64) - 1.5
+    sd = torch.from_numpy(sc).cuda()
+    bs = torch.full((F,), float("nan"), dtype=torch.float64, device="cuda")
+    bmk = torch.zeros(F, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    h.best_subsets(sd, 1, bs, bmk)
+    torch.cuda.synchronize()
+    h.close()
+    ref = oracle.best_subsets(sc, m)
+    np.testing.assert_array_equal(bs.cpu().numpy(), ref[0])
+    np.testing.assert_array_equal(bmk.cpu().numpy().view(np.uint32), ref[1])
 
 
 def test_best_subsets_errors():

@@ -21,6 +21,7 @@ for _ in range(3):
 e1.record(s); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
 nb = m - 1
-passes = 1 + (max(0, nb - 12) + 7) // 8
+R = max(0, nb - 12)
+passes = 1 + (0 if R == 0 else (1 if R < 4 else (R + 7) // 8))
 byts = F * 16 + F * 12 + (passes - 1) * F * 24      # low: read records, write (score, mask); groups: r+w
 print(f"cfg{cfg} m={m}: best_subsets {ms:.2f} ms, {passes} passes, {byts / 1e9:.0f} GB moved, {byts / ms / 1e6:.0f} GB/s")
