@@ -7,12 +7,12 @@
 // It is a subset-max transform over the m - 1 bits of the compressed index
 // (compression keeps the order and the popcount of the masks, so G14 can compare
 // compressed indices): for every bit b, bps[c] = better(bps[c], bps[c ^ 2^b]) for
-// the c with bit b set.  HBM-bound: the bits are processed in groups inside
-// shared-memory tiles, one read and one write of the (score, mask) table per group:
-//   * low group (bits 0..T-1, T <= 12): a tile = 2^T consecutive entries;
-//   * higher groups of <= 8 bits: a tile = 2^LO consecutive entries (coalesced rows,
-//     LO >= 5 and LO + G >= 12 where the bits allow) x the 2^G settings of the group.
-// The last pass writes user-id masks (bit v inserted).
+// the c with bit b set.  HBM-bound: the bits are processed in passes, one read and one
+// write of the (score, mask) table per pass, the user-id masks written by the last:
+//   * m - 1 >= 12: the low 12 bits, then balanced groups of 4..8 bits, in
+//     register-tiled tiles of 4096 entries (16 per thread, see below);
+//   * small cases (m <= 12, a leftover group of 1..3 bits): shared-memory tiles, one
+//     barrier per bit.
 #include <cstdint>
 #include <algorithm>
 #include "kernels.h"
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(512) bps_group_kernel(int m, int b0, int G, in
 }
 
 // ---- register-tiled passes (nb >= 12): each thread keeps 16 entries in registers ----
-// A tile's index bits are split three ways in each of two phases: lane bits (5, the
-// coalesced ones), register bits (4: the entries one thread holds) and warp bits.
-// Register bits are transformed in registers, lane bits (low kernel only) by warp
-// shuffles; between the phases the tile goes through shared memory once so that the
-// remaining bits become register bits.  Shared-memory traffic: one write and one read
-// of (score, mask) per entry, one barrier per tile.
+// A tile's index bits are split three ways in each phase: lane bits (5; coalesced in
+// the phases that touch HBM), register bits (4: the entries one thread holds) and
+// warp bits.  Only register bits are transformed, in registers; between the phases the
+// tile goes through shared memory so that the remaining bits become register bits
+// (group tiles: 2 phases, one exchange; the 12-bit low tile: 3 phases, two exchanges,
+// swizzled so that no phase's accesses conflict).  No shuffles.
 constexpr int kRegE = 16;
 
 struct Ent {
@@ -147,35 +147,24 @@ __device__ __forceinline__ void reg_pass(Ent& e, int active)
     }
 }
 
-// bits 0..4 of the lane index
-__device__ __forceinline__ void lane_pass(Ent& e)
-{
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int b = 0; b < 5; ++b) {
-        const bool upper = (lane >> b) & 1;
-#pragma unroll
-        for (int r = 0; r < kRegE; ++r) {
-            const double so = __shfl_xor_sync(0xffffffffu, e.s[r], 1 << b);
-            const uint32_t co = __shfl_xor_sync(0xffffffffu, e.c[r], 1 << b);
-            if (upper && bps_better(so, co, e.s[r], e.c[r])) {
-                e.s[r] = so;
-                e.c[r] = co;
-            }
-        }
-    }
-}
-
 __device__ __forceinline__ uint32_t scatter4(int r, int p0, int p1, int p2, int p3)
 {
     return ((uint32_t)(r & 1) << p0) | ((uint32_t)((r >> 1) & 1) << p1) | ((uint32_t)((r >> 2) & 1) << p2) |
            ((uint32_t)((r >> 3) & 1) << p3);
 }
 
-// bits 0..11 of the compressed index: tile = 4096 consecutive entries, 256 threads.
-// phase A: lane = bits 0..4, registers = bits 5..8, warps = bits 9..11;
-// phase B: lane = bits 0..4, registers = bits 9,10,11 (+5, inactive), warps = bits 6..8.
-__global__ void __launch_bounds__(256) bps_low_reg_kernel(const double* __restrict__ sc_in, int64_t stride, int m,
+// shared-memory swizzles of the low tile (bijections on 0..4095): scores (8 B) XOR
+// bits 0..3 with bits 4..7, masks (4 B) bits 0..4 with bits 4..8, so that a warp whose
+// lanes run over bits 0..4 or over bits 4..8 hits distinct banks
+__device__ __forceinline__ uint32_t swz_s(uint32_t t) { return t ^ ((t >> 4) & 15u); }
+__device__ __forceinline__ uint32_t swz_c(uint32_t t) { return t ^ ((t >> 4) & 31u); }
+
+// bits 0..11 of the compressed index: tile = 4096 consecutive entries, 256 threads,
+// three register phases with two shared-memory exchanges (swizzled):
+// phase A: lane = bits 0..4 (coalesced loads), registers = bits 5..8, warps = bits 9..11;
+// phase B: registers = bits 0..3, lane = bits 4..8, warps = bits 9..11;
+// phase C: registers = bits 9, 10, 11, 4, lane = bits 0..3 and 8, warps = bits 5..7.
+__global__ void __launch_bounds__(256, 4) bps_low_reg_kernel(const double* __restrict__ sc_in, int64_t stride, int m,
                                                           double* __restrict__ out_s, uint32_t* __restrict__ out_m,
                                                           int final_pass)
 {
@@ -197,39 +186,56 @@ __global__ void __launch_bounds__(256) bps_low_reg_kernel(const double* __restri
             e.c[r] = base + t;
         }
         reg_pass(e, 4);
-        lane_pass(e);
 #pragma unroll
         for (int r = 0; r < kRegE; ++r) {
             const uint32_t t = tb | ((uint32_t)r << 5);
-            ts[t] = e.s[r];
-            tc[t] = e.c[r];
+            ts[swz_s(t)] = e.s[r];
+            tc[swz_c(t)] = e.c[r];
         }
     }
     __syncthreads();
     {
-        const uint32_t tb = (uint32_t)lane | ((uint32_t)warp << 6);
+        // registers = bits 0..3, lane = bits 4..8, warps = bits 9..11 (swizzled: conflict-free)
+        const uint32_t tb = ((uint32_t)lane << 4) | ((uint32_t)warp << 9);
 #pragma unroll
         for (int r = 0; r < kRegE; ++r) {
-            const uint32_t t = tb | scatter4(r, 9, 10, 11, 5);
-            e.s[r] = ts[t];
-            e.c[r] = tc[t];
+            e.s[r] = ts[swz_s(tb | (uint32_t)r)];
+            e.c[r] = tc[swz_c(tb | (uint32_t)r)];
         }
-        reg_pass(e, 3);
+        reg_pass(e, 4);
 #pragma unroll
         for (int r = 0; r < kRegE; ++r) {
-            const uint32_t t = tb | scatter4(r, 9, 10, 11, 5);
+            ts[swz_s(tb | (uint32_t)r)] = e.s[r];
+            tc[swz_c(tb | (uint32_t)r)] = e.c[r];
+        }
+    }
+    __syncthreads();
+    {
+        // registers = bits 9, 10, 11, 4, lane = bits 0..3 and 8 (16-entry runs: full
+        // sectors), warps = bits 5..7
+        const uint32_t tb = ((uint32_t)lane & 15u) | (((uint32_t)lane >> 4) << 8) | ((uint32_t)warp << 5);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | scatter4(r, 9, 10, 11, 4);
+            e.s[r] = ts[swz_s(t)];
+            e.c[r] = tc[swz_c(t)];
+        }
+        reg_pass(e, 4);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = tb | scatter4(r, 9, 10, 11, 4);
             __stcs(out_s + row + base + t, e.s[r]);
             __stcs(out_m + row + base + t, final_pass ? user_mask(e.c[r], v) : e.c[r]);
         }
     }
 }
 
-// group bits b0..b0+G-1, 4 <= G <= 8: tile = 2^LO consecutive entries x 2^G group
-// settings (LO + G = 12, or LO = 5 at G = 8), tile index t = (g << LO) | row bits,
+// group bits b0..b0+G-1, 4 <= G <= 7: tile = 2^LO consecutive entries x 2^G group
+// settings (LO + G = 12), tile index t = (g << LO) | row bits,
 // 2^(LO+G-4) threads.  phase A: lane = row bits 0..4, registers = g bits 0..3,
 // warps = g bits 4..G-1 then row bits 5..LO-1; phase B: registers = g bits 4..G-1
 // (the active ones) then g bits 0..7-G, warps = g bits 8-G..3 then row bits 5..LO-1.
-__global__ void __launch_bounds__(512, 2) bps_group_reg_kernel(int m, int b0, int G, int LO, double* __restrict__ s_io,
+__global__ void __launch_bounds__(256, 4) bps_group_reg_kernel(int m, int b0, int G, int LO, double* __restrict__ s_io,
                                                             uint32_t* __restrict__ m_io, int final_pass)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -293,6 +299,66 @@ __global__ void __launch_bounds__(512, 2) bps_group_reg_kernel(int m, int b0, in
     }
 }
 
+// group of 8 bits b0..b0+7 over tiles of 16 consecutive entries (128 B runs of scores:
+// full sectors) x the 256 group settings, 256 threads, 48 KB: tile index t = (g << 4) |
+// row bits.  phase A: lane = row bits 0..3 and g bit 7, registers = g bits 0..3, warps =
+// g bits 4..6; phase B: lane = row bits 0..3 and g bit 0, registers = g bits 4..7,
+// warps = g bits 1..3.  Masks swizzled (t bit 4 ^= t bit 11) so both phases hit 32 banks.
+__device__ __forceinline__ uint32_t swz_g8(uint32_t t) { return t ^ ((t >> 7) & 16u); }
+
+__global__ void __launch_bounds__(256, 4) bps_group8_kernel(int m, int b0, double* __restrict__ s_io,
+                                                         uint32_t* __restrict__ m_io, int final_pass)
+{
+    __shared__ double ts[4096];
+    __shared__ uint32_t tc[4096];
+    const int nb = m - 1;
+    const int rest_bits = nb - 12;
+    const int v = blockIdx.x >> rest_bits;
+    const uint32_t rr = blockIdx.x & ((1u << rest_bits) - 1u);
+    const int lowr = b0 - 4;
+    const uint32_t fixed = ((rr & ((1u << lowr) - 1u)) << 4) | ((rr >> lowr) << (b0 + 8));
+    const int64_t row = (int64_t)v << nb;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t rowbits = lane & 15u, lg = lane >> 4;
+    const int64_t gs = (int64_t)1 << b0;
+    Ent e;
+    {
+        // g = (lg << 7) | (warp << 4) | r
+        const uint32_t g0 = (lg << 7) | (warp << 4);
+        const int64_t i0 = row + fixed + rowbits + ((int64_t)g0 << b0);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            e.s[r] = __ldcs(s_io + i0 + r * gs);
+            e.c[r] = __ldcs(m_io + i0 + r * gs);
+        }
+        reg_pass(e, 4);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = ((g0 | (uint32_t)r) << 4) | rowbits;
+            ts[t] = e.s[r];
+            tc[swz_g8(t)] = e.c[r];
+        }
+    }
+    __syncthreads();
+    {
+        // g = (r << 4) | (warp << 1) | lg
+        const uint32_t g0 = (warp << 1) | lg;
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            const uint32_t t = ((g0 | ((uint32_t)r << 4)) << 4) | rowbits;
+            e.s[r] = ts[t];
+            e.c[r] = tc[swz_g8(t)];
+        }
+        reg_pass(e, 4);
+        const int64_t i0 = row + fixed + rowbits + ((int64_t)g0 << b0);
+#pragma unroll
+        for (int r = 0; r < kRegE; ++r) {
+            __stcs(s_io + i0 + ((int64_t)r << (b0 + 4)), e.s[r]);
+            __stcs(m_io + i0 + ((int64_t)r << (b0 + 4)), final_pass ? user_mask(e.c[r], v) : e.c[r]);
+        }
+    }
+}
+
 cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_s, uint32_t* out_m, cudaStream_t st)
 {
     if (m < 2 || m > 30) return cudaErrorInvalidValue;
@@ -319,8 +385,10 @@ cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_
             e = cudaFuncSetAttribute(bps_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             bps_group_kernel<<<m << (nb - LO - G), 512, smem, st>>>(m, b0, G, LO, out_s, out_m, last ? 1 : 0);
+        } else if (G == 8) {
+            bps_group8_kernel<<<m << (nb - 12), 256, 0, st>>>(m, b0, out_s, out_m, last ? 1 : 0);
         } else {
-            const int LO = G == 8 ? 5 : 12 - G;
+            const int LO = 12 - G;
             const size_t smem = ((size_t)1 << (LO + G)) * 12;
             e = cudaFuncSetAttribute(bps_group_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
