@@ -152,6 +152,16 @@ bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride
  * masks NULL, before a run). */
 bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta);
 
+/* The same for a batch of families (coefficients per family,
+ * e.g. every family of a small m, or the families a search selected): family f is
+ * child children[f] regressed on masks[f] (bit children[f] ignored, bits >= m
+ * ignored).  children, masks: DEVICE, count entries; beta: DEVICE, count*m doubles,
+ * row f as in bnreg_coefficients; a child outside [0, m) gets a row of NaN.
+ * Asynchronous on the handle's stream; count == 0 is a no-op.  BNREG_E_INVAL for
+ * count < 0 or NULL pointers with count > 0, BNREG_E_STATE before data is loaded. */
+bnreg_status bnreg_coefficients_batch(bnreg_t* h, const int32_t* children, const uint32_t* masks, int64_t count,
+                                      double* beta);
+
 /* The north-star calls: the RSS table alone / the BIC table alone. */
 bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
 bnreg_status bnreg_bic(bnreg_t* h, double* out);

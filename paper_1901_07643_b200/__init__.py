@@ -26,7 +26,7 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
-           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_best_subsets", "bnreg_set_root_method",
+           "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_coefficients_batch", "bnreg_best_subsets", "bnreg_set_root_method",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
@@ -76,6 +76,7 @@ def lib():
         "bnreg_run_pairs": ([H, P, P, P], i32),
         "bnreg_set_score": ([H, i32], i32),
         "bnreg_coefficients": ([H, P, P], i32),
+        "bnreg_coefficients_batch": ([H, P, P, i64, P], i32),
         "bnreg_best_subsets": ([H, P, i64, P, P], i32),
         "bnreg_set_root_method": ([H, i32], i32),
         "bnreg_run_pairs_async": ([H, P, P, P], i32),
@@ -228,6 +229,11 @@ class Bnreg:
         """bnreg_best_subsets: for every (child, candidate set) the best score over the set's
         subsets and that subset (DEVICE pointers / tensors; asynchronous)."""
         _check(lib().bnreg_best_subsets(self._h, _dptr(scores), stride, _dptr(best_score), _dptr(best_mask)))
+
+    def coefficients_batch(self, children, masks, count: int, beta):
+        """bnreg_coefficients_batch: coefficients of children[f] on masks[f] for count families
+        into beta (count x m) -- DEVICE pointers / tensors; asynchronous."""
+        _check(lib().bnreg_coefficients_batch(self._h, _dptr(children), _dptr(masks), count, _dptr(beta)))
 
     def coefficients(self, masks=None) -> np.ndarray:
         """bnreg_coefficients: least-squares coefficients of each child on masks[child] (None:

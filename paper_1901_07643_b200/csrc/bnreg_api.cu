@@ -649,9 +649,20 @@ bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta)
         CK(cudaMemcpyAsync(h->d_cmask, masks, (size_t)m * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
         dm = h->d_cmask;
     }
-    CK(launch_coefficients(h->d_root, h->d_order, m, dm, h->d_coef, h->stream));
+    CK(launch_coefficients(h->d_root, h->d_order, m, nullptr, dm, m, h->d_coef, h->stream));
     CK(cudaMemcpyAsync(beta, h->d_coef, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(stream_wait(h->stream));
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_coefficients_batch(bnreg_t* h, const int32_t* children, const uint32_t* masks, int64_t count,
+                                      double* beta)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (count < 0) return fail(BNREG_E_INVAL, "negative count");
+    if (count > 0 && (!children || !masks || !beta)) return fail(BNREG_E_INVAL, "NULL children, masks or beta");
+    if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
+    CK(launch_coefficients(h->d_root, h->d_order, h->plan.m, children, masks, count, beta, h->stream));
     return BNREG_OK;
 }
 

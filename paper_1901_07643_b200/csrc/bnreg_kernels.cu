@@ -344,64 +344,78 @@ cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask
 // regression equations"), from the root R: X~ = Q0 R0 with Q0 orthonormal, so the
 // regression of x~_v on X~_S is that of R0[:, v] on R0[:, S].  One warp per child,
 // lane = row of the m x (|S| + 1) matrix [R0[:, S] | R0[:, v]] (columns by ascending
-// user id): Householder QR, then back-substitution on the |S| x |S| triangle.
+// user id): Householder QR, then back-substitution on the |S| x |S| triangle.  A batch
+// of families (children[f], masks[f]) runs one CTA per family (children NULL: family f
+// is child f); a child outside [0, m) gets a row of NaN.
 __global__ void __launch_bounds__(32) coef_kernel(const double* __restrict__ R, const int* __restrict__ order, int m,
-                                                  const uint32_t* __restrict__ masks, double* __restrict__ beta)
+                                                  const int32_t* __restrict__ children,
+                                                  const uint32_t* __restrict__ masks, int64_t count,
+                                                  double* __restrict__ beta)
 {
     __shared__ double M[32 * 33];          // column-major, ld 32
     __shared__ int cols[32];
-    const int v = blockIdx.x, lane = threadIdx.x;
-    const uint32_t S = masks[v] & ~(1u << v);
-    // position of user id u in the root order
-    int k = 0;
-    if (lane == 0) {
-        for (int u = 0; u < m; ++u)
-            if ((S >> u) & 1u) cols[k++] = u;
-        cols[k] = v;
-    }
-    __syncwarp();
-    k = __popc(S);
-    for (int j = 0; j <= k; ++j) {
-        const int u = cols[j];
-        int pu = 0;
-        for (int c = 0; c < m; ++c)
-            if (order[c] == u) pu = c;
-        M[j * 32 + lane] = lane < m ? R[(size_t)lane * m + pu] : 0.0;
-    }
-    __syncwarp();
-    for (int j = 0; j < k; ++j) {
-        const double xj = M[j * 32 + lane];
-        const double x = lane >= j ? xj : 0.0;
-        const double nrm2 = warp_sum(x * x);
-        const double x0 = __shfl_sync(FULLMASK, xj, j);
-        const double alpha = x0 > 0.0 ? -sqrt(nrm2) : sqrt(nrm2);
-        const double vr = lane == j ? x0 - alpha : x;          // Householder vector (rows >= j)
-        const double vn2 = nrm2 - x0 * x0 + (x0 - alpha) * (x0 - alpha);
-        for (int c = j + 1; c <= k; ++c) {
-            const double mc = M[c * 32 + lane];
-            const double d = warp_sum(vr * mc);
-            if (lane >= j && vn2 > 0.0) M[c * 32 + lane] = mc - 2.0 * vr * d / vn2;
+    const int lane = threadIdx.x;
+    for (int64_t f = blockIdx.x; f < count; f += gridDim.x) {
+        const int v = children ? children[f] : (int)f;
+        if (v < 0 || v >= m) {
+            if (lane < m) beta[f * m + lane] = __longlong_as_double(0x7ff8000000000000LL);
+            continue;
+        }
+        const uint32_t S = masks[f] & ~(1u << v) & (m == 32 ? 0xffffffffu : ((1u << m) - 1u));
+        // position of user id u in the root order
+        int k = 0;
+        if (lane == 0) {
+            for (int u = 0; u < m; ++u)
+                if ((S >> u) & 1u) cols[k++] = u;
+            cols[k] = v;
         }
         __syncwarp();
-        if (lane == j) M[j * 32 + j] = alpha;
-        __syncwarp();
-    }
-    if (lane == 0) {
-        double b[32];
-        for (int i = k - 1; i >= 0; --i) {
-            double t = M[k * 32 + i];
-            for (int c = i + 1; c < k; ++c) t -= M[c * 32 + i] * b[c];
-            b[i] = t / M[i * 32 + i];
+        k = __popc(S);
+        for (int j = 0; j <= k; ++j) {
+            const int u = cols[j];
+            int pu = 0;
+            for (int c = 0; c < m; ++c)
+                if (order[c] == u) pu = c;
+            M[j * 32 + lane] = lane < m ? R[(size_t)lane * m + pu] : 0.0;
         }
-        for (int u = 0; u < m; ++u) beta[(size_t)v * m + u] = 0.0;
-        for (int i = 0; i < k; ++i) beta[(size_t)v * m + cols[i]] = b[i];
+        __syncwarp();
+        for (int j = 0; j < k; ++j) {
+            const double xj = M[j * 32 + lane];
+            const double x = lane >= j ? xj : 0.0;
+            const double nrm2 = warp_sum(x * x);
+            const double x0 = __shfl_sync(FULLMASK, xj, j);
+            const double alpha = x0 > 0.0 ? -sqrt(nrm2) : sqrt(nrm2);
+            const double vr = lane == j ? x0 - alpha : x;          // Householder vector (rows >= j)
+            const double vn2 = nrm2 - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+            for (int c = j + 1; c <= k; ++c) {
+                const double mc = M[c * 32 + lane];
+                const double d = warp_sum(vr * mc);
+                if (lane >= j && vn2 > 0.0) M[c * 32 + lane] = mc - 2.0 * vr * d / vn2;
+            }
+            __syncwarp();
+            if (lane == j) M[j * 32 + j] = alpha;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            double b[32];
+            for (int i = k - 1; i >= 0; --i) {
+                double t = M[k * 32 + i];
+                for (int c = i + 1; c < k; ++c) t -= M[c * 32 + i] * b[c];
+                b[i] = t / M[i * 32 + i];
+            }
+            for (int u = 0; u < m; ++u) beta[f * m + u] = 0.0;
+            for (int i = 0; i < k; ++i) beta[f * m + cols[i]] = b[i];
+        }
+        __syncwarp();
     }
 }
 
-cudaError_t launch_coefficients(const double* R, const int* order, int m, const uint32_t* masks, double* beta,
-                                cudaStream_t st)
+cudaError_t launch_coefficients(const double* R, const int* order, int m, const int32_t* children,
+                                const uint32_t* masks, int64_t count, double* beta, cudaStream_t st)
 {
-    coef_kernel<<<m, 32, 0, st>>>(R, order, m, masks, beta);
+    if (count <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>(count, (int64_t)148 * 32 * 8);
+    coef_kernel<<<grid, 32, 0, st>>>(R, order, m, children, masks, count, beta);
     return cudaGetLastError();
 }
 

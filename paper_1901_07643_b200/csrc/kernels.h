@@ -79,8 +79,8 @@ cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask
 // best parent set within every candidate set (subset-max transform of a score column)
 cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_s, uint32_t* out_m, cudaStream_t st);
 // least-squares coefficients of every child on masks[child] from the root R (one warp per child)
-cudaError_t launch_coefficients(const double* R, const int* order, int m, const uint32_t* masks, double* beta,
-                                cudaStream_t st);
+cudaError_t launch_coefficients(const double* R, const int* order, int m, const int32_t* children,
+                                const uint32_t* masks, int64_t count, double* beta, cudaStream_t st);
 cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2* tab, cudaStream_t st);
 
 }  // namespace bnr

@@ -381,6 +381,50 @@ def test_coefficients_against_oracle():
         h.close()
 
 
+def test_coefficients_batch_against_oracle():
+    """bnreg_coefficients_batch (coefficients per family): every
+    family of cfg1 (1024) and 3000 random families of cfg3 (near-collinear pair
+    included) against oracle.coefficients (lstsq on the centred data), relative 1e-8
+    of the coefficient scale (cfg3: 1e-5, kappa of its pair ~ 5e7); a child
+    outside [0, m) gives a NaN row; bits >= m and the child's own bit are ignored;
+    count 0 is a no-op, a negative count an error."""
+    import torch
+    bn = _bn()
+    rng = np.random.default_rng(12)
+    for cfg in (1, 3):
+        X = datagen.config_data(cfg)
+        n, m = X.shape
+        Xc = oracle.centre(X)
+        h = bn.Bnreg.create(X)
+        if cfg == 1:
+            fams = [(v, S) for v in range(m) for S in range(1 << m) if not (S >> v) & 1]
+        else:
+            fams = [(int(rng.integers(0, m)), int(rng.integers(0, 1 << m))) for _ in range(3000)]
+            fams = [(v, S & ~(1 << v)) for v, S in fams]
+        ch = np.array([v for v, _ in fams] + [-1, m, 0], dtype=np.int32)
+        mk = np.array([S for _, S in fams] + [3, 3, 0xffffffff], dtype=np.uint32)
+        F = len(ch)
+        cd = torch.from_numpy(ch).cuda()
+        md = torch.from_numpy(mk.view(np.int32)).cuda()
+        beta = torch.full((F, m), 7.0, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        h.coefficients_batch(cd, md, F, beta)
+        h.coefficients_batch(cd, md, 0, beta)
+        with pytest.raises(bn.BnregError):
+            h.coefficients_batch(cd, md, -1, beta)
+        torch.cuda.synchronize()
+        b = beta.cpu().numpy()
+        h.close()
+        for f, (v, S) in enumerate(fams):
+            ref = oracle.coefficients(Xc, v, S)
+            scale = max(1.0, np.abs(ref).max())
+            tol = 1e-5 if cfg == 3 else 1e-8
+            assert np.abs(b[f] - ref).max() <= tol * scale, (cfg, v, S)
+        assert np.isnan(b[F - 3]).all() and np.isnan(b[F - 2]).all()
+        ref = oracle.coefficients(Xc, 0, ((1 << m) - 1) & ~1)       # 0xffffffff: every other variable
+        assert np.abs(b[F - 1] - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max())
+
+
 def _bps_run(cfg, layout):
     import torch
     bn = _bn()
