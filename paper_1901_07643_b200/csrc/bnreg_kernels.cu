@@ -2,7 +2,7 @@
 //
 //   centre_kernel      a1  centre the columns (fixed-order sums), NaN/Inf flag
 //   tsqr_kernel        a2  TSQR: Householder QR of 256-row leaves in shared
-//                          memory, then a binary tree of [R_a; R_b] merges
+//                          memory, then an 8-ary tree of stacked-R merges
 //                          (last-arriving CTA merges), diag > 0, rank check
 //   tree_level_kernel  a5  one level of the Alg.2 seed tree: a node's R for
 //                          the residual of the not-yet-decided variables
@@ -54,45 +54,59 @@ __global__ void __launch_bounds__(256) centre_kernel(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------- a2 TSQR
-// Householder QR in shared memory of a column-major nr x m tile (ld = nr),
-// 256 threads.  On return the upper triangle holds R (diag may be negative).
-__device__ void householder_tile(double* T, int nr, int m, double* sh)
+// Householder QR in shared memory of a column-major nr x m tile (ld = nr), a CTA of
+// kTsqrThreads.  On return the upper triangle holds R (diag may be negative); below
+// it are the Householder vectors (callers read the upper triangle only).  Reflection
+// j: x = column j (rows j..), alpha = -sign(x0) ||x||, v = x - alpha e_j; the other
+// columns c > j get c -= 2 (v.c / v.v) v.  One barrier per column: every thread
+// derives alpha and v.v from ||x||^2, which the warp that updated column j (in step
+// j - 1) summed on the fly (double-buffered in sh[0..1]); v's head v0 replaces x0 in
+// registers, so the tile is not written between the barriers except by the updates.
+constexpr int kTsqrThreads = 512;
+__device__ void householder_tile(double* T, int nr, int m, double* sh /* 2 + m */)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int j = 0; j < m && j < nr; ++j) {
-        double* cj = T + (int64_t)j * nr;
-        if (warp == 0) {
-            double s = 0.0;
-            for (int i = j + lane; i < nr; i += 32) s = fma(cj[i], cj[i], s);
-            s = warp_sum(s);
-            if (lane == 0) {
-                double x0 = cj[j];
-                double nrm = sqrt(s);
-                double alpha = (x0 > 0.0) ? -nrm : nrm;
-                double v0 = x0 - alpha;
-                double vtv = s - x0 * x0 + v0 * v0;
-                cj[j] = v0;
-                sh[0] = alpha;
-                sh[1] = vtv;
-            }
-        }
-        __syncthreads();
-        double vtv = sh[1];
-        if (vtv > 0.0) {
-            for (int c = j + 1 + warp; c < m; c += nwarp) {
-                double* cc = T + (int64_t)c * nr;
+    double* const diag = sh + 2;
+    if (warp == 0) {
+        double s = 0.0;
+        for (int i = lane; i < nr; i += 32) s = fma(T[i], T[i], s);
+        s = warp_sum(s);
+        if (lane == 0) sh[0] = s;
+    }
+    __syncthreads();
+    const int nj = m < nr ? m : nr;
+    for (int j = 0; j < nj; ++j) {
+        const double* cj = T + (int64_t)j * nr;
+        const double s = sh[j & 1];
+        const double x0 = cj[j];
+        const double nrm = sqrt(s);
+        const double alpha = (x0 > 0.0) ? -nrm : nrm;
+        const double v0 = x0 - alpha;
+        const double vtv = s - x0 * x0 + v0 * v0;      // 0 only for a zero column (alpha = 0)
+        if (threadIdx.x == 0) diag[j] = alpha;
+        for (int c = j + 1 + warp; c < m; c += nwarp) {
+            double* cc = T + (int64_t)c * nr;
+            double f = 0.0;
+            if (vtv > 0.0) {
                 double d = 0.0;
-                for (int i = j + lane; i < nr; i += 32) d = fma(cj[i], cc[i], d);
-                d = warp_sum(d);
-                double f = 2.0 * d / vtv;
-                for (int i = j + lane; i < nr; i += 32) cc[i] = fma(-f, cj[i], cc[i]);
+                for (int i = j + lane; i < nr; i += 32) d = fma(i == j ? v0 : cj[i], cc[i], d);
+                f = 2.0 * warp_sum(d) / vtv;
+            }
+            double s2 = 0.0;                            // ||column j+1, rows j+1..||^2 after the update
+            for (int i = j + lane; i < nr; i += 32) {
+                const double y = fma(-f, i == j ? v0 : cj[i], cc[i]);
+                cc[i] = y;
+                if (i > j) s2 = fma(y, y, s2);
+            }
+            if (c == j + 1) {
+                s2 = warp_sum(s2);
+                if (lane == 0) sh[(j + 1) & 1] = s2;
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) cj[j] = (vtv > 0.0) ? sh[0] : cj[j];
-        for (int i = j + 1 + (int)threadIdx.x; i < nr; i += blockDim.x) cj[i] = 0.0;
         __syncthreads();
     }
+    for (int j = threadIdx.x; j < nj; j += blockDim.x) T[(int64_t)j * nr + j] = diag[j];
+    __syncthreads();
 }
 
 // rbuf: the merge tree's R's level by level (leaves first, then ceil(c / F) nodes per
@@ -100,12 +114,12 @@ __device__ void householder_tile(double* T, int nr, int m, double* sh)
 // internal node (self-resetting).  A merge of F children is one Householder QR of
 // their stacked R's (F m x m): fewer sequential levels than a binary tree.
 constexpr int kTsqrFanIn = 8;
-__global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr, int64_t n, int m, int rb,
+__global__ void __launch_bounds__(kTsqrThreads) tsqr_kernel(const double* __restrict__ Xr, int64_t n, int m, int rb,
                                                    double* rbuf, unsigned* counters, int nleaf2,
                                                    double* Rroot, int* status)
 {
     extern __shared__ double smem[];
-    __shared__ double sh[4];
+    __shared__ double sh[2 + 32];
     __shared__ int s_old;
     const int b = blockIdx.x;
     const int64_t r0 = (int64_t)b * rb;
@@ -113,9 +127,12 @@ __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr
     if (r0 < n) nr = (int)((n - r0) < rb ? (n - r0) : rb);
     int nrp = nr < m ? m : nr;                    // pad to at least m rows
     double* T = smem;                             // nrp x m, column-major
-    for (int c = 0; c < m; ++c)
-        for (int i = threadIdx.x; i < nrp; i += blockDim.x)
-            T[(int64_t)c * nrp + i] = (i < nr) ? Xr[(int64_t)c * n + r0 + i] : 0.0;
+    // flat element loop, unrolled: the loads of several elements are in flight at once
+#pragma unroll 4
+    for (int e = threadIdx.x; e < nrp * m; e += blockDim.x) {
+        const int c = e / nrp, i = e - c * nrp;
+        T[e] = (i < nr) ? __ldg(Xr + (int64_t)c * n + r0 + i) : 0.0;
+    }
     __syncthreads();
     householder_tile(T, nrp, m, sh);
     // the merge tree: level 0 = the nl leaves, level l+1 has ceil(c_l / F) nodes; the
@@ -141,12 +158,12 @@ __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr
         if (threadIdx.x == 0) counters[poff - nl + parent] = 0u;   // reset for the next launch
         // last arriver: stack the children's R's (nch * m x m) and re-factor
         const int nr2 = nch * m;
-        for (int q = 0; q < nch; ++q) {
-            const double* Rq = rbuf + (int64_t)(off + F * parent + q) * m * m;
-            for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-                int i = e / m, c = e % m;
-                T[(int64_t)c * nr2 + q * m + i] = __ldcg(Rq + e);
-            }
+        const double* R0 = rbuf + (int64_t)(off + F * parent) * m * m;   // the children are consecutive
+#pragma unroll 4
+        for (int e = threadIdx.x; e < nch * m * m; e += blockDim.x) {
+            const int q = e / (m * m), r = e - q * m * m;
+            const int i = r / m, c = r - i * m;
+            T[(int64_t)c * nr2 + q * m + i] = __ldcg(R0 + e);
         }
         __syncthreads();
         householder_tile(T, nr2, m, sh);
@@ -160,27 +177,23 @@ __global__ void __launch_bounds__(256) tsqr_kernel(const double* __restrict__ Xr
         }
         nrp = nr2;
     }
-    // root: sign-normalise rows (diag > 0), rank check (G26)
-    __syncthreads();
-    const double* R = dst;
+    // root: sign-normalise rows (diag > 0), rank check (G26), from the tile
+    // (T holds the root R in its upper triangle, ld = nrp)
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        int i = e / m, c = e % m;
-        double d = __ldcg(R + i * m + i);
-        double v = __ldcg(R + e);
+        const int i = e / m, c = e - i * m;
+        const double d = T[(int64_t)i * nrp + i];
+        const double v = T[(int64_t)c * nrp + i];
         Rroot[e] = (c < i) ? 0.0 : (d < 0.0 ? -v : v);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mx = 0.0;
-        for (int c = 0; c < m; ++c) {
-            double s = 0.0;
-            for (int i = 0; i <= c; ++i) s = fma(Rroot[i * m + c], Rroot[i * m + c], s);
-            mx = fmax(mx, sqrt(s));
-        }
-        bool deficient = !(mx > 0.0);
-        for (int j = 0; j < m; ++j)
-            if (!(fabs(Rroot[j * m + j]) > 1e-12 * mx)) deficient = true;
-        if (deficient) atomicOr(status, 4);
+    if (threadIdx.x < 32) {
+        const int c = threadIdx.x;
+        double s = 0.0;
+        if (c < m)
+            for (int i = 0; i <= c; ++i) s = fma(T[(int64_t)c * nrp + i], T[(int64_t)c * nrp + i], s);
+        double mx = sqrt(s);
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const bool bad = c < m && !(fabs(T[(int64_t)c * nrp + c]) > 1e-12 * mx);
+        if (__any_sync(0xffffffffu, bad || !(mx > 0.0)) && c == 0) atomicOr(status, 4);
     }
 }
 
@@ -315,7 +328,7 @@ cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsign
     if (e != cudaSuccess) return e;
     const int nl = (int)((n + rb - 1) / rb);
     (void)nleaf2;
-    tsqr_kernel<<<nl, 256, smem, st>>>(Xr, n, m, rb, rbuf, counters, nleaf2, Rroot, status);
+    tsqr_kernel<<<nl, kTsqrThreads, smem, st>>>(Xr, n, m, rb, rbuf, counters, nleaf2, Rroot, status);
     return cudaGetLastError();
 }
 
