@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(256) centre_kernel(const double* __restrict__ 
 // derives alpha and v.v from ||x||^2, which the warp that updated column j (in step
 // j - 1) summed on the fly (double-buffered in sh[0..1]); v's head v0 replaces x0 in
 // registers, so the tile is not written between the barriers except by the updates.
-constexpr int kTsqrThreads = 512;
+#ifndef TSQR_THREADS
+#define TSQR_THREADS 1024
+#endif
+constexpr int kTsqrThreads = TSQR_THREADS;
 __device__ void householder_tile(double* T, int nr, int m, double* sh /* 2 + m */)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
