@@ -122,3 +122,27 @@ def test_walk_rejects_large_k(bn):
     nibbles, at most 2 entries per lane)."""
     with pytest.raises(bn.BnregError):
         bn.bnreg_plan_query(24, 1000, bn.options(free_vars=9))
+
+
+def test_null_handle_is_rejected(bn):
+    """include/bnreg.h: every call taking a handle returns BNREG_E_INVAL (1) for a NULL
+    handle, with a message in bnreg_last_error, before touching the device (no GPU
+    needed); the int64 queries return -1 and bnreg_destroy(NULL) is a no-op."""
+    import ctypes
+    L = bn.lib()
+    checked = 0
+    for name in bn.SYMBOLS:
+        f = getattr(L, name)
+        args = f.argtypes or []
+        if not args or args[0] is not ctypes.c_void_p or name == "bnreg_create":
+            continue
+        vals = [None] + [0 if a in (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32) else None for a in args[1:]]
+        r = f(*vals)
+        if f.restype is ctypes.c_int32:
+            assert r == 1, name
+            assert L.bnreg_last_error(), name
+            checked += 1
+        elif f.restype is ctypes.c_int64:
+            assert r == -1, name
+    assert checked >= 15
+    L.bnreg_destroy(None)
