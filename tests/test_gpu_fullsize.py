@@ -179,14 +179,20 @@ def test_cfg5_full_size():
     _check(5, 5000, 100000, pairs=True)   # the bench layout
 
 
-def test_cfg4_best_subsets_sampled():
-    """bnreg_best_subsets at cfg4's full size (23 mask bits: the low tile and two high
-    groups), in place over the record table's BIC column copy: for sampled candidate
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_best_subsets_sampled(cfg):
+    """bnreg_best_subsets at full size on the record table's BIC column: cfg4 (23 mask
+    bits: the low tile and groups of 6 and 5) and cfg5 (27 bits: the low tile and groups
+    of 8 and 7, the timed configuration of tools/bps_time.py): for sampled candidate
     sets of up to 9 variables, the maximum over their subsets by enumeration of the
     GPU's own scores (G14), and for every child the full set = the run's best."""
     import torch
     import paper_1901_07643_b200 as bn
-    X = datagen.config_data(4)
+    if cfg == 5:
+        free, total = torch.cuda.mem_get_info()
+        if free < 110e9:
+            pytest.skip("cfg5 needs 105 GB of device memory (records + best tables)")
+    X = datagen.config_data(cfg)
     n, m = X.shape
     h = bn.Bnreg.create(X)
     F = h.num_families()
@@ -197,7 +203,7 @@ def test_cfg4_best_subsets_sampled():
     bmk = torch.empty(F, dtype=torch.int32, device="cuda")
     h.best_subsets(t.data_ptr() + 8, 2, bs, bmk)
     torch.cuda.synchronize()
-    rng = np.random.default_rng(24)
+    rng = np.random.default_rng(20 + cfg)
     for v in range(m):
         i = oracle.index(m, v, ((1 << m) - 1) & ~(1 << v))
         assert _gather(bmk, [i]).view(np.uint32)[0] == best_m[v] and _gather(bs, [i])[0] == best_b[v]
@@ -215,3 +221,5 @@ def test_cfg4_best_subsets_sampled():
         i = oracle.index(m, v, sum(1 << u for u in C))
         assert _gather(bs, [i])[0] == bsc and _gather(bmk, [i]).view(np.uint32)[0] == bS
     h.close()
+    del t, bs, bmk
+    torch.cuda.empty_cache()
