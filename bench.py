@@ -187,6 +187,125 @@ def bench_reference(args):
 
 
 # ---------------------------------------------------------------------------- ours
+class NcclComm:
+    """The step's two exchanges over torch.distributed on the current stream (NCCL over
+    NVLink): a3 broadcast of the root R, a11 all-gather of the per-rank best records."""
+
+    def __init__(self, dist):
+        self.dist = dist
+
+    def broadcast(self, t, src):
+        self.dist.broadcast(t, src)
+
+    def all_gather(self, out, t):
+        self.dist.all_gather_into_tensor(out, t)
+
+
+class HostStagedComm(NcclComm):
+    """The same exchanges for a CPU-only backend (gloo): the device tensors are staged
+    through host memory.  Used by the multi-process test on one GPU (tests/), where
+    NCCL cannot put two ranks on one device."""
+
+    def broadcast(self, t, src):
+        c = t.cpu()
+        self.dist.broadcast(c, src)
+        t.copy_(c)
+
+    def all_gather(self, out, t):
+        import torch
+        c = torch.empty(out.numel(), dtype=out.dtype)        # gloo wants a flat output
+        self.dist.all_gather_into_tensor(c, t.cpu().reshape(-1))
+        out.copy_(c.view(out.shape))
+
+
+class Pipeline:
+    """One bench step on this rank, through the C-ABI (paper_1901_07643_b200):
+      rank 0: a1-a2 load (centre + TSQR) of X          [bnreg_load_async]
+      N > 1:  a3 broadcast of R from rank 0              [bnreg_get/set_root_device + comm]
+      every rank: a4-a11 seeds, walk, stores, best      [bnreg_run_pairs_async / bnreg_run_async]
+      N > 1:  all-gather of the per-rank best records, device merge (G14)
+                                                         [comm + bnreg_best_merge_async]
+    No host synchronisation inside a device step; load errors surface at sync()."""
+
+    def __init__(self, bn, h, X, world, rank, dev, comm=None, pairs=True, outputs="both"):
+        import numpy as np
+        import torch
+        self.bn, self.h, self.world, self.rank, self.comm = bn, h, world, rank, comm
+        n, m = X.shape
+        self.m = m
+        F = h.num_families()
+        self.pairs = pairs
+        if pairs:
+            self.tab = torch.empty((F, 2), dtype=torch.float64, device=dev)
+            self.rss = self.bic = None
+        else:
+            self.tab = None
+            self.rss = torch.empty(F, dtype=torch.float64, device=dev) if outputs in ("both", "rss") else None
+            self.bic = torch.empty(F, dtype=torch.float64, device=dev) if outputs in ("both", "bic") else None
+        self.Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)          # column-major n x m
+        self.Xpin = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()
+        self.Xpin_np = self.Xpin.numpy().T                                   # Fortran view of pinned memory
+        self.Rt = torch.empty(m * m, dtype=torch.float64, device=dev)
+        # this rank's best as one record [m BICs | m masks | pad] (16 m bytes): one all-gather
+        self.rec = torch.empty(2 * m, dtype=torch.float64, device=dev)
+        self.gat = torch.empty((world, 2 * m), dtype=torch.float64, device=dev)
+        self.best_bic = torch.empty(m, dtype=torch.float64, device=dev)
+        self.best_mask = torch.empty(m, dtype=torch.int32, device=dev)
+
+    def _rec_ptrs(self, base):
+        return base + 8 * self.m, base        # (masks, bics)
+
+    def _exchange_root(self):
+        if self.world > 1:
+            if self.rank == 0:
+                self.h.get_root_device(self.Rt)
+            self.comm.broadcast(self.Rt, 0)
+            if self.rank != 0:
+                self.h.set_root_device(self.Rt)
+
+    def _walk(self):
+        bm, bb = self._rec_ptrs(self.rec.data_ptr())
+        if self.world == 1:
+            bm, bb = self.best_mask.data_ptr(), self.best_bic.data_ptr()
+        if self.pairs:
+            self.h.run_pairs_async(self.tab, bm, bb)
+        else:
+            self.h.run_async(self.rss, self.bic, bm, bb)
+
+    def _merge(self):
+        if self.world > 1:
+            self.comm.all_gather(self.gat, self.rec)
+            gm, gb = self._rec_ptrs(self.gat.data_ptr())
+            self.h.best_merge_async(self.world, gm, gb, self.best_mask, self.best_bic, row_bytes=16 * self.m)
+
+    def step_device(self):
+        """Inputs resident in HBM."""
+        if self.rank == 0:
+            self.h.load_async(self.Xd)
+        self._exchange_root()
+        self._walk()
+        self._merge()
+
+    def step_e2e(self):
+        """X from pinned host memory (H2D inside the step), the merged per-child best read
+        back to the host (D2H) -- returns (best_mask, best_bic) numpy."""
+        import numpy as np
+        if self.rank == 0:
+            self.h.load_async(self.Xpin_np)
+        self._exchange_root()
+        self._walk()
+        self._merge()
+        bm = self.best_mask.cpu().numpy().view(np.uint32)
+        bb = self.best_bic.cpu().numpy()
+        return bm, bb
+
+    def h2d_bytes(self):
+        return self.Xd.numel() * 8 if self.rank == 0 else 0
+
+    def d2h_bytes(self):
+        return self.m * (4 + 8)
+
+
 def bench_ours(args):
     import numpy as np
     import torch
@@ -206,72 +325,16 @@ def bench_ours(args):
     opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, warps_per_cta=args.wpc)
     h = bn.Bnreg(n, m, opt)
     plan = bn.bnreg_plan_query(m, n, opt)
-    # one explicit (non-legacy) stream for torch and the handle: the timing events are
-    # recorded on the stream the kernels run on (the legacy default stream would make
-    # bnreg_set_stream fall back to the handle's own stream)
+    # one explicit (non-legacy) stream for torch, NCCL ordering and the handle: the timing
+    # events are recorded on the stream the kernels run on
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     h.set_stream(stream.cuda_stream)
     F = h.num_families()
     total = m << (m - 1)
     pairs = args.layout == "pairs" and args.outputs == "both"
-    if pairs:
-        tab = torch.empty((F, 2), dtype=torch.float64, device=dev)
-        rss = bic = None
-    else:
-        rss = torch.empty(F, dtype=torch.float64, device=dev)
-        bic = torch.empty(F, dtype=torch.float64, device=dev)
-    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)       # column-major n x m
-    Rt = torch.empty(m * m, dtype=torch.float64, device=dev)
-    bm_d = torch.empty(m, dtype=torch.int32, device=dev)
-    bb_d = torch.empty(m, dtype=torch.float64, device=dev)
-    Xpin = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()
-    Xpin_np = Xpin.numpy().T                                         # Fortran view of pinned memory
-
-    def broadcast_root():
-        if world > 1:
-            if rank == 0:
-                h.get_root_device(Rt)
-            dist.broadcast(Rt, 0)
-            if rank != 0:
-                h.set_root_device(Rt)
-
-    def gather_best(bm_host=None, bb_host=None):
-        if world == 1:
-            return
-        gm = [torch.empty_like(bm_d) for _ in range(world)]
-        gb = [torch.empty_like(bb_d) for _ in range(world)]
-        dist.all_gather(gm, bm_d)
-        dist.all_gather(gb, bb_d)
-        M = torch.stack(gm).cpu().numpy().view(np.uint32)
-        B = torch.stack(gb).cpu().numpy()
-        bn.bnreg_best_merge(m, M, B)
-
-    out_r = rss if args.outputs in ("both", "rss") else None
-    out_b = bic if args.outputs in ("both", "bic") else None
-
-    def step_device():
-        if rank == 0:
-            h.load(Xd)
-        broadcast_root()
-        if pairs:
-            h.run_pairs_async(tab, bm_d, bb_d)
-        else:
-            h.run_async(out_r, out_b, bm_d, bb_d)
-        gather_best()
-
-    def step_e2e():
-        if rank == 0:
-            h.load(Xpin_np)                      # H2D of X from pinned host memory
-        broadcast_root()
-        if pairs:
-            bm, bb = h.run_pairs(tab)            # D2H of the per-child best
-        else:
-            bm, bb = h.run(rss, bic)
-        if world > 1:
-            bm_d.copy_(torch.from_numpy(bm.view(np.int32)))
-            bb_d.copy_(torch.from_numpy(bb))
-            gather_best()
+    pipe = Pipeline(bn, h, X, world, rank, dev, NcclComm(dist) if world > 1 else None, pairs, args.outputs)
+    step_device, step_e2e = pipe.step_device, pipe.step_e2e
 
     def timed(step, k, w, with_clocks=False):
         for _ in range(w):
@@ -300,9 +363,12 @@ def bench_ours(args):
             ms = float(t.item())
         return ms, clocks
 
-    # device-resident inputs: the headline value + the traversal kernel's own time
-    h.timing(1)
+    # device-resident inputs: the headline value (no host synchronisation inside the timed
+    # steps), then the same steps again with the handle's per-phase CUDA events (the
+    # traversal kernel's own time; collecting them synchronises once per step)
+    h.timing(0)
     ms, clocks = timed(step_device, args.steps, args.warmup, with_clocks=True)
+    h.sync()                                   # deferred load checks (NaN/Inf, rank)
     h.timing(1)
     ms_chk, _ = timed(step_device, args.steps, 0)
     tms, runs = h.timing(0)
@@ -313,7 +379,7 @@ def bench_ours(args):
     if not args.no_e2e:
         ms_e2e, _ = timed(step_e2e, args.steps, 1)
         e2e = {"value": total * args.steps / (ms_e2e / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": world * m * (4 + 8),
+               "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": world * pipe.d2h_bytes(),
                "ms_per_step": ms_e2e / args.steps}
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_FAMILY * F / (trav_ms / 1e3) / 1e9
@@ -328,7 +394,7 @@ def bench_ours(args):
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{done} families uniformly sampled from cfg{args.config}'s {total} "
                          f"(O1 per-family Householder QR, n={n}), {el:.1f} s on the host"}
-    launches = args.steps * (h.launches_per_run() + (2 if rank == 0 else 0))
+    launches = args.steps * (h.launches_per_run() + (2 if rank == 0 else 0) + (1 if world > 1 else 0))
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,

@@ -27,8 +27,11 @@
  *     the smaller |S|, then the smaller mask.
  *   - A handle is not thread-safe; distinct handles are independent.  Output is
  *     bit-identical across runs at a fixed world size and build.
- *   - Limits: 2 <= m <= 30 (device memory limits m far below: the RSS+BIC tables
- *     take 16 m 2^(m-1) bytes, 60 GB at m = 28), n >= m + 1.
+ *   - Limits: 2 <= m <= 30, n >= m + 1.  One rank writes at most 2^32 table
+ *     entries (32-bit entry offsets in the walk kernel): m <= 28 on one rank,
+ *     m = 29 needs world >= 2 and m = 30 world >= 4 (bnreg_create_ex returns
+ *     BNREG_E_INVAL otherwise).  Device memory limits m further: the RSS+BIC
+ *     tables take 16 m 2^(m-1) bytes per job (60 GB at m = 28).
  */
 #ifndef BNREG_H
 #define BNREG_H
@@ -53,7 +56,8 @@ typedef enum {
 
 typedef struct {
     int32_t free_vars;        /* k, the free block each worker permutes with Upsilon(k);
-                                 0 = auto (min(m, 9)); 2 <= k <= min(m, 16)              */
+                                 0 = auto (min(m, 8)); 2 <= k <= min(m, 8) (the walk
+                                 kernel keeps a step's free list in one u32 of nibbles) */
     int32_t levels_in_warp;   /* seed-tree levels each warp derives itself; -1 = auto (4) */
     int32_t world;            /* ranks sharing the walk (power of two); 0 or 1 = single */
     int32_t rank;             /* this rank, 0 <= rank < world                             */
@@ -76,6 +80,17 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* opt, bnr
  * a HOST pointer when x_on_device == 0 (copied host->device here), else a
  * DEVICE pointer (read in place).  Errors: BNREG_E_NONFINITE, BNREG_E_RANK. */
 bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device);
+
+/* As bnreg_load, enqueued on the handle's stream without waiting for it (no host
+ * synchronisation inside a pipelined step).  A host X must stay valid (and, for
+ * an asynchronous copy, be pinned) until the stream has passed the load.  The
+ * NaN/Inf and rank checks are deferred: the next synchronous call on the handle
+ * (bnreg_sync, bnreg_run, bnreg_run_pairs) reports BNREG_E_NONFINITE /
+ * BNREG_E_RANK; work enqueued in between computes on the rejected data. */
+bnreg_status bnreg_load_async(bnreg_t* h, const double* X, int32_t x_on_device);
+
+/* Wait for the handle's stream; report a CUDA error or a deferred load error. */
+bnreg_status bnreg_sync(bnreg_t* h);
 
 /* Number of table entries this handle writes: m 2^(m-1), or this rank's share. */
 int64_t bnreg_num_families(const bnreg_t* h);
@@ -136,7 +151,9 @@ bnreg_status bnreg_set_root_method(bnreg_t* h, int32_t method);
  * tie-break: larger score, then smaller |S|, then smaller mask).  scores: DEVICE, the
  * score column of a run on this handle: the BIC table (stride 1) or the record
  * table's column (out_pairs + 1, stride 2).  best_score / best_mask: DEVICE,
- * bnreg_num_families entries each (best_score may alias scores when stride == 1).
+ * bnreg_num_families entries each.  best_score may alias scores only exactly and
+ * with stride == 1; any other overlap of [scores, scores + stride * entries) with
+ * best_score or best_mask is rejected (BNREG_E_INVAL).
  * Single rank only (world 1: a child's candidate lattice is not split).
  * Asynchronous on the handle's stream. */
 bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride, double* best_score,
@@ -149,7 +166,7 @@ bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride
  * the last run.  beta: HOST, m*m doubles, row-major: beta[v*m + u] is the
  * coefficient of parent u in child v's regression on the centred data, 0 for u
  * outside the set.  Synchronous.  BNREG_E_STATE before data is loaded (or, with
- * masks NULL, before a run). */
+ * masks NULL, before a run on the currently loaded data or root). */
 bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta);
 
 /* The same for a batch of families (coefficients per family,
@@ -162,7 +179,12 @@ bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta)
 bnreg_status bnreg_coefficients_batch(bnreg_t* h, const int32_t* children, const uint32_t* masks, int64_t count,
                                       double* beta);
 
-/* The north-star calls: the RSS table alone / the BIC table alone. */
+/* The north-star calls: the RSS table alone (the residual sum of squares of every
+ * family, §1 "regressions for all child and parent-set combinations",
+ * Eq.5 PAPER.md:109-113 read with G3) / the BIC table alone (reading G5).
+ * out: caller-owned DEVICE buffer of bnreg_num_families(h) doubles, table layout as
+ * above.  = bnreg_run(h, out, NULL, NULL, NULL) / bnreg_run(h, NULL, out, NULL, NULL):
+ * synchronous; BNREG_E_STATE before data (or a root) is loaded. */
 bnreg_status bnreg_all_rss(bnreg_t* h, double* out);
 bnreg_status bnreg_bic(bnreg_t* h, double* out);
 
@@ -174,11 +196,14 @@ bnreg_status bnreg_set_stream(bnreg_t* h, void* stream);
  * and that order (order[pos] = user id).  Either pointer may be NULL. HOST. */
 bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host);
 
-/* Multi-GPU step a3: copy the root R (m*m doubles, row-major, root order) into
- * / out of a caller-owned DEVICE buffer, so the harness can broadcast it from
- * rank 0 with NCCL over NVLink.  Ranks that receive it call
- * bnreg_set_root_device instead of bnreg_load.  Both are stream-ordered on the
- * handle's stream and synchronise before returning. */
+/* Multi-GPU step a3 (§6: every processor walks from the root QRD;
+ * the north star broadcasts it from rank 0 instead of refactoring X per rank):
+ * copy the root R (m*m doubles, row-major, root order) into / out of a
+ * caller-owned DEVICE buffer, so the harness can broadcast it with NCCL over
+ * NVLink.  Ranks that receive it call bnreg_set_root_device instead of
+ * bnreg_load.  Both are enqueued on the handle's stream WITHOUT host
+ * synchronisation: order the collective on the same stream (or synchronise).
+ * get: BNREG_E_STATE before a load. */
 bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev);
 bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev);
 
@@ -192,10 +217,20 @@ bnreg_status bnreg_plan_shard_ranges(int32_t m, int64_t n, const bnreg_options* 
                                      int64_t* lens);
 int64_t bnreg_plan_local_index(int32_t m, int64_t n, const bnreg_options* opt, int64_t global_index);
 
-/* Deterministic merge of per-rank bests (step a11 after the all-gather):
- * masks/bics are nparts x m row-major HOST arrays. */
+/* Deterministic merge of per-rank bests (step a11 after the all-gather; reading
+ * G14): masks/bics are nparts x m row-major HOST arrays; a mask 0xffffffff marks
+ * "no candidate". */
 bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, const double* bics,
                               uint32_t* out_mask, double* out_bic);
+
+/* The same merge on the device, enqueued on the handle's stream (no host round
+ * trip inside a multi-GPU step): row q (q < nparts) of masks_dev / bics_dev holds
+ * m DEVICE entries at byte offset q * row_bytes (row_bytes = 0: dense rows, 4m /
+ * 8m bytes; else a multiple of 8, >= 8m -- e.g. one all-gathered record per rank
+ * [m BICs | m masks | pad] with row_bytes = 16m); out_* DEVICE arrays of m.
+ * Bit-identical to bnreg_best_merge. */
+bnreg_status bnreg_best_merge_async(bnreg_t* h, int32_t nparts, const uint32_t* masks_dev, const double* bics_dev,
+                                    int64_t row_bytes, uint32_t* out_mask_dev, double* out_bic_dev);
 
 /* Per-phase device time of the runs since the last reset, from CUDA events on
  * the launching stream.  enable: 1 = start recording (and reset), 0 = stop,
@@ -208,9 +243,10 @@ bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* r
  * best reduction); bnreg_load adds 2 (centre, TSQR).  -1 for a NULL handle. */
 int64_t bnreg_launches_per_run(const bnreg_t* h);
 
-/* Plan introspection (host only, no GPU): info[0..11] = k, b, p, bh, L1, LW,
- * npacks (this rank), schedule length, local families, total families,
- * traversal smem bytes per warp, r (rank selector bits). */
+/* Plan introspection (host only, no GPU): info must hold 13 entries:
+ * info[0..12] = k, b, p, bh, L1, LW, npacks (this rank), schedule length, local
+ * families, total families, traversal smem bytes per warp, r (rank selector
+ * bits), g (gang bits: 2^g lockstep warps per walk CTA). */
 bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* opt, int64_t* info);
 
 /* Upsilon(k) (1-based swap positions) as the kernels use it; returns its length

@@ -32,9 +32,11 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc, -O2, OpenMP)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
         cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-D_GNU_SOURCE",
-               "-o", _LIB, _SRC, "-lm"]
+               "-o", tmp, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
+        os.replace(tmp, _LIB)        # atomic: a process that has the old library mapped keeps it
     return _LIB
 
 
@@ -73,6 +75,10 @@ def lib():
         L.oracle_rss_reduced_indices.restype = None
         L.oracle_best.argtypes = [P, i32, P, P]
         L.oracle_best.restype = None
+        L.oracle_reduced_table.argtypes = [P, i32, i64, P, P, i32]
+        L.oracle_reduced_table.restype = None
+        L.oracle_best_reduced.argtypes = [P, i32, i64, P, P, P, P, P, i32]
+        L.oracle_best_reduced.restype = None
         L.oracle_num_threads.argtypes = []
         L.oracle_num_threads.restype = i32
         _lib = L
@@ -289,3 +295,29 @@ def best(bic_table, m: int):
     bb = np.zeros(m)
     lib().oracle_best(_ptr(b), m, _ptr(bm), _ptr(bb))
     return bm, bb
+
+
+def best_reduced(R0, n: int, threads: int = 0):
+    """oracle_best_reduced: per child, over all 2^(m-1) parent sets, the G14 best by O2 RSS
+    and BIC, and the runner-up, without storing the table.  Returns a dict of arrays:
+    best_mask, best_bic, best_rss, second_mask, second_bic."""
+    R0 = _f64(R0)
+    m = R0.shape[0]
+    bm = np.zeros(m, dtype=np.uint32)
+    bb = np.zeros(m)
+    br = np.zeros(m)
+    sm = np.zeros(m, dtype=np.uint32)
+    sb = np.zeros(m)
+    lib().oracle_best_reduced(_ptr(R0), m, n, _ptr(bm), _ptr(bb), _ptr(br), _ptr(sm), _ptr(sb), threads)
+    return {"best_mask": bm, "best_bic": bb, "best_rss": br, "second_mask": sm, "second_bic": sb}
+
+
+def reduced_table(R0, n: int, want_bic: bool = True, threads: int = 0):
+    """O2 RSS and its BIC over all m*2^(m-1) families (oracle_reduced_table)."""
+    R0 = _f64(R0)
+    m = R0.shape[0]
+    total = m << (m - 1)
+    r = np.empty(total)
+    b = np.empty(total) if want_bic else None
+    lib().oracle_reduced_table(_ptr(R0), m, n, _ptr(r), _ptr(b) if want_bic else None, threads)
+    return r, b

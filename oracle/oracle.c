@@ -47,6 +47,10 @@
  *   oracle_bic           G5/G13.
  *   oracle_table         O1 over every family (OpenMP over families).
  *   oracle_best          G14 argmax per child over a full BIC table.
+ *   oracle_reduced_table O2 + oracle_bic over every family (full-size parity).
+ *   oracle_best_reduced  oracle_best over O2 + oracle_bic, streamed (no table):
+ *                        per child the G14 best and runner-up (cfg4/cfg5 argmax
+ *                        goldens, tests/golden/make_best_golden.py).
  */
 #include <math.h>
 #include <stdint.h>
@@ -308,6 +312,23 @@ ORACLE_API void oracle_rss_reduced_indices(const double *R0, int m, const int64_
     }
 }
 
+/* O2 over the whole table with its BIC (either output may be NULL). */
+ORACLE_API void oracle_reduced_table(const double *R0, int m, int64_t n, double *rss, double *bic, int threads)
+{
+    int64_t total = (int64_t)m << (m - 1);
+#ifdef _OPENMP
+    if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(threads)
+#endif
+    for (int64_t q = 0; q < total; ++q) {
+        int v;
+        uint32_t S = oracle_mask_of(m, q, &v);
+        double r = oracle_rss_reduced(R0, m, v, S);
+        if (rss) rss[q] = r;
+        if (bic) bic[q] = oracle_bic(r, n, popc32(S));
+    }
+}
+
 /* ---- a11: argmax per child (G14) --------------------------------------- */
 ORACLE_API void oracle_best(const double *bic, int m, uint32_t *best_mask, double *best_bic)
 {
@@ -326,6 +347,71 @@ ORACLE_API void oracle_best(const double *bic, int m, uint32_t *best_mask, doubl
         }
         best_mask[v] = bm;
         best_bic[v] = bb;
+    }
+}
+
+/* ---- a11 over O2 without storing the table (cfg4/cfg5 full size) -------- */
+/* For every child v: over all 2^(m-1) parent sets, the G14 best (mask, BIC,
+ * RSS) and the runner-up (the G14 best of the other sets) by O2 RSS
+ * (oracle_rss_reduced) and oracle_bic -- the composition of oracle_rss_reduced,
+ * oracle_bic and oracle_best, streamed so the table never exists.  out arrays
+ * have m entries each (any may be NULL except best_mask / best_bic).
+ * R0: row-major m x m (oracle_qr_r). */
+static int g14_better(double b1, uint32_t s1, double b2, uint32_t s2)
+{
+    if (b1 != b2) return b1 > b2;
+    int p1 = popc32(s1), p2 = popc32(s2);
+    return p1 != p2 ? p1 < p2 : s1 < s2;
+}
+
+typedef struct { double b1, b2, r1; uint32_t m1, m2; int have1, have2; } top2_t;
+
+static void top2_add(top2_t *t, double b, uint32_t S, double rss)
+{
+    if (!t->have1 || g14_better(b, S, t->b1, t->m1)) {
+        if (t->have1) { t->b2 = t->b1; t->m2 = t->m1; t->have2 = 1; }
+        t->b1 = b; t->m1 = S; t->r1 = rss; t->have1 = 1;
+    } else if (!t->have2 || g14_better(b, S, t->b2, t->m2)) {
+        t->b2 = b; t->m2 = S; t->have2 = 1;
+    }
+}
+
+ORACLE_API void oracle_best_reduced(const double *R0, int m, int64_t n, uint32_t *best_mask, double *best_bic,
+                                    double *best_rss, uint32_t *second_mask, double *second_bic, int threads)
+{
+    int64_t per = (int64_t)1 << (m - 1);
+#ifdef _OPENMP
+    if (threads <= 0) threads = omp_get_max_threads();
+#endif
+    for (int v = 0; v < m; ++v) {
+        top2_t all = {0};
+#ifdef _OPENMP
+#pragma omp parallel num_threads(threads)
+#endif
+        {
+            top2_t t = {0};
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 4096)
+#endif
+            for (int64_t c = 0; c < per; ++c) {
+                int vv;
+                uint32_t S = oracle_mask_of(m, (int64_t)v * per + c, &vv);
+                double r = oracle_rss_reduced(R0, m, v, S);
+                top2_add(&t, oracle_bic(r, n, popc32(S)), S, r);
+            }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+            {
+                if (t.have1) top2_add(&all, t.b1, t.m1, t.r1);
+                if (t.have2) top2_add(&all, t.b2, t.m2, 0.0);
+            }
+        }
+        best_mask[v] = all.m1;
+        best_bic[v] = all.b1;
+        if (best_rss) best_rss[v] = all.r1;
+        if (second_mask) second_mask[v] = all.have2 ? all.m2 : 0xffffffffu;
+        if (second_bic) second_bic[v] = all.have2 ? all.b2 : -INFINITY;
     }
 }
 

@@ -25,7 +25,7 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
           5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
-SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_num_families", "bnreg_index",
+SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", "bnreg_sync", "bnreg_best_merge_async", "bnreg_num_families", "bnreg_index",
            "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_coefficients_batch", "bnreg_best_subsets", "bnreg_set_root_method",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
@@ -68,6 +68,9 @@ def lib():
         "bnreg_create": ([P, i64, i32, PH], i32),
         "bnreg_create_ex": ([i64, i32, POPT, PH], i32),
         "bnreg_load": ([H, P, i32], i32),
+        "bnreg_load_async": ([H, P, i32], i32),
+        "bnreg_sync": ([H], i32),
+        "bnreg_best_merge_async": ([H, i32, P, P, i64, P, P], i32),
         "bnreg_num_families": ([H], i64),
         "bnreg_index": ([i32, i32, u32], i64),
         "bnreg_local_index": ([H, i64], i64),
@@ -206,6 +209,28 @@ class Bnreg:
             _check(lib().bnreg_load(self._h, _hptr(X), 0))
         else:
             _check(lib().bnreg_load(self._h, _dptr(X), 1))
+
+    def load_async(self, X):
+        """bnreg_load_async: a device pointer / CUDA tensor, or a host numpy array that stays
+        alive (pinned for an overlapped copy) until the stream passes the load; the NaN/rank
+        checks surface on the next synchronous call."""
+        if isinstance(X, np.ndarray):
+            if X.shape != (self.n, self.m) or not X.flags.f_contiguous or X.dtype != np.float64:
+                raise ValueError("load_async needs a Fortran-ordered float64 (n, m) array")
+            self._keep = X
+            _check(lib().bnreg_load_async(self._h, _hptr(X), 0))
+        else:
+            _check(lib().bnreg_load_async(self._h, _dptr(X), 1))
+
+    def sync(self):
+        """bnreg_sync: wait for the handle's stream; raises a deferred load error."""
+        _check(lib().bnreg_sync(self._h))
+
+    def best_merge_async(self, nparts: int, masks_dev, bics_dev, out_mask_dev, out_bic_dev, row_bytes: int = 0):
+        """bnreg_best_merge_async: G14 merge of nparts rows of m device (mask, BIC) entries
+        (row q at byte offset q * row_bytes; 0 = dense rows)."""
+        _check(lib().bnreg_best_merge_async(self._h, nparts, _dptr(masks_dev), _dptr(bics_dev), row_bytes,
+                                            _dptr(out_mask_dev), _dptr(out_bic_dev)))
 
     def num_families(self) -> int:
         return lib().bnreg_num_families(self._h)

@@ -1,6 +1,12 @@
-"""Build libbnreg.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension)."""
+"""Build libbnreg.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
+
+The library is rebuilt whenever the sources, headers, nvcc flags or extra -D
+defines differ from the ones recorded in libbnreg.stamp (a hash), so a copied-in
+or variant build can never be mistaken for the committed sources.  Variant builds
+(e.g. the K8 write-counting debug build) go to their own path (`out=`)."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -15,28 +21,42 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(OUT):
-        return True
-    t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(HERE, "..", "include", "bnreg.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+def _digest(defines) -> str:
+    h = hashlib.sha256()
+    for f in SOURCES + HEADERS:
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    with open(os.path.join(HERE, "..", "include", "bnreg.h"), "rb") as fh:
+        h.update(fh.read())
+    h.update(" ".join([NVCC, *FLAGS, *defines]).encode())
+    return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, *[os.path.join(CSRC, s) for s in SOURCES]]
+def _stamp(out):
+    return os.path.splitext(out)[0] + ".stamp"
+
+
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    defines = list(defines)
+    dg = _digest(defines)
+    st = _stamp(out)
+    if not force and os.path.exists(out) and os.path.exists(st) and open(st).read().strip() == dg:
+        return out
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *defines, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed")
-    with open(os.path.join(HERE, "ptxas.log"), "w") as f:
-        f.write(r.stderr)
+    os.replace(tmp, out)             # atomic: a process that has the old library mapped keeps it
+    if out == OUT:
+        with open(os.path.join(HERE, "ptxas.log"), "w") as f:
+            f.write(r.stderr)
+    with open(st, "w") as f:
+        f.write(dg + "\n")
     if verbose:
         sys.stderr.write(r.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -80,6 +80,8 @@ struct bnreg {
     double2* d_lntab9 = nullptr;   // fast-log table (a9), 512 entries (walk kernel, debug_ln)
     int wpc = 4;                   // warps per walk CTA (one gang)
     bool loaded = false;
+    bool pending = false;          // an asynchronous load's status flags are not checked yet
+    int* h_status = nullptr;       // pinned host copy of d_status (deferred checks)
     // timing
     bool timing = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -126,6 +128,7 @@ static void free_all(bnreg* h)
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    if (h->h_status) cudaFreeHost(h->h_status);
 }
 
 extern "C" {
@@ -302,6 +305,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
     CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
+    CKH(cudaMallocHost(&h->h_status, sizeof(int)));
     {
         // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/512)); -ln r_j in long double
         std::vector<double2> tab9(512);
@@ -342,9 +346,9 @@ bnreg_status bnreg_set_stream(bnreg_t* h, void* stream)
     return BNREG_OK;
 }
 
-bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
+// a1-a2 enqueued on the handle's stream; the status flags land in d_status
+static bnreg_status load_enqueue(bnreg_t* h, const double* X, int32_t x_on_device)
 {
-    if (!h || !X) return fail(BNREG_E_INVAL, "NULL handle or X");
     const Plan& P = h->plan;
     const size_t nm = (size_t)P.n * P.m;
     const double* src = X;
@@ -360,13 +364,54 @@ bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
     } else {
         CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
     }
-    int status = 0;
-    CK(cudaMemcpyAsync(&status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(stream_wait(h->stream));
+    CK(cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    h->ran = false;
+    return BNREG_OK;
+}
+
+// the status flags of the last load, once the stream has passed it
+static bnreg_status load_status(bnreg_t* h)
+{
+    const int status = *h->h_status;
+    h->pending = false;
+    if (status & 6) {
+        h->loaded = false;
+        if (status & 2) return fail(BNREG_E_NONFINITE, "X contains NaN or Inf");
+        return fail(BNREG_E_RANK, "data is rank deficient (|r_jj| <= 1e-12 max column norm)");
+    }
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
+{
+    if (!h || !X) return fail(BNREG_E_INVAL, "NULL handle or X");
     h->loaded = false;
-    if (status & 2) return fail(BNREG_E_NONFINITE, "X contains NaN or Inf");
-    if (status & 4) return fail(BNREG_E_RANK, "data is rank deficient (|r_jj| <= 1e-12 max column norm)");
+    bnreg_status s = load_enqueue(h, X, x_on_device);
+    if (s != BNREG_OK) return s;
+    CK(stream_wait(h->stream));
     h->loaded = true;
+    return load_status(h);
+}
+
+bnreg_status bnreg_load_async(bnreg_t* h, const double* X, int32_t x_on_device)
+{
+    if (!h || !X) return fail(BNREG_E_INVAL, "NULL handle or X");
+    bnreg_status s = load_enqueue(h, X, x_on_device);
+    if (s != BNREG_OK) {
+        h->loaded = false;
+        return s;
+    }
+    h->loaded = true;      // provisionally: the flags are checked by the next synchronous call
+    h->pending = true;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_sync(bnreg_t* h)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    CK(stream_wait(h->stream));
+    CK(cudaGetLastError());
+    if (h->pending) return load_status(h);
     return BNREG_OK;
 }
 
@@ -376,7 +421,6 @@ bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev)
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
     const int m = h->plan.m;
     CK(cudaMemcpyAsync(R_dev, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(stream_wait(h->stream));
     return BNREG_OK;
 }
 
@@ -385,8 +429,9 @@ bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev)
     if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
     const int m = h->plan.m;
     CK(cudaMemcpyAsync(h->d_root, R_dev, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(stream_wait(h->stream));
     h->loaded = true;
+    h->pending = false;    // the sender checked its data
+    h->ran = false;
     return BNREG_OK;
 }
 
@@ -496,7 +541,10 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
                 nodes = ch;
             }
         } else {
-            CK(launch_tree_direct(h->d_root, h->d_nodes[0], P.m, P.L1, P.bh, P.p, P.k, st));
+            // multi-GPU: only the nodes above this rank's work items (its two selector patterns)
+            const uint32_t t0 = (uint32_t)P.rank, t1 = ((1u << P.r) - 1u) ^ (uint32_t)P.rank;
+            CK(launch_tree_direct(h->d_root, h->d_nodes[0], P.m, P.L1, P.bh, P.p, P.k, P.world > 1 ? P.r : 0, t0, t1,
+                                  st));
             nodes = h->d_nodes[0];
         }
     }
@@ -550,8 +598,11 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         CK(launch_walk(T, C.grid, st));
     }
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
+    // the handle keeps its own copy of the best masks whatever the caller's target
+    // (bnreg_coefficients with masks NULL reads it)
     CK(launch_best_reduce(h->d_part_bic, h->d_part_mask, h->nparts, P.m,
-                          bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask, st));
+                          bb_dev ? bb_dev : h->d_best_bic, bm_dev ? bm_dev : h->d_best_mask,
+                          bm_dev ? h->d_best_mask : nullptr, st));
     if (h->timing) CK(cudaEventRecord(h->ev[3], st));
     h->ran = true;
     return BNREG_OK;
@@ -583,6 +634,10 @@ static bnreg_status run_sync(bnreg_t* h, double* out_rss, double* out_bic, doubl
         CK(cudaMemcpyAsync(best_bic, h->d_best_bic, m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(stream_wait(h->stream));
     CK(cudaGetLastError());
+    if (h->pending) {
+        const bnreg_status ls = load_status(h);
+        if (ls != BNREG_OK) return ls;
+    }
     return collect_timing(h);
 }
 
@@ -628,8 +683,19 @@ bnreg_status bnreg_best_subsets(bnreg_t* h, const double* scores, int64_t stride
     if (!h || !scores || !best_score || !best_mask) return fail(BNREG_E_INVAL, "NULL argument");
     if (stride < 1) return fail(BNREG_E_INVAL, "stride must be >= 1");
     if (h->plan.world != 1) return fail(BNREG_E_INVAL, "bnreg_best_subsets needs the whole table (world 1)");
-    if (stride != 1 && (const void*)scores == (const void*)best_score)
-        return fail(BNREG_E_INVAL, "best_score may alias scores only with stride 1");
+    {
+        // the passes read and write in place across CTAs: an output may alias the scores
+        // only exactly (best_score == scores, stride 1); any other overlap races
+        const uintptr_t F = (uintptr_t)h->plan.local_families;
+        const uintptr_t s0 = (uintptr_t)scores, s1 = s0 + ((uintptr_t)stride * (F - 1) + 1) * sizeof(double);
+        const uintptr_t b0 = (uintptr_t)best_score, b1 = b0 + F * sizeof(double);
+        const uintptr_t m0 = (uintptr_t)best_mask, m1 = m0 + F * sizeof(uint32_t);
+        const bool exact = stride == 1 && (const void*)scores == (const void*)best_score;
+        if (!exact && b0 < s1 && s0 < b1)
+            return fail(BNREG_E_INVAL, "best_score overlaps scores (allowed only as best_score == scores with stride 1)");
+        if (m0 < s1 && s0 < m1) return fail(BNREG_E_INVAL, "best_mask overlaps scores");
+        if (m0 < b1 && b0 < m1) return fail(BNREG_E_INVAL, "best_mask overlaps best_score");
+    }
     CK(launch_bps(scores, stride, h->plan.m, best_score, best_mask, h->stream));
     return BNREG_OK;
 }
@@ -695,6 +761,18 @@ bnreg_status bnreg_best_merge(int32_t m, int32_t nparts, const uint32_t* masks, 
         if (out_mask) out_mask[v] = bm;
         if (out_bic) out_bic[v] = bb;
     }
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_best_merge_async(bnreg_t* h, int32_t nparts, const uint32_t* masks_dev, const double* bics_dev,
+                                    int64_t row_bytes, uint32_t* out_mask_dev, double* out_bic_dev)
+{
+    if (!h || nparts < 1 || !masks_dev || !bics_dev || !out_mask_dev || !out_bic_dev || row_bytes < 0 ||
+        (row_bytes & 7) || (row_bytes > 0 && row_bytes < 8 * (int64_t)h->plan.m))
+        return fail(BNREG_E_INVAL, "bad arguments");
+    // the same deterministic G14 reduction as the per-warp partials (one CTA per child)
+    CK(launch_best_reduce(bics_dev, masks_dev, nparts, h->plan.m, out_bic_dev, out_mask_dev, nullptr, h->stream,
+                          (size_t)row_bytes));
     return BNREG_OK;
 }
 

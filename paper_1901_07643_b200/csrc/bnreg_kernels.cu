@@ -285,7 +285,8 @@ cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2
 // tree reduction -> deterministic.
 __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restrict__ part_bic,
                                                           const uint32_t* __restrict__ part_mask, int nparts, int m,
-                                                          double* best_bic, uint32_t* best_mask)
+                                                          size_t sb_bytes, size_t sm_bytes, double* best_bic,
+                                                          uint32_t* best_mask, uint32_t* mask_copy)
 {
     __shared__ double sb[256];
     __shared__ uint32_t sm[256];
@@ -293,8 +294,8 @@ __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restri
     double bb = -__longlong_as_double(0x7ff0000000000000LL);
     uint32_t bm = 0xffffffffu;
     for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
-        double b = part_bic[(size_t)q * m + v];
-        uint32_t mk = part_mask[(size_t)q * m + v];
+        double b = ((const double*)((const char*)part_bic + (size_t)q * sb_bytes))[v];
+        uint32_t mk = ((const uint32_t*)((const char*)part_mask + (size_t)q * sm_bytes))[v];
         if (better(b, mk, bb, bm)) { bb = b; bm = mk; }
     }
     sb[threadIdx.x] = bb;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restri
     if (threadIdx.x == 0) {
         best_bic[v] = sb[0];
         best_mask[v] = sm[0];
+        if (mask_copy) mask_copy[v] = sm[0];   // the handle's copy (bnreg_coefficients after an async run)
     }
 }
 
@@ -349,9 +351,12 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
 }
 
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
-                               double* best_bic, uint32_t* best_mask, cudaStream_t st)
+                               double* best_bic, uint32_t* best_mask, uint32_t* mask_copy, cudaStream_t st,
+                               size_t row_bytes)
 {
-    best_reduce_kernel<<<m, 256, 0, st>>>(part_bic, part_mask, nparts, m, best_bic, best_mask);
+    const size_t sb = row_bytes ? row_bytes : (size_t)m * sizeof(double);
+    const size_t sm = row_bytes ? row_bytes : (size_t)m * sizeof(uint32_t);
+    best_reduce_kernel<<<m, 256, 0, st>>>(part_bic, part_mask, nparts, m, sb, sm, best_bic, best_mask, mask_copy);
     return cudaGetLastError();
 }
 

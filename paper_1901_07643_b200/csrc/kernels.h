@@ -53,8 +53,9 @@ struct SeedParams {
 __host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw);
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st);
 // the seed tree's nodes at depth L1 in one launch (one warp per node, derived from the root)
-cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
-                               cudaStream_t st);
+// rsel > 0: only the nodes under this rank's selector patterns t0, t1 (low rsel levels)
+cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k, int rsel,
+                               uint32_t t0, uint32_t t1, cudaStream_t st);
 
 // walk kernel: 2^lw = 8 lockstep workers per warp, gang of 2^g warps per CTA; the back
 // slots' walk state in TMEM (walk_tmem_cols per CTA), the free slots' in shared memory
@@ -74,7 +75,8 @@ cudaError_t launch_gram_chol(const double* Xr, int64_t n, int m, double* G, doub
 cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
                               cudaStream_t st);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
-                               double* best_bic, uint32_t* best_mask, cudaStream_t st);
+                               double* best_bic, uint32_t* best_mask, uint32_t* mask_copy, cudaStream_t st,
+                               size_t row_bytes = 0);   // bytes between rows (0: dense m-entry rows)
 
 // best parent set within every candidate set (subset-max transform of a score column)
 cudaError_t launch_bps(const double* scores, int64_t stride, int m, double* out_s, uint32_t* out_m, cudaStream_t st);

@@ -80,15 +80,20 @@ __device__ __forceinline__ void snapshot_sq(const double* A, int SAq, int sn, in
 // tree applies: a level's variable in F stays at the front and is dropped, one
 // not in F is bubbled behind the remaining tree levels, the warp variables and
 // the free block).  Output: m x m row-major, top-left sn x sn in position order.
+// With a rank selector (rsel > 0, multi-GPU), only the nodes whose low rsel
+// levels match one of the rank's two patterns t0, t1 are derived (the rank's
+// work items lie below them): warp q takes node ((q >> 1) << rsel) | t_{q & 1}.
 __global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restrict__ root, double* __restrict__ nodes,
-                                                          int m, int L1, int bh, int p, int k)
+                                                          int m, int L1, int bh, int p, int k, int rsel, uint32_t t0,
+                                                          uint32_t t1)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
-    const uint32_t nid = blockIdx.x * (blockDim.x >> 5) + wib;
-    if (nid >= (1u << L1)) return;
+    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib;
+    const uint32_t nid = rsel > 0 ? (((q >> 1) << rsel) | ((q & 1u) ? t1 : t0)) : q;
+    if ((rsel > 0 ? (q >> 1) << rsel : q) >= (1u << L1)) return;
     if (lane < m)
         for (int r = 0; r < m; ++r) A[r * SAq + lane] = root[r * m + lane];
     __syncwarp();
@@ -112,15 +117,16 @@ __global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restri
     (void)sn;
 }
 
-cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k,
-                               cudaStream_t st)
+cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1, int bh, int p, int k, int rsel,
+                               uint32_t t0, uint32_t t1, cudaStream_t st)
 {
     if (L1 <= 0) return cudaSuccess;
     const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
-    const unsigned n = 1u << L1;
+    if (rsel > L1) rsel = 0;                       // the selector is below the global tree: all nodes
+    const unsigned n = rsel > 0 ? 2u << (L1 - rsel) : 1u << L1;
     cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tree_direct_kernel<<<(n + 3) / 4, 128, smem, st>>>(root, nodes, m, L1, bh, p, k);
+    tree_direct_kernel<<<(n + 3) / 4, 128, smem, st>>>(root, nodes, m, L1, bh, p, k, rsel, t0, t1);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,7 @@ def _check_full(X, opt=None, o2=False, threads=0, pairs=False):
     assert np.array_equal(bm, om), f"argmax mismatch: {bm} vs {om}"
     np.testing.assert_allclose(bb, ob, atol=BIC_ATOL)
     h.close()
+    _check_full.best = (bm, bb)
     return rss, bic
 
 
@@ -145,6 +146,8 @@ def test_cfg3_collinear_full_o2_and_o1_sample():
     meta = {}
     X = datagen.config_data(3, meta=meta)
     rss, bic = _check_full(X, o2=True)
+    from test_gpu_fullsize import check_argmax_golden
+    check_argmax_golden(3, *_check_full.best)     # the committed oracle-only golden (G14, gaps >= 3.2e-5)
     Xc = oracle.centre(X)
     m = 20
     i, j = meta["pair"]
@@ -505,6 +508,42 @@ def test_best_subsets_errors():
         h.best_subsets(t, 0, t, k)
     with pytest.raises(bn.BnregError):
         h.best_subsets(t, 2, t, k)                     # aliasing needs stride 1
+    # the record table: best_score = the records themselves overlaps the BIC column (stride 2)
+    F = h.num_families()
+    rec = torch.empty((F, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(bn.BnregError):
+        h.best_subsets(rec.data_ptr() + 8, 2, rec, k)
+    with pytest.raises(bn.BnregError):
+        h.best_subsets(t, 1, torch.empty_like(t), t)   # best_mask over the scores
+    with pytest.raises(bn.BnregError):
+        h.best_subsets(t, 1, t.data_ptr() + 8 * (F // 2), k)   # partial alias
+    h.close()
+
+
+def test_coefficients_after_async_run():
+    """bnreg_coefficients(masks=NULL) uses the per-child best of the last run even when
+    that run wrote its best into a caller's device array (bnreg_run_async /
+    bnreg_run_pairs_async), and refuses after new data is loaded (no stale sets)."""
+    import torch
+    bn = _bn()
+    X = datagen.config_data(2)
+    n, m = X.shape
+    h = bn.Bnreg.create(X)
+    F = h.num_families()
+    bm_d = torch.zeros(m, dtype=torch.int32, device="cuda")
+    bb_d = torch.zeros(m, dtype=torch.float64, device="cuda")
+    rec = torch.empty((F, 2), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    h.run_pairs_async(rec, bm_d, bb_d)
+    beta_none = h.coefficients(None)
+    bm = bm_d.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(beta_none, h.coefficients(bm))
+    _, refb = oracle.table(oracle.centre(X))
+    om, _ = oracle.best(refb, m)
+    np.testing.assert_array_equal(bm, om)
+    h.load(X)
+    with pytest.raises(bn.BnregError):
+        h.coefficients(None)
     h.close()
 
 

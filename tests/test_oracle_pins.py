@@ -220,6 +220,97 @@ def test_reduced_oracle_matches_o1():
     np.testing.assert_allclose(b, a, rtol=1e-10)
 
 
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_reduced_oracle_matches_o1_1e5(cfg):
+    """O2 must match O1 on >= 1e5 seeded families per config before its
+    full-table results (cfg3 parity, the cfg4 full-table comparison, the cfg4/cfg5 argmax
+    goldens) are trusted.  Same tolerance as the GPU bar (RSS relative 1e-9); at cfg3 also
+    2000 families that hold both members of the near-collinear pair (G23), where the
+    columns' conditioning is worst."""
+    X = datagen.config_data(cfg)
+    n, m = X.shape
+    Xc = oracle.centre(X)
+    R0 = oracle.qr_r(Xc)
+    idx = datagen.sample_indices(m, 100_000, seed=40 + cfg)
+    a = oracle.rss_indices(Xc, idx)
+    b = oracle.rss_reduced_indices(R0, idx)
+    assert (np.abs(b - a) / a).max() <= 1e-9
+    if cfg == 3:
+        meta = {}
+        datagen.config_data(cfg, meta=meta)
+        i, j = meta["pair"]
+        rng = np.random.default_rng(7)
+        fam = []
+        while len(fam) < 2000:
+            v = int(rng.integers(0, m))
+            if v in (i, j):
+                continue
+            S = int(rng.integers(0, 1 << m)) & ~(1 << v)
+            fam.append(oracle.index(m, v, S | (1 << i) | (1 << j)))
+        fam = np.array(fam, dtype=np.int64)
+        a = oracle.rss_indices(Xc, fam)
+        b = oracle.rss_reduced_indices(R0, fam)
+        assert (np.abs(b - a) / a).max() <= 1e-9
+
+
+def test_best_reduced_equals_table_argmax():
+    """oracle.best_reduced (streamed O2 + BIC + G14, no table) == oracle.best over the O1
+    table (cfg1, cfg2), and its runner-up == the G14 best of the table with the winner
+    removed; on a table full of exact ties (integer data, duplicated columns) the G14
+    order decides."""
+    for cfg in (1, 2):
+        X = datagen.config_data(cfg)
+        n, m = X.shape
+        Xc = oracle.centre(X)
+        _, bic = oracle.table(Xc)
+        bm, bb = oracle.best(bic, m)
+        d = oracle.best_reduced(oracle.qr_r(Xc), n)
+        np.testing.assert_array_equal(d["best_mask"], bm)
+        assert np.abs(d["best_bic"] - bb).max() <= 1e-9
+        for v in range(m):
+            blk = bic[v << (m - 1):(v + 1) << (m - 1)].copy()
+            blk[oracle.index(m, v, int(bm[v])) - (v << (m - 1))] = -np.inf
+            sm, sb = oracle.best(np.concatenate([np.full(v << (m - 1), -np.inf), blk,
+                                                 np.full((m - 1 - v) << (m - 1), -np.inf)]), m)
+            assert d["second_mask"][v] == sm[v] and abs(d["second_bic"][v] - sb[v]) <= 1e-9
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_best_golden_pinned_to_o1(cfg, golden_dir):
+    """The committed argmax goldens (tests/golden/make_best_golden.py: O2 over the full
+    table) checked against O1 where O1 is affordable: each child's best RSS equals O1's,
+    its BIC is the formula of that RSS, and no single add/remove neighbour of the best set
+    scores higher under O1 (a necessary condition of the global argmax)."""
+    path = os.path.join(golden_dir, f"best_cfg{cfg}.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    g = json.load(open(path))
+    X = datagen.config_data(cfg)
+    n, m = X.shape
+    assert (g["m"], g["n"], g["families"]) == (m, n, m << (m - 1))
+    Xc = oracle.centre(X)
+    idx, nb = [], []
+    for r in g["children"]:
+        v, S = r["child"], r["best_mask"]
+        idx.append(oracle.index(m, v, S))
+        for u in range(m):
+            if u != v:
+                nb.append((v, S ^ (1 << u)))
+    rss = oracle.rss_indices(Xc, np.array(idx, dtype=np.int64))
+    for r, x in zip(g["children"], rss):
+        # RSS at the north-star bar; the BIC is the formula of the golden's own RSS (at
+        # cfg3 the pair's families have RSS ~ n 1e-12: O1 and O2 each sit ~2e-10 from a
+        # 50-digit Gram/LU value, so O1 vs O2 can differ by ~1e-6 in BIC, G15/G16)
+        assert abs(r["best_rss"] - x) <= 1e-9 * x
+        assert r["best_bic"] == oracle.bic(r["best_rss"], n, bin(r["best_mask"]).count("1"))
+        assert r["gap"] > 0 and r["second_mask"] != r["best_mask"]
+    nidx = np.array([oracle.index(m, v, S) for v, S in nb], dtype=np.int64)
+    nr = oracle.rss_indices(Xc, nidx)
+    best_of = {r["child"]: r["best_bic"] for r in g["children"]}
+    for (v, S), x in zip(nb, nr):
+        assert oracle.bic(x, n, bin(S).count("1")) <= best_of[v] + 1e-5
+
+
 def test_bic_spec_value():
     """SPEC.md:239: n=50, rss=50 -> log-likelihood -25(1 + ln 2 pi) = -70.946926660;
     with no parents BIC equals the log-likelihood; each parent costs ln(n)/2."""
