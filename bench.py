@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--k", type=int, default=0, help="free block size (0 = library default)")
     ap.add_argument("--lw", type=int, default=-1, help="seed-tree levels derived in-warp (-1 = default)")
-    ap.add_argument("--wpc", type=int, default=0)
+    ap.add_argument("--pack-bits", type=int, default=0, help="log2 lockstep workers per warp (0 = library default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--layout", default="pairs", choices=["pairs", "tables"],
@@ -322,7 +322,7 @@ def bench_ours(args):
     dev = torch.device("cuda", local)
     X = datagen.config_data(args.config, args.seed)
     n, m = X.shape
-    opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, warps_per_cta=args.wpc)
+    opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, pack_bits=args.pack_bits)
     h = bn.Bnreg(n, m, opt)
     plan = bn.bnreg_plan_query(m, n, opt)
     # one explicit (non-legacy) stream for torch, NCCL ordering and the handle: the timing

@@ -61,7 +61,10 @@ typedef struct {
     int32_t levels_in_warp;   /* seed-tree levels each warp derives itself; -1 = auto (4) */
     int32_t world;            /* ranks sharing the walk (power of two); 0 or 1 = single */
     int32_t rank;             /* this rank, 0 <= rank < world                             */
-    int32_t warps_per_cta;    /* reserved (a traversal CTA is one gang of 2^g warps)      */
+    int32_t pack_bits;        /* log2 of the lockstep workers a walk warp runs: 0 = auto
+                                 (3: 8 workers x 4 lanes, gangs of 4 warps); 5 = 32
+                                 workers, one lane each (walk7: a warp's record store
+                                 writes one whole 512 B region; slower)     */
     int32_t ctas_per_sm;      /* traversal CTAs per SM; 0 = occupancy maximum             */
 } bnreg_options;
 

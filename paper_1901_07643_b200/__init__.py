@@ -16,7 +16,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbnreg.so")
+# BNREG_LIB: load a variant build (e.g. tools/variants.sh A/B builds, the K8 debug build)
+# from its own path; the in-tree libbnreg.so is never overwritten by a variant
+LIB_PATH = os.environ.get("BNREG_LIB") or os.path.join(_HERE, "libbnreg.so")
 
 OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE = range(7)
 SCORE_BIC, SCORE_AIC, SCORE_LOGLIK = 0, 1, 2
@@ -42,11 +44,13 @@ class BnregError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("free_vars", ctypes.c_int32), ("levels_in_warp", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+                ("pack_bits", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
 
 
-def options(free_vars=0, levels_in_warp=-1, world=1, rank=0, warps_per_cta=0, ctas_per_sm=0):
-    return Options(free_vars, levels_in_warp, world, rank, warps_per_cta, ctas_per_sm)
+def options(free_vars=0, levels_in_warp=-1, world=1, rank=0, pack_bits=0, ctas_per_sm=0):
+    """bnreg_options: pack_bits 0 = auto (3: 8 lockstep workers x 4 lanes per warp, gangs of
+    4 warps), 5 = walk7 (32 workers per warp, one lane each)."""
+    return Options(free_vars, levels_in_warp, world, rank, pack_bits, ctas_per_sm)
 
 
 _lib = None

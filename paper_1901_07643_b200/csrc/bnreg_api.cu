@@ -104,12 +104,16 @@ struct bnreg {
     unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
     size_t wsteps_len = 0;         // steps per class table
+    // walk7 (32 lockstep workers per warp; P.lw == 5)
+    bool w7 = false;
+    int w7_warps = 4, w7_TB = 16, w7_KA = 8, w7_nbmax = 0;
+    unsigned long long w7_sblk = 0;     // doubles per item of the seed blocks
 };
 
 static bnreg_options defaults(const bnreg_options* o)
 {
     bnreg_options d{};
-    d.free_vars = 0; d.levels_in_warp = -1; d.world = 1; d.rank = 0; d.warps_per_cta = 0; d.ctas_per_sm = 0;
+    d.free_vars = 0; d.levels_in_warp = -1; d.world = 1; d.rank = 0; d.pack_bits = 0; d.ctas_per_sm = 0;
     if (o) {
         d = *o;
         if (d.world <= 0) d.world = 1;
@@ -155,7 +159,7 @@ bnreg_status bnreg_plan_query(int32_t m, int64_t n, const bnreg_options* o, int6
     if (!info) return fail(BNREG_E_INVAL, "info is NULL");
     bnreg_options d = defaults(o);
     try {
-        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank, d.pack_bits);
         info[0] = P.k; info[1] = P.b; info[2] = P.p; info[3] = P.bh; info[4] = P.L1; info[5] = P.LW;
         info[6] = (int64_t)P.packs.size(); info[7] = (int64_t)P.sched.size(); info[8] = P.local_families;
         info[9] = P.total_families; info[10] = (int64_t)walk_cta_smem(P.m, P.k, P.m, P.g, P.lw) >> P.g; info[11] = P.r;
@@ -170,7 +174,7 @@ int64_t bnreg_plan_packs(int32_t m, int64_t n, const bnreg_options* o, uint32_t*
 {
     bnreg_options d = defaults(o);
     try {
-        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank, d.pack_bits);
         if (out)
             for (int64_t i = 0; i < (int64_t)P.packs.size() && i < cap; ++i) out[i] = P.packs[i];
         return (int64_t)P.packs.size();
@@ -187,7 +191,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     bnreg_options d = defaults(o);
     Plan P;
     try {
-        P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank, d.pack_bits);
     } catch (std::exception& e) {
         return fail(BNREG_E_INVAL, e.what());
     }
@@ -231,10 +235,44 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     if (!P.packs.empty())
         CKH(cudaMemcpy(h->d_packs, P.packs.data(), P.packs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     h->wpc = 1 << P.g;                                    // one CTA = one gang of lockstep warps
-    (void)d.warps_per_cta;
     if (P.local_families > (int64_t)0xffffffffLL)
         return bail(fail(BNREG_E_INVAL, "this rank's table exceeds 2^32 entries (use more ranks)"));
-    {
+    if (P.lw == 5) {
+        // walk7: one launch over every item; one CTA of up to 4 independent warps per SM (one per
+        // TMEM lane quarter); back slots beyond the TMEM capacity TB go to shared memory
+        h->w7 = true;
+        const int k = P.k;
+        h->w7_TB = std::min(20, 4 * (32 / k));
+        h->w7_nbmax = P.b;
+        const int so = std::max(0, h->w7_nbmax - h->w7_TB);
+        if (so > 4) return bail(fail(BNREG_E_INVAL, "too many back slots for the walk's state (lower m or raise k)"));
+        h->w7_KA = k + so;
+        int warps = 4;
+        while (warps > 0 && walk7_cta_smem(k, h->w7_KA, k + h->w7_nbmax, warps) > (size_t)227 * 1024) --warps;
+        if (warps < 1) return bail(fail(BNREG_E_NOMEM, "walk7 state does not fit in shared memory"));
+        h->w7_warps = warps;
+        h->w7_sblk = (unsigned long long)(k + h->w7_nbmax) * k * 32 + (unsigned long long)h->w7_nbmax * 32;
+        const int64_t ni = (int64_t)P.packs.size();
+        bnreg::WalkClass c;
+        c.begin = 0; c.end = (int)ni; c.S_alloc = 0; c.jbmax = 0;
+        c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms, (ni + warps - 1) / warps));
+        c.part_base = 0;
+        h->nparts = c.grid * warps;
+        h->classes.push_back(c);
+        h->seed_off.push_back(0);
+        CKH(cudaMalloc(&h->d_seeds, std::max<size_t>((size_t)ni * h->w7_sblk * sizeof(double), 16)));
+        CKH(cudaMalloc(&h->d_counters, sizeof(unsigned)));
+        const auto recs = step_records(P.k, P.sched);
+        h->wsteps_len = recs.size();
+        auto tb = walk_step_table(recs, P.k, h->w7_KA, 32);
+        tb.push_back(WalkStep{});
+        CKH(cudaMalloc(&h->d_wsteps, tb.size() * sizeof(WalkStep)));
+        CKH(cudaMemcpy(h->d_wsteps, tb.data(), tb.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
+        if (getenv("BNREG_VERBOSE"))
+            fprintf(stderr, "walk7: items %lld grid %d warps %d TB %d KA %d nbmax %d smem %zu seed blocks %.2f GB\n",
+                    (long long)ni, c.grid, warps, h->w7_TB, h->w7_KA, h->w7_nbmax,
+                    walk7_cta_smem(k, h->w7_KA, k + h->w7_nbmax, warps), ni * h->w7_sblk * 8.0 / 1e9);
+    } else {
         // walk kernel: items are sorted costliest first = most walk slots first
         // (a gang's slots: m - |F among its tree levels|).  A launch ("class") takes
         // the items whose warps need the same TMEM allocation (back entries per lane
@@ -307,16 +345,16 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
     CKH(cudaMallocHost(&h->h_status, sizeof(int)));
     {
-        // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/512)); -ln r_j in long double
-        std::vector<double2> tab9(512);
-        for (int j = 0; j < 512; ++j) {
-            long double t = 1.0L + ((long double)j + 0.5L) / 512.0L;
+        // (r_j, -ln r_j), r_j = fl(1 / (1 + (j + 1/2)/2^kLnBits)); -ln r_j in long double
+        std::vector<double2> tab9(kLnEntries);
+        for (int j = 0; j < kLnEntries; ++j) {
+            long double t = 1.0L + ((long double)j + 0.5L) / (long double)kLnEntries;
             double r = (double)(1.0L / t);
             tab9[j].x = r;
             tab9[j].y = (double)(-logl((long double)r));
         }
-        CKH(cudaMalloc(&h->d_lntab9, 512 * sizeof(double2)));
-        CKH(cudaMemcpy(h->d_lntab9, tab9.data(), 512 * sizeof(double2), cudaMemcpyHostToDevice));
+        CKH(cudaMalloc(&h->d_lntab9, kLnEntries * sizeof(double2)));
+        CKH(cudaMemcpy(h->d_lntab9, tab9.data(), kLnEntries * sizeof(double2), cudaMemcpyHostToDevice));
     }
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
 #undef CKH
@@ -478,7 +516,7 @@ bnreg_status bnreg_plan_shard_ranges(int32_t m, int64_t n, const bnreg_options* 
     if (!count) return fail(BNREG_E_INVAL, "NULL argument");
     bnreg_options d = defaults(o);
     try {
-        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank, d.pack_bits);
         shard_ranges_of(P, count, starts, lens);
     } catch (std::exception& e) {
         return fail(BNREG_E_INVAL, e.what());
@@ -490,7 +528,7 @@ int64_t bnreg_plan_local_index(int32_t m, int64_t n, const bnreg_options* o, int
 {
     bnreg_options d = defaults(o);
     try {
-        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank);
+        Plan P = make_plan(m, n, d.free_vars, d.levels_in_warp, d.world, d.rank, d.pack_bits);
         if (g < 0 || g >= P.total_families) return -1;
         return local_index(P, g);
     } catch (std::exception& e) {
@@ -581,7 +619,12 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     SP.item_begin = 0;
     SP.item_end = (int)P.packs.size();
     SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = h->d_seeds;
-    CK(launch_seed(SP, st));
+    if (h->w7) {
+        SP.TB = h->w7_TB; SP.nbmax = h->w7_nbmax; SP.sblk = h->w7_sblk;
+        CK(launch_seed7(SP, st));
+    } else {
+        CK(launch_seed(SP, st));
+    }
     if (h->timing) CK(cudaEventRecord(h->ev[1], st));
     // a6-a11: the walk, one launch per shared-memory class
     for (size_t c = 0; c < h->classes.size(); ++c) {
@@ -595,7 +638,12 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         T.part_base = C.part_base;
         T.wsteps = h->d_wsteps + c * h->wsteps_len;
         T.seeds = h->d_seeds + h->seed_off[c];
-        CK(launch_walk(T, C.grid, st));
+        if (h->w7) {
+            T.KA = h->w7_KA; T.TB = h->w7_TB; T.nbmax = h->w7_nbmax; T.sblk = h->w7_sblk;
+            CK(launch_walk7(T, C.grid, h->w7_warps, st));
+        } else {
+            CK(launch_walk(T, C.grid, st));
+        }
     }
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
     // the handle keeps its own copy of the best masks whatever the caller's target

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(128) tree_level_kernel(const double* __restric
 __global__ void debug_ln_kernel(const double* x, double* y, int64_t n, const double2* tab)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) y[i] = fast_ln9(x[i], tab);   // the walk kernel's log (512-entry table)
+    if (i < n) y[i] = fast_ln9(x[i], tab);   // the walk kernel's log (kLnEntries-entry table)
 }
 
 cudaError_t launch_debug_ln(const double* x, double* y, int64_t n, const double2* tab, cudaStream_t st)

@@ -58,31 +58,45 @@ __device__ __forceinline__ void givens_fr(double a, double b, double& c, double&
 // user id of seed-tree level l (plan.h hv_id): top ids first, the gang ids last
 __device__ __forceinline__ int hv_of(int l, int m, int gs, int fv0) { return l < gs ? m - 1 - l : fv0 - 1 - (l - gs); }
 
-// Constants of the fast log (compile-time literals: the compiler keeps them in
-// its constant bank and uses them as DFMA operands directly).
-constexpr double kLnC0 = -0.5, kLnC1 = -0.25, kLnC2 = 1.0 / 3.0;
+// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top kLnBits bits
+// of f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/2^kLnBits)
+// (host, long double); u = f r_j - 1 (|u| <= 2^-(kLnBits+1));
+// ln x = e ln2 + (-ln r_j) + log1p(u), log1p(u) = u q(u):
+//   BNREG_LN_DEG 4 (512 entries): q = 1 - u/2 + u^2/3 - u^3/4, truncation u^5/5 < 2e-16;
+//   BNREG_LN_DEG 3 (1024 entries): q = 1 + u(-1/2 + u/3), truncation u^4/4 < 1.5e-14
+//   (BIC error (n/2) 1.5e-14 <= 7.5e-11 at n = 1e4, against the 1e-6 bar).
+// Constants are compile-time literals: the compiler keeps them in its constant bank and
+// uses them as DFMA operands directly.
+// (BNREG_LN_DEG, kLnBits, kLnEntries: kernels.h)
 constexpr double kLn2 = 6.93147180559945309417e-01;   // correctly rounded: e * ln2 in one FMA
                                                         // (error |e| * 2.3e-17 <= 2.4e-14 for |e| <= 1023)
 
-// Fast natural log for the BIC (a9).  x = 2^e f, f in [1,2); j = top 9 bits of
-// f's mantissa; tab[j] = (r_j, -ln r_j) with r_j ~ 1/(1 + (j+0.5)/512) (host,
-// long double); u = f r_j - 1 (|u| <= 9.8e-4);  ln x = e ln2 + (-ln r_j) + log1p(u),
-// log1p(u) = u q(u) with q the degree-3 Taylor polynomial (truncation u^5/5 <
-// 2e-16).  Absolute error ~1e-15 for normal x (tests/test_gpu_parity.py).
+__device__ __forceinline__ double ln_poly(double u, double base)
+{
+#if BNREG_LN_DEG == 3
+    const double t = fma(u, 1.0 / 3.0, -0.5);
+    const double q = fma(u, t, 1.0);
+    return fma(u, q, base);
+#else
+    const double u2 = u * u;
+    const double a = fma(u, -0.5, 1.0);
+    const double b = fma(u, -0.25, 1.0 / 3.0);
+    const double q = fma(u2, b, a);
+    return fma(u, q, base);
+#endif
+}
+
+// byte offset of the table entry of x's mantissa (16 B entries)
+__device__ __forceinline__ int ln_tab_off(int hi) { return (hi >> (16 - kLnBits)) & ((kLnEntries - 1) << 4); }
+
 __device__ __forceinline__ double fast_ln9(double x, const double2* tab)
 {
     const int hi = __double2hiint(x), lo = __double2loint(x);
     const int e = (hi >> 20) - 1023;
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 t = *(const double2*)((const char*)tab + ((hi >> 7) & 0x1ff0));
-    const double ed = (double)e;
-    const double base = fma(ed, kLn2, t.y);
-    const double u = fma(f, t.x, -1.0);
-    const double u2 = u * u;
-    const double a = fma(u, kLnC0, 1.0);
-    const double b = fma(u, kLnC1, kLnC2);
-    const double q = fma(u2, b, a);
-    return fma(u, q, base);
+    const double2 t = *(const double2*)((const char*)tab + ln_tab_off(hi));
+    const double base = fma((double)e, kLn2, t.y);
+    return ln_poly(fma(f, t.x, -1.0), base);
 }
 
 // fast_ln9 with the table addressed in the shared window (tab = shared address).
@@ -92,15 +106,9 @@ __device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
     const int e = (hi >> 20) - 1023;
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     double tx, ty;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ((hi >> 7) & 0x1ff0)));
-    const double ed = (double)e;
-    const double base = fma(ed, kLn2, ty);
-    const double u = fma(f, tx, -1.0);
-    const double u2 = u * u;
-    const double a = fma(u, kLnC0, 1.0);
-    const double b = fma(u, kLnC1, kLnC2);
-    const double q = fma(u2, b, a);
-    return fma(u, q, base);
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ln_tab_off(hi)));
+    const double base = fma((double)e, kLn2, ty);
+    return ln_poly(fma(f, tx, -1.0), base);
 }
 
 // BIC (reading G5): -(n/2) ln(RSS/n) - (n/2)(1 + ln 2pi) - (|S|/2) ln n

@@ -6,6 +6,14 @@
 
 namespace bnr {
 
+// fast log of the BIC epilogue (device.cuh fast_ln9): polynomial degree and table size
+#ifndef BNREG_LN_DEG
+#define BNREG_LN_DEG 4
+#endif
+constexpr int kMaxFreeWalk7 = 8;   // walk7: free variables per worker (a step's free list = one u32 of nibbles)
+constexpr int kLnBits = BNREG_LN_DEG == 3 ? 10 : 9;
+constexpr int kLnEntries = 1 << kLnBits;
+
 // Parameters of the fused traversal kernel (K4 seed derivation + K5 walk +
 // a8 harvest + a9 BIC + a10 store + a11 per-child running best).
 struct TravParams {
@@ -23,7 +31,7 @@ struct TravParams {
     uint32_t* part_mask;        // [warps of all launches][m] per-warp best mask
     double mhalf_n;             // -n/2
     double tiny_bic;            // lower bound of the BIC (fast log) of any RSS <= 1e-300 (G13 candidates)
-    const double2* lntab9;      // fast-log table (512 x (r_j, -ln r_j))
+    const double2* lntab9;      // fast-log table (kLnEntries x (r_j, -ln r_j))
     double Kc[33];              // BIC constant per parent-set size
     int r;                      // rank-selector bits (world > 1)
     unsigned patlo;             // smaller selector pattern of this rank (non-selector children)
@@ -34,6 +42,11 @@ struct TravParams {
     const unsigned char* seeds; // this launch's seed blocks (seed kernel), one per (item, warp)
     int jbmax;                  // most back entries per lane of this launch's warps (ceil(back slots / 4))
     int tm_cols;                // TMEM columns per CTA (walk_tmem_cols(k, jbmax))
+    // walk7 (32 lockstep workers per warp, one lane each):
+    int KA;                     // shared-memory slots per free row: k free + overflow back slots
+    int TB;                     // back slots held in TMEM (512 columns / (4 k))
+    int nbmax;                  // most back slots of any item (p + tree levels)
+    unsigned long long sblk;    // doubles per item of the seed blocks (seed7 layout)
 };
 
 // seed kernel: one warp per pack derives its 2^p workers' seeds (the remaining
@@ -49,7 +62,15 @@ struct SeedParams {
     const double* nodes;                       // seed-tree nodes at depth L1
     const uint32_t* packs;
     unsigned char* seeds;
+    int TB, nbmax;                             // seed7: back slots in TMEM, most back slots of an item
+    unsigned long long sblk;                   // seed7: doubles per item
 };
+// seed7: the compact seed blocks of the 32-worker walk (R of the free rows, slot-major,
+// worker fastest, + the tail sum of squares of every back slot); one warp per item
+cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st);
+// walk7: 32 lockstep workers per warp, one CTA of `warps` independent warps per SM
+size_t walk7_cta_smem(int k, int KA, int nslots, int warps);
+cudaError_t launch_walk7(const TravParams& P, int grid, int warps, cudaStream_t st);
 __host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw);
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st);
 // the seed tree's nodes at depth L1 in one launch (one warp per node, derived from the root)

@@ -39,7 +39,9 @@ namespace bnr {
 constexpr int kMaxM = 30;        // u32 masks, 64-bit indices; memory caps m far below
 constexpr int kMaxFree = 16;     // free vars per worker: 4-bit permutation nibbles in a u64
 constexpr int kMaxFreeWalk = 8;  // walk kernel: a step's free list (<= 8 slots) fits one u32 of nibbles, <= 2 per lane
-constexpr int kPackBits = 3;     // 8 lockstep workers per warp (walk kernel)
+constexpr int kPackBits = 3;     // default: 8 lockstep workers per warp in gangs of 4 warps (walk kernel);
+                                 // 5 = 32 workers per warp, one lane each (walk7 kernel: measured slower,
+                                 // DESIGN.md §4 "walk7")
 
 // Alg.1 GreedySwaps(m) with Eq.10's +1.
 // Returns 1-based swap positions, length 2^m - m - 1 (Eq.9).
@@ -184,7 +186,8 @@ inline int64_t pack_cost(const Plan& P, uint32_t pack)
 }
 
 // k: requested free count (0 = auto).  lw: tree levels derived in-warp (-1 = auto).
-inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
+// pack_bits: log2 lockstep workers per warp (0 = auto = kPackBits; 3 or 5).
+inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank, int pack_bits = 0)
 {
     Plan P;
     if (m < 2 || m > kMaxM) throw std::invalid_argument("m must be in [2, 30]");
@@ -198,7 +201,9 @@ inline Plan make_plan(int m, int64_t n, int k, int lw, int world, int rank)
     if (k > kMaxFreeWalk)
         throw std::invalid_argument("the walk kernel takes at most 8 free variables (k <= 8)");
     P.m = m; P.n = n; P.k = k; P.b = m - k;
-    P.lw = kPackBits;
+    if (pack_bits == 0) pack_bits = kPackBits;
+    if (pack_bits != 3 && pack_bits != 5) throw std::invalid_argument("pack_bits must be 3 or 5 (8 or 32 workers per warp)");
+    P.lw = pack_bits;
     P.p = std::min(P.lw, P.b);
     P.bh = P.b - P.p;
     // walk kernel: a CTA's 2^g warps x 2^lw workers = 32 workers = 256 B per (child, step)

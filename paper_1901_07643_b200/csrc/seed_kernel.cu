@@ -228,6 +228,132 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
     }
 }
 
+// ---------------------------------------------------------------- a5 for the 32-worker walk (walk7)
+// Seed -> compact seed7 block of worker w: R(slot, l, w) of the k free rows l for
+// every walk slot (slot-major, worker fastest: the walk reads 256 B per (slot, row)),
+// and the tail sum of squares (rows below the free block) of every back slot; the
+// walk rebuilds the suffix sums.  A warp variable in the worker's F (absent back
+// slot) gets zeros.
+__device__ __forceinline__ void snapshot7(const double* A, int SAq, int sn, int og, int k, int lane, int pos, int slot,
+                                          bool haveslot, double* blk, double* tails, int w)
+{
+    const bool mine = haveslot && pos >= og && pos < sn;
+    const bool zero = haveslot && pos < og && slot >= k;
+    double acc = 0.0;
+    const double* pa = A + (sn - 1) * SAq + lane;
+    for (int r = sn - 1; r >= og + k; --r, pa -= SAq) {
+        const double x = (mine && r <= pos) ? *pa : 0.0;
+        acc = fma(x, x, acc);
+    }
+    if ((mine || zero) && slot >= k) tails[(size_t)(slot - k) * 32 + w] = mine ? acc : 0.0;
+    for (int l = 0; l < k; ++l) {
+        const int r = og + l;
+        const double x = (mine && r <= pos) ? A[r * SAq + lane] : 0.0;
+        if (mine || zero) blk[((size_t)slot * k + l) * 32 + w] = x;
+    }
+}
+
+// One warp per item (= pack of 2^p workers, p <= 5): the node at tree depth L1, the
+// remaining tree levels, the workers' seeds along a Gray path over the warp variables.
+__global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ SeedParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int m = P.m, k = P.k, p = P.p, bh = P.bh;
+    const int fv0 = p, gs = bh;
+    const int SAq = m | 1;
+    double* const A = (double*)smem + (size_t)wib * m * SAq;
+    const int npk = P.item_end - P.item_begin;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
+        const int item = P.item_begin + q;
+        double* const blk = (double*)P.seeds + (size_t)q * P.sblk;
+        double* const tails = blk + (size_t)(k + P.nbmax) * k * 32;
+        const uint32_t pack = P.packs[item];
+        const uint32_t nid = pack & ((1u << P.L1) - 1u);
+        const int sn = m - __popc(nid);
+        {
+            const double* src = P.nodes + (size_t)nid * m * m;
+            if (lane < sn)
+                for (int r = 0; r < sn; ++r) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(A + r * SAq + lane);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + r * m + lane));
+                }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+        }
+        int pos = lane < sn ? lane : 1 << 20;
+        int myvar = -1;
+        {
+            const int nlev = bh - P.L1;
+            const int qq = lane;
+            if (qq < nlev) myvar = hv_of(P.L1 + qq, m, gs, fv0);
+            else if (qq < nlev + p) myvar = p - 1 - (qq - nlev);
+            else if (qq < nlev + p + k) myvar = fv0 + (qq - nlev - p);
+            else if (qq < sn) {
+                int cc = qq - nlev - p - k;
+                for (int l = P.L1 - 1; l >= 0; --l)
+                    if (!((pack >> l) & 1u)) {
+                        if (cc == 0) { myvar = hv_of(l, m, gs, fv0); break; }
+                        --cc;
+                    }
+            }
+        }
+        // walk slot: [free 0..k-1 | warp vars 0..p-1 | tree back set ascending id]
+        int slot = 0;
+        const bool haveslot = myvar >= 0 && !(myvar >= fv0 + k && ((pack >> (m - 1 - myvar)) & 1u));
+        if (myvar >= 0) {
+            if (myvar >= fv0 && myvar < fv0 + k) slot = myvar - fv0;
+            else if (myvar < fv0) slot = k + myvar;
+            else {
+                const uint32_t lv = ~pack & ((1u << gs) - 1u);
+                const uint32_t bmask = (uint32_t)(__brev(lv) >> (32 - m));
+                slot = k + fv0 + __popc(bmask & ((1u << myvar) - 1u));
+            }
+        }
+        int org = 0;
+        for (int l = P.L1; l < bh; ++l) {
+            if ((pack >> l) & 1u) {
+                ++org;
+                continue;
+            }
+            const int T = (bh - l - 1) + p + k;
+            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+        }
+        int wcur = P.nw - 1;
+        snapshot7(A, SAq, sn, org + p, k, lane, pos, slot, haveslot, blk, tails, wcur);
+        for (int i = 1; i < P.nw; ++i) {
+            const int j = __ffs(i) - 1;
+            const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
+            const int d = k + j;
+            if ((wcur >> j) & 1) {
+                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
+            } else {
+                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
+            }
+            wcur ^= 1 << j;
+            snapshot7(A, SAq, sn, org + __popc(wcur), k, lane, pos, slot, haveslot, blk, tails, wcur);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st)
+{
+    const int m = P.m;
+    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const int npk = P.item_end - P.item_begin;
+    if (npk <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min((npk + 3) / 4, sms * 16);
+    cudaError_t e = cudaFuncSetAttribute(seed7_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    seed7_kernel<<<grid, 128, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;

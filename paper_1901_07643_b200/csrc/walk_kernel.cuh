@@ -1,4 +1,4 @@
-// walk_kernel.cu -- the hot kernel of the bnreg path:
+// walk_kernel.cuh -- the hot kernel of the bnreg path:
 // Alg.2 workers each walk d + Upsilon(k) (Alg.1 with Eq.10's
 // +1) from their seed R, one GRC per step
 // (Eq.3-4 with reading G1), harvesting every new family from
@@ -28,11 +28,15 @@
 //     step, live in shared memory (worker-interleaved, 128 B per LDS phase).
 //     Moving the back state out of shared memory is what lets 16 warps share an
 //     SM (shared memory held 8 before).
+#pragma once
+// (included by walk_pairs.cu and walk_tables.cu, which instantiate the kernel for the
+// record layout and the two-table layouts in separate translation units)
 #include <cstdint>
 #include <cmath>
 #include <algorithm>
 #include "kernels.h"
 #include "device.cuh"
+#include "tmem.cuh"
 
 #ifndef BNREG_SYNC_EVERY
 #define BNREG_SYNC_EVERY 16  // (RSS, BIC) records: gang barrier every this many steps (a power of two;
@@ -44,96 +48,6 @@ namespace bnr {
 
 constexpr int kW = 8;          // lockstep workers per warp
 constexpr int kCS = kW * 16;   // bytes between free slots of the shared state
-
-// ---------------------------------------------------------------- tensor memory
-__device__ __forceinline__ void tm_ld4(uint32_t a, uint32_t* r)
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(a));
-}
-__device__ __forceinline__ void tm_ld8(uint32_t a, uint32_t* r)
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(a));
-}
-__device__ __forceinline__ void tm_ld16(uint32_t a, uint32_t* r)
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                 : "r"(a));
-}
-__device__ __forceinline__ void tm_ld32(uint32_t a, uint32_t* r)
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-                   "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-                   "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-                   "=r"(r[30]), "=r"(r[31])
-                 : "r"(a));
-}
-__device__ __forceinline__ void tm_st4(uint32_t a, const uint32_t* r)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(r[0]), "r"(r[1]),
-                 "r"(r[2]), "r"(r[3]));
-}
-__device__ __forceinline__ void tm_st8(uint32_t a, const uint32_t* r)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(r[0]),
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
-}
-__device__ __forceinline__ void tm_st16(uint32_t a, const uint32_t* r)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(a),
-                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
-}
-__device__ __forceinline__ void tm_st32(uint32_t a, const uint32_t* r)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-                 "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(a),
-                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-                 "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-                 "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-                 "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-// N consecutive 32-bit columns of the lane's TMEM lane (N a multiple of 4)
-template <int N>
-__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t* r)
-{
-    if constexpr (N >= 32) { tm_ld32(a, r); tm_ld<N - 32>(a + 32, r + 32); }
-    else if constexpr (N >= 16) { tm_ld16(a, r); tm_ld<N - 16>(a + 16, r + 16); }
-    else if constexpr (N >= 8) { tm_ld8(a, r); tm_ld<N - 8>(a + 8, r + 8); }
-    else if constexpr (N >= 4) { tm_ld4(a, r); tm_ld<N - 4>(a + 4, r + 4); }
-}
-template <int N>
-__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t* r)
-{
-    if constexpr (N >= 32) { tm_st32(a, r); tm_st<N - 32>(a + 32, r + 32); }
-    else if constexpr (N >= 16) { tm_st16(a, r); tm_st<N - 16>(a + 16, r + 16); }
-    else if constexpr (N >= 8) { tm_st8(a, r); tm_st<N - 8>(a + 8, r + 8); }
-    else if constexpr (N >= 4) { tm_st4(a, r); tm_st<N - 4>(a + 4, r + 4); }
-}
-// wait for the lane's outstanding tcgen05.ld, then pin the destination
-// registers behind the wait (the compiler does not know the wait defines them)
-template <int N>
-__device__ __forceinline__ void tm_wait_ld(uint32_t* r)
-{
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
-}
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ double tm_f64(const uint32_t* r) { return __hiloint2double((int)r[1], (int)r[0]); }
-__device__ __forceinline__ void tm_put(uint32_t* r, double x)
-{
-    r[0] = (uint32_t)__double2loint(x);
-    r[1] = (uint32_t)__double2hiint(x);
-}
 
 // ---------------------------------------------------------------- shared memory layout
 // Per CTA: [log table 512 x 16 B][K(s) 33 doubles] then per warp:
@@ -169,9 +83,9 @@ __host__ __device__ inline WalkLayout walk_layout(int k, int SA)
     return L;
 }
 
-constexpr int kWalkHead = 8192 + 272;   // log table + K(s) table
+constexpr int kWalkHead = 16 * kLnEntries + 272;   // log table + K(s) table
 
-size_t walk_cta_smem(int m, int k, int SA, int g, int lw)
+inline size_t walk_cta_smem_h(int m, int k, int SA, int g, int lw)
 {
     (void)m;
     (void)lw;
@@ -179,43 +93,11 @@ size_t walk_cta_smem(int m, int k, int SA, int g, int lw)
 }
 
 // TMEM columns a CTA allocates: a warp's back state is k rows x JB slots x 4 columns
-int walk_tmem_cols(int k, int jbmax)
+inline int walk_tmem_cols_h(int k, int jbmax)
 {
     int need = k * jbmax * 4, c = 32;
     while (c < need) c <<= 1;
     return c;
-}
-
-// Predicated stores that stay predicated (no branch around them, so the
-// entries of a step remain one basic block the scheduler can interleave).
-__device__ __forceinline__ void stg2_cs_if(double* p, double a, double b, bool q)
-{
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.global.cs.v2.f64 [%0], {%1, %2};\n\t}" ::"l"(p),
-                 "d"(a), "d"(b), "r"((unsigned)q));
-}
-__device__ __forceinline__ void stg_cs_if(double* p, double v, bool q)
-{
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
-                 "r"((unsigned)q));
-}
-__device__ __forceinline__ void sts_pair_if(unsigned a, double x, double u, double y, int rs, bool q)
-{
-    // E_i = (x, u) at a, E_{i+1}.x = y at a + rs
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.shared.v2.f64 [%0], {%1, %2};\n\t"
-                 "@q st.shared.f64 [%3], %4;\n\t}" ::"r"(a), "d"(x), "d"(u), "r"(a + rs), "d"(y), "r"((unsigned)q)
-                 : "memory");
-}
-__device__ __forceinline__ double lds1(unsigned a)
-{
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ double2 lds2(unsigned a)
-{
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
-    return v;
 }
 
 // Per-lane constants of the current item.
@@ -438,10 +320,12 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
         const unsigned ncol = L.sbase + q.y;
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(ncol));
         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(ncol + RS));
+#ifndef BNREG_CHAIN_NOSEL
         if (!((fl >> 7) & 1u)) {
             a = 0.0;
             b = 1.0;
         }
+#endif
         givens_fr(a, b, c, sg, hh);
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
@@ -524,9 +408,9 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_item, s_taddr;
     double2* const lntab = (double2*)smem;
-    double* const KC = (double*)(smem + 8192);
+    double* const KC = (double*)(smem + 16 * kLnEntries);
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-    for (int j = tid; j < 512; j += blockDim.x) lntab[j] = P.lntab9[j];
+    for (int j = tid; j < kLnEntries; j += blockDim.x) lntab[j] = P.lntab9[j];
     for (int j = tid; j < 33; j += blockDim.x) KC[j] = P.Kc[j];
     if (wib == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -705,9 +589,9 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
 // Dynamic shared memory of a launch: the layout, padded so that no more CTAs
 // share an SM than its 512 TMEM columns hold (a CTA beyond that would wait in
 // tcgen05.alloc).
-static size_t walk_launch_smem(const TravParams& P)
+static inline size_t walk_launch_smem(const TravParams& P)
 {
-    size_t smem = walk_cta_smem(P.m, P.k, P.S_alloc, P.g, P.lw);
+    size_t smem = walk_cta_smem_h(P.m, P.k, P.S_alloc, P.g, P.lw);
     const int occ_tm = 512 / P.tm_cols;
     const size_t cap = (size_t)233472 / (size_t)(occ_tm + 1);   // 228 KB per SM / (occ + 1)
     if (smem + 1024 <= cap) smem = cap - 1024 + 16;
@@ -715,7 +599,7 @@ static size_t walk_launch_smem(const TravParams& P)
 }
 
 template <bool HR, bool HB, bool HP, int JBMAX>
-static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
+static inline cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
 {
     const size_t smem = walk_launch_smem(P);
     auto f = walk_kernel<HR, HB, HP, JBMAX>;
@@ -723,51 +607,6 @@ static cudaError_t launch_w(const TravParams& P, int grid, cudaStream_t st)
     if (e != cudaSuccess) return e;
     f<<<grid, 32 << P.g, smem, st>>>(P);
     return cudaGetLastError();
-}
-
-template <int JBMAX>
-static cudaError_t launch_jb(const TravParams& P, int grid, cudaStream_t st)
-{
-    if (P.out_pairs) return launch_w<false, false, true, JBMAX>(P, grid, st);
-    const int key = (P.out_rss ? 2 : 0) | (P.out_bic ? 1 : 0);
-    switch (key) {
-        case 3: return launch_w<true, true, false, JBMAX>(P, grid, st);
-        case 2: return launch_w<true, false, false, JBMAX>(P, grid, st);
-        case 1: return launch_w<false, true, false, JBMAX>(P, grid, st);
-        default: return launch_w<false, false, false, JBMAX>(P, grid, st);
-    }
-}
-
-cudaError_t launch_walk(const TravParams& P, int grid, cudaStream_t st)
-{
-    if (P.lw != 3 || P.k > 8 || P.jbmax > 7) return cudaErrorInvalidValue;   // 8 workers per warp, k <= 8
-    return P.jbmax <= 4 ? launch_jb<4>(P, grid, st) : launch_jb<7>(P, grid, st);
-}
-
-int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int jbmax)
-{
-    // computed from the limits directly: cudaOccupancyMaxActiveBlocksPerMultiprocessor
-    // reports 1 CTA per SM for this kernel (measured on B200, CUDA 12.9), although the
-    // SM runs 4 (ncu launch__occupancy_limit_*)
-    TravParams P{};
-    P.m = m; P.k = k; P.S_alloc = S_alloc; P.g = g; P.lw = 3; P.jbmax = jbmax;
-    P.tm_cols = walk_tmem_cols(k, jbmax);
-    const size_t smem = walk_launch_smem(P);
-    auto f = jbmax <= 4 ? walk_kernel<true, true, false, 4> : walk_kernel<true, true, false, 7>;
-    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-    cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 0;
-    int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
-    const int threads = 32 << g;
-    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
-    const int by_regs = regs_sm / (regs_warp * (threads / 32));
-    const int by_smem = (int)((size_t)smem_sm / (smem + fa.sharedSizeBytes + 1024));
-    const int by_thr = thr_sm / threads;
-    return std::max(0, std::min(std::min(by_regs, by_smem), std::min(by_thr, 512 / P.tm_cols)));
 }
 
 }  // namespace bnr

@@ -602,3 +602,24 @@ def test_cholesky_root_comparison():
         h.close()
     assert errs[bn.ROOT_TSQR] <= RSS_RTOL
     assert errs[bn.ROOT_CHOLESKY] >= 1e3 * max(errs[bn.ROOT_TSQR], 1e-15), errs
+
+
+@pytest.mark.parametrize("case", ["cfg1_k4", "cfg1_k8", "cfg2", "cfg2_pairs", "m12_k3", "m6_k2", "cfg3"])
+def test_walk7_parity(case):
+    """The alternative walk design (bnreg_options.pack_bits = 5: 32 lockstep workers per
+    warp, one lane each; walk7_kernel.cu + seed7) against the oracle exactly like the
+    default: every entry written, RSS relative 1e-9, BIC absolute 1e-6, exact argmax."""
+    bn = _bn()
+    if case.startswith("cfg1"):
+        X, opt = datagen.config_data(1), bn.options(free_vars=int(case[-1]), pack_bits=5)
+        _check_full(X, opt)
+    elif case == "cfg2":
+        _check_full(datagen.config_data(2), bn.options(pack_bits=5))
+    elif case == "cfg2_pairs":
+        _check_full(datagen.config_data(2), bn.options(pack_bits=5), pairs=True)
+    elif case == "m12_k3":
+        _check_full(datagen.dag_data(12, 200, 0.25, 0.5, 2.0, seed=12), bn.options(free_vars=3, pack_bits=5))
+    elif case == "m6_k2":
+        _check_full(datagen.dag_data(6, 40, 0.3, 0.5, 2.0, seed=6), bn.options(free_vars=2, pack_bits=5))
+    else:
+        _check_full(datagen.config_data(3), bn.options(pack_bits=5), o2=True, pairs=True)
