@@ -263,6 +263,15 @@ int64_t bnreg_plan_packs(int32_t m, int64_t n, const bnreg_options* opt, uint32_
  * count DEVICE doubles x_dev (> 1e-300, finite) -> out_dev.  Synchronous. */
 bnreg_status bnreg_debug_ln(bnreg_t* h, const double* x_dev, double* out_dev, int64_t count);
 
+/* Test hook (reading G11 "every family exactly once"): in the debug
+ * build libbnreg_k8.so (-DBNREG_K8) every table store of later runs also increments
+ * counts_dev[local index] (a caller-owned, zeroed DEVICE array of bnreg_num_families + 1
+ * uint32; NULL = stop counting), so a test can assert each entry is written exactly once;
+ * counts_dev[bnreg_num_families] counts violated bounds checks of the walk kernels (a table
+ * index out of range, a shared-memory state or TMEM address outside the warp's region).
+ * The release library returns BNREG_E_INVAL. */
+bnreg_status bnreg_debug_write_counts(bnreg_t* h, uint32_t* counts_dev);
+
 const char* bnreg_last_error(void);
 
 void bnreg_destroy(bnreg_t* h);   /* NULL-safe; frees device state */

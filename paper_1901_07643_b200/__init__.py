@@ -32,7 +32,8 @@ SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", 
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
-           "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_last_error", "bnreg_destroy"]
+           "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_debug_write_counts", "bnreg_last_error",
+           "bnreg_destroy"]
 
 
 class BnregError(RuntimeError):
@@ -103,6 +104,7 @@ def lib():
         "bnreg_schedule": ([i32, P, i64], i64),
         "bnreg_plan_packs": ([i32, i64, POPT, P, i64], i64),
         "bnreg_debug_ln": ([H, P, P, i64], i32),
+        "bnreg_debug_write_counts": ([H, P], i32),
         "bnreg_last_error": ([], ctypes.c_char_p),
         "bnreg_destroy": ([H], None),
     }
@@ -334,6 +336,11 @@ class Bnreg:
     def debug_ln(self, x_dev, out_dev, count: int):
         """Test hook: the BIC epilogue's fp64 log on device buffers."""
         _check(lib().bnreg_debug_ln(self._h, _dptr(x_dev), _dptr(out_dev), count))
+
+    def debug_write_counts(self, counts_dev):
+        """K8 test hook (libbnreg_k8.so only): count every table store of later runs into
+        counts_dev (zeroed device uint32[num_families]); None stops counting."""
+        _check(lib().bnreg_debug_write_counts(self._h, _dptr(counts_dev)))
 
     def close(self):
         if getattr(self, "_h", None):

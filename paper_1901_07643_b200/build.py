@@ -81,5 +81,13 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     return out
 
 
+K8_OUT = os.path.join(HERE, "libbnreg_k8.so")
+
+
+def build_k8(force: bool = False) -> str:
+    """The K8 debug build (per-entry write counters, bnreg_debug_write_counts)."""
+    return build(force=force, out=K8_OUT, defines=["-DBNREG_K8=1"])
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -108,6 +108,7 @@ struct bnreg {
     bool w7 = false;
     int w7_warps = 4, w7_TB = 16, w7_KA = 8, w7_nbmax = 0;
     unsigned long long w7_sblk = 0;     // doubles per item of the seed blocks
+    unsigned* k8 = nullptr;             // BNREG_K8 debug builds: caller's per-entry write counters
 };
 
 static bnreg_options defaults(const bnreg_options* o)
@@ -604,6 +605,9 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.world1 = P.world == 1 ? 1 : 0;
     for (int s = 0; s <= 32; ++s) T.Kc[s] = K[s];
     T.r = P.r;
+    T.k8 = h->k8;
+    T.k8_n = (unsigned long long)P.local_families;
+    T.k8_selftest = getenv("BNREG_K8_SELFTEST") ? 1 : 0;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
     CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
     // a5: every pack's seeds, in the walk kernel's layout
@@ -822,6 +826,18 @@ bnreg_status bnreg_best_merge_async(bnreg_t* h, int32_t nparts, const uint32_t* 
     CK(launch_best_reduce(bics_dev, masks_dev, nparts, h->plan.m, out_bic_dev, out_mask_dev, nullptr, h->stream,
                           (size_t)row_bytes));
     return BNREG_OK;
+}
+
+bnreg_status bnreg_debug_write_counts(bnreg_t* h, uint32_t* counts_dev)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+#ifdef BNREG_K8
+    h->k8 = counts_dev;
+    return BNREG_OK;
+#else
+    (void)counts_dev;
+    return fail(BNREG_E_INVAL, "this library was built without BNREG_K8 (libbnreg_k8.so has the write counters)");
+#endif
 }
 
 bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* runs)

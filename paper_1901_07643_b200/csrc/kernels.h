@@ -47,6 +47,10 @@ struct TravParams {
     int TB;                     // back slots held in TMEM (512 columns / (4 k))
     int nbmax;                  // most back slots of any item (p + tree levels)
     unsigned long long sblk;    // doubles per item of the seed blocks (seed7 layout)
+    unsigned* k8;               // BNREG_K8 debug builds: per-entry write counters (rank-local index), or null;
+                                // k8[k8_n] counts out-of-range accesses (table index, shared state, TMEM)
+    unsigned long long k8_n;    // this rank's table entries
+    int k8_selftest;            // BNREG_K8: lane 0 of every warp reports one deliberate violation
 };
 
 // seed kernel: one warp per pack derives its 2^p workers' seeds (the remaining

@@ -114,6 +114,21 @@ __device__ __forceinline__ void tm_put(uint32_t* r, double x)
 
 // Predicated stores that stay predicated (no branch around them, so the
 // entries of a step remain one basic block the scheduler can interleave).
+// BNREG_K8 debug builds: count a violated bounds condition in k8[k8_n]
+#ifdef BNREG_K8
+#define K8_CHECK(L, cond)                                                                           \
+    do {                                                                                            \
+        if ((L).k8 && !(cond)) atomicAdd((L).k8 + (L).k8_n, 1u);                                     \
+    } while (0)
+#define K8_COUNT(L, ok, ix)                                                                         \
+    do {                                                                                            \
+        if ((L).k8 && (ok)) atomicAdd((L).k8 + ((ix) < (L).k8_n ? (unsigned long long)(ix) : (L).k8_n), 1u); \
+    } while (0)
+#else
+#define K8_CHECK(L, cond) do { } while (0)
+#define K8_COUNT(L, ok, ix) do { } while (0)
+#endif
+
 #ifndef BNREG_ST_POLICY
 #define BNREG_ST_POLICY ".cs"   // the record stores' cache operator (A/B: "", ".cg", ".cs")
 #endif

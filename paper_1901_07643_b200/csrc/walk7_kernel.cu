@@ -102,6 +102,11 @@ struct L7 {
     double* out_rss;
     double* out_bic;
     double* out_pairs;
+    unsigned* k8;        // BNREG_K8: write counters (+ the violation counter k8[k8_n])
+    unsigned long long k8_n;
+    unsigned sb0;        // BNREG_K8 bounds checks: the warp's shared state [sb0, sb0 + sbytes)
+    unsigned sbytes;
+    unsigned tmcols;     // and the TMEM columns it may address
 };
 
 // Harvest of NE entries (a9-a11): ln RSS, BIC, the record / table stores and the
@@ -129,6 +134,7 @@ __device__ __forceinline__ void harvest7(const L7& L, const double* rs, const un
             stg_cs_if(L.out_bic + ix, bic, okv[e] && L.out_bic != nullptr);
         }
         if (HP) stg2_cs_if(L.out_pairs + 2 * (size_t)ix, rss, bic, okv[e]);
+        K8_COUNT(L, okv[e], ix);   // K8 debug builds: every entry written exactly once, in range
         upd |= (okv[e] && bic >= rr.x) ? (1u << e) : 0u;
     }
     unsigned bal = __ballot_sync(FULLMASK, upd != 0);
@@ -250,6 +256,7 @@ template <int NC>
 __device__ __forceinline__ void back_rot2(const L7& L, int i, int cc0, double c, double sg, double* rs, unsigned* ra,
                                           bool* okv)
 {
+    K8_CHECK(L, i >= 0 && (unsigned)(((cc0 + NC - 1) * L.k + i) * 16 + 32) <= L.tmcols);
     uint32_t ab[NC][16], cd[NC][16];
 #pragma unroll
     for (int h = 0; h < NC; ++h) {
@@ -305,6 +312,7 @@ __device__ __forceinline__ void grc_step7(const L7& L, const uint4 q, double& c,
 #pragma unroll
     for (int j = 0; j < 4 * NFC; ++j) {
         const unsigned fa = bi + ((q.z >> (4 * j)) & 15u) * kCS7;
+        K8_CHECK(L, j >= nf || (fa + RS + 16 - L.sb0 <= L.sbytes && fa >= L.sb0));
         const double x = lds1(fa);
         const double2 y = lds2(fa + RS);
         const double xa = fma(c, x, sg * y.x), ya = fma(c, y.x, -sg * x);
@@ -533,6 +541,12 @@ __global__ void __launch_bounds__(128, 1) walk7_kernel(const __grid_constant__ T
     L.out_rss = P.out_rss;
     L.out_bic = P.out_bic;
     L.out_pairs = P.out_pairs;
+    L.k8 = P.k8;
+    L.k8_n = P.k8_n;
+    L.sb0 = (unsigned)__cvta_generic_to_shared(wb + Ly.state);
+    L.sbytes = (unsigned)(k * P.KA * kCS7);
+    L.tmcols = 512u;
+    K8_CHECK(L, !(P.k8_selftest && (threadIdx.x & 31) == 0));   // (a negative control of the counter path)
     const uint4* const st = stab;
     __syncwarp();
 

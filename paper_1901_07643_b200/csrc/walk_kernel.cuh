@@ -124,6 +124,11 @@ struct LaneC {
     double* out_rss;
     double* out_bic;
     double* out_pairs;
+    unsigned* k8;        // BNREG_K8: write counters (+ the violation counter k8[k8_n])
+    unsigned long long k8_n;
+    unsigned sb0;        // BNREG_K8 bounds checks: the warp's shared state [sb0, sb0 + sbytes)
+    unsigned sbytes;
+    unsigned tmcols;     // and the TMEM columns it may address
 };
 
 // phase C of a step: ln RSS, BIC (a9), the two table stores (a10) and the
@@ -149,6 +154,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
         if (HR) stg_cs_if(L.out_rss + ix, rss, okv[e]);
         if (HB) stg_cs_if(L.out_bic + ix, bic, okv[e]);
         if (HP) stg2_cs_if(L.out_pairs + 2 * (size_t)ix, rss, bic, okv[e]);
+        K8_COUNT(L, okv[e], ix);   // K8 debug builds: every entry written exactly once, in range
         // candidate: BIC >= the slot's threshold min(running best, tiny_bic); a perfect fit
         // (RSS <= 1e-300, G13: BIC = +inf, fixed on the rare path) has BIC >= tiny_bic
         upd |= (okv[e] && bic >= rr.x) ? (1u << e) : 0u;
@@ -272,6 +278,7 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
     if constexpr (JB > 0) {
         uint32_t rb[8 * JB];
         const uint32_t tcol = L.tb + (uint32_t)(i * JB * 4);
+        K8_CHECK(L, i >= 0 && (unsigned)((i + 2) * JB * 4) <= L.tmcols);
         tm_wait_st();
         tm_ld<8 * JB>(tcol, rb);
 #pragma unroll
@@ -304,6 +311,7 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
     }
 #pragma unroll
     for (int j = 0; j < NFE; ++j) {
+        K8_CHECK(L, !fo[j] || (bi + sl[j] * kCS + RS + 16 - L.sb0 <= L.sbytes && bi + sl[j] * kCS >= L.sb0));
         const double xa = fma(c, f0[j], sg * f1[j].x), ya = fma(c, f1[j].x, -sg * f0[j]);
         const double ru = fma(ya, ya, f1[j].y);
         sts_pair_if(bi + sl[j] * kCS, xa, ru, ya, RS, fo[j]);
@@ -457,6 +465,12 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     L.out_rss = P.out_rss;
     L.out_bic = P.out_bic;
     L.out_pairs = P.out_pairs;
+    L.k8 = P.k8;
+    L.k8_n = P.k8_n;
+    L.sb0 = (unsigned)__cvta_generic_to_shared(st);
+    L.sbytes = (unsigned)(k * k * kW * 16);
+    L.tmcols = (unsigned)P.tm_cols;
+    K8_CHECK(L, !(P.k8_selftest && (threadIdx.x & 31) == 0));   // (a negative control of the counter path)
     {
         // the worker's warp and gang variables in F (user-id bits): w, and gang slot wib
         // bit j = seed-tree level gs + j = gang variable fv0 - 1 - j (plan.h hv_id)
