@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--outputs", default="both", choices=["both", "rss", "bic", "none"],
                     help="diagnostic: which tables the timed run writes (the metric needs both)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sim-world", type=int, default=1,
+                    help="diagnostic (one GPU, no collectives): run logical rank --sim-rank of a world of this size "
+                         "(its shard of the lattice, rank-filtered seed tree) to measure per-rank costs")
+    ap.add_argument("--sim-rank", type=int, default=0)
     return ap.parse_args()
 
 
@@ -74,12 +78,37 @@ def load_peaks():
 
 
 def ncu_traffic(cfg):
-    """dram read+write bytes per traverse launch from the committed ncu capture, if any."""
+    """dram read+write bytes of the walk launches of one step, from the committed ncu
+    capture (a capture value, not measured in this run): (bytes, source tag) or (None, None)."""
     p = os.path.join(ROOT, "profiles", "traverse_ncu_summary.json")
     if os.path.exists(p):
         d = json.load(open(p))
         if d.get("config") == cfg and d.get("traffic_bytes_per_launch"):
-            return float(d["traffic_bytes_per_launch"])
+            return float(d["traffic_bytes_per_launch"]), "ncu --set full capture %s (profiles/traverse_ncu_summary.json)" % (
+                d.get("tag"),)
+    return None, None
+
+
+# Measured on this pool's B200 (tools/microbench.cu, profiles/r01_microbench_b200.txt): the FP64 FMA
+# peak and the store-only bandwidth of coalesced 16 B stores (the copy peak of MEASURED_PEAKS.json
+# counts reads and writes)
+FP64_PEAK_TFLOPS = 34.79
+STORE_PEAK_GBS = 6967.5
+
+
+def eq13_flops(m):
+    """Eq.13 (reading G6): the Givens flops of the whole walk,
+    3m 2^m + 6 2^m - 3m^2 - 9m - 6 (the roofline's FP64 term, north star)."""
+    return 3 * m * 2 ** m + 6 * 2 ** m - 3 * m * m - 9 * m - 6
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
     return None
 
 
@@ -136,9 +165,9 @@ class Clocks:
 # ---------------------------------------------------------------------------- oracle timing
 def oracle_rate(X, seconds, seed=1234, batch=256):
     """The oracle (O1, per-family Householder, OpenMP over families) as it stands,
-    on a bounded uniform sample of the workload's families."""
+    on a bounded uniform sample of the workload's families; and the reduced oracle O2
+    (Householder on slices of the oracle's root QR) on 1e6 sampled families."""
     import numpy as np
-    import datagen
     import oracle
     n, m = X.shape
     Xc = oracle.centre(X)
@@ -150,7 +179,11 @@ def oracle_rate(X, seconds, seed=1234, batch=256):
         done += min(batch, len(idx) - done)
         batch = min(batch * 2, 8192)
     el = time.perf_counter() - t0
-    return done / el, done, el, oracle.num_threads()
+    t1 = time.perf_counter()
+    R0 = oracle.qr_r(Xc)
+    oracle.rss_reduced_indices(R0, idx[:1_000_000])
+    o2 = 1_000_000 / (time.perf_counter() - t1)
+    return done / el, done, el, oracle.num_threads(), o2
 
 
 def bench_reference(args):
@@ -322,7 +355,9 @@ def bench_ours(args):
     dev = torch.device("cuda", local)
     X = datagen.config_data(args.config, args.seed)
     n, m = X.shape
-    opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=world, rank=rank, pack_bits=args.pack_bits)
+    sim = args.sim_world > 1 and world == 1
+    opt = bn.options(free_vars=args.k, levels_in_warp=args.lw, world=args.sim_world if sim else world,
+                     rank=args.sim_rank if sim else rank, pack_bits=args.pack_bits)
     h = bn.Bnreg(n, m, opt)
     plan = bn.bnreg_plan_query(m, n, opt)
     # one explicit (non-legacy) stream for torch, NCCL ordering and the handle: the timing
@@ -374,7 +409,10 @@ def bench_ours(args):
     tms, runs = h.timing(0)
     trav_ms = tms[2] / max(runs, 1)
     run_ms = tms[0] / max(runs, 1)
-    value = total * args.steps / (ms / 1e3)
+    phases = {"load_ms (rank 0: centre + root QR)": (tms[4] / tms[5]) if tms[5] else None,
+              "seeds_ms (seed tree + seed kernel)": tms[1] / max(runs, 1), "walk_ms": trav_ms,
+              "best_reduce_ms": tms[3] / max(runs, 1), "run_ms (seeds + walk + reduce)": run_ms}
+    value = (F if sim else total) * args.steps / (ms / 1e3)
     e2e = None
     if not args.no_e2e:
         ms_e2e, _ = timed(step_e2e, args.steps, 1)
@@ -383,17 +421,35 @@ def bench_ours(args):
                "ms_per_step": ms_e2e / args.steps}
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_FAMILY * F / (trav_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(f"cfg{args.config}")
+    # FP64 side of the roofline: the walk's algorithmic Givens flops (Eq.13 over this rank's share
+    # of the lattice) per walk time, against the measured FP64 FMA peak
+    fl = eq13_flops(m) * F / total
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(f"cfg{args.config}"), "kernel": "walk_kernel (all shared-memory classes of a step)",
+            "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": "walk_kernel (all shared-memory classes of a step)",
             "kernel_ms": trav_ms, "algorithmic_bytes_per_launch": BYTES_PER_FAMILY * F,
             "peak_source": peak_src,
+            "store_peak": STORE_PEAK_GBS, "frac_of_store_peak": achieved / STORE_PEAK_GBS,
+            "store_peak_source": "measured store-only bandwidth, coalesced 16 B stores (tools/microbench.cu, "
+                                 "profiles/r01_microbench_b200.txt)",
+            "fp64": {"algorithmic_flops_per_step": fl, "achieved_tflops": fl / (trav_ms / 1e3) / 1e12,
+                     "peak_tflops": FP64_PEAK_TFLOPS, "frac": fl / (trav_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "t_fp64_ms": fl / (FP64_PEAK_TFLOPS * 1e12) * 1e3,
+                     "t_hbm_ms": BYTES_PER_FAMILY * F / (peak * 1e9) * 1e3,
+                     "note": "Eq.13 Givens flops (PAPER.md:235-239, G6); peak = measured DFMA throughput "
+                             "(tools/microbench.cu); the HBM term binds by ~14x"},
             "step_frac": (BYTES_PER_FAMILY * total * args.steps / (ms / 1e3) / 1e9) / peak / world}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, done, el, cores = oracle_rate(X, args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+        rate, done, el, cores, o2 = oracle_rate(X, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{done} families uniformly sampled from cfg{args.config}'s {total} "
-                         f"(O1 per-family Householder QR, n={n}), {el:.1f} s on the host"}
+                         f"(O1 per-family Householder QR, n={n}), {el:.1f} s on the host",
+               "full_table_s_extrapolated": total / rate,
+               "reduced_oracle_O2": {"value": o2, "unit": UNIT,
+                                     "sample": "1e6 of the same families, Householder on slices of the "
+                                               "oracle's root QR (SURVEY.md §8(c) O2)"}}
     launches = args.steps * (h.launches_per_run() + (2 if rank == 0 else 0) + (1 if world > 1 else 0))
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -409,7 +465,11 @@ def bench_ours(args):
                           "l2": "outputs (16 B/family, %.1f GB) >> L2 126 MB: every step evicts L2" % (
                               BYTES_PER_FAMILY * total / 1e9)},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
-               "ms_per_step_recheck": ms_chk / args.steps, "run_ms_device": run_ms}
+               "ms_per_step_recheck": ms_chk / args.steps, "run_ms_device": run_ms, "phases": phases}
+        if sim:
+            out["sim"] = {"world": args.sim_world, "rank": args.sim_rank, "rank_families": F,
+                          "note": "one logical rank on one GPU, no collectives; value = this rank's families/s "
+                                  "(every logical rank loads and factors X itself)"}
         print(json.dumps(out), flush=True)
     h.close()
     if world > 1:

@@ -237,8 +237,10 @@ bnreg_status bnreg_best_merge_async(bnreg_t* h, int32_t nparts, const uint32_t* 
 
 /* Per-phase device time of the runs since the last reset, from CUDA events on
  * the launching stream.  enable: 1 = start recording (and reset), 0 = stop,
- * -1 = just read.  out_ms[0] = whole run, [1] = seed tree, [2] = traversal
- * kernel, [3] = best reduce; *runs = number of runs accumulated. */
+ * -1 = just read.  out_ms (6 entries): [0] = whole run, [1] = seed tree + seed
+ * kernel, [2] = walk kernel, [3] = best reduce, [4] = loads (centre + root QR) of
+ * timed loads, [5] = number of those loads; *runs = number of runs accumulated.
+ * Collecting the events synchronises once per run. */
 bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* runs);
 
 /* Kernel launches of one bnreg_run / bnreg_run_async on this handle (the seed

@@ -328,7 +328,8 @@ class Bnreg:
         return lib().bnreg_launches_per_run(self._h)
 
     def timing(self, enable: int = -1):
-        ms = np.zeros(4)
+        """bnreg_timing -> (ms[6]: run, seeds, walk, reduce, load total, load count; runs)."""
+        ms = np.zeros(6)
         runs = ctypes.c_int64(0)
         _check(lib().bnreg_timing(self._h, enable, _hptr(ms), ctypes.byref(runs)))
         return ms, runs.value

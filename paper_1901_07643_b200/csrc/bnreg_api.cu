@@ -85,7 +85,9 @@ struct bnreg {
     // timing
     bool timing = false;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    double acc_ms[4] = {0, 0, 0, 0};
+    double acc_ms[6] = {0, 0, 0, 0, 0, 0};   // run, seeds, walk, reduce, load (centre + root QR), loads
+    cudaEvent_t evl[2] = {nullptr, nullptr};
+    bool load_timed = false;       // a timed load is waiting to be collected
     int64_t runs = 0;
     // walk kernel: one launch per shared-memory class of work items
     struct WalkClass {
@@ -131,6 +133,8 @@ static void free_all(bnreg* h)
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : h->evl)
         if (e) cudaEventDestroy(e);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     if (h->h_status) cudaFreeHost(h->h_status);
@@ -273,6 +277,48 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             fprintf(stderr, "walk7: items %lld grid %d warps %d TB %d KA %d nbmax %d smem %zu seed blocks %.2f GB\n",
                     (long long)ni, c.grid, warps, h->w7_TB, h->w7_KA, h->w7_nbmax,
                     walk7_cta_smem(k, h->w7_KA, k + h->w7_nbmax, warps), ni * h->w7_sblk * 8.0 / 1e9);
+    } else if (!getenv("BNREG_NO_SPLIT")) {
+        // walk kernel, one launch: every item at 4 CTAs per SM (4 back entries per lane in TMEM,
+        // 16 back slots per warp); an item with more back slots gets a second pass over back
+        // slots 16.. (entry 0x80000000 | item appended to the item list; it rotates the free
+        // entries without harvesting them).  Items stay sorted costliest first.
+        const int gs = P.bh - P.g;
+        std::vector<uint32_t> items(P.packs.begin(), P.packs.end());
+        const int64_t na = (int64_t)items.size();
+        int nbmax = 0;
+        for (int64_t i = 0; i < na; ++i) {
+            const int nb = P.p + P.g + (gs - popc(P.packs[i] & ((1u << gs) - 1u)));
+            nbmax = std::max(nbmax, nb);
+            if (nb > 16) items.push_back(0x80000000u | (uint32_t)i);
+        }
+        if (nbmax > 32) return bail(fail(BNREG_E_INVAL, "too many back slots per item (raise k)"));
+        const int S0 = P.k + nbmax;
+        int occ = d.ctas_per_sm > 0 ? d.ctas_per_sm : walk_max_ctas_per_sm(m, P.k, S0, P.g, 4);
+        if (occ <= 0) return bail(fail(BNREG_E_NOMEM, "walk kernel does not fit in shared memory / TMEM"));
+        bnreg::WalkClass c;
+        c.begin = 0; c.end = (int)items.size(); c.S_alloc = S0; c.jbmax = 4;
+        c.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->num_sms * occ, (int64_t)items.size()));
+        c.part_base = 0;
+        h->nparts = c.grid * h->wpc;
+        h->classes.push_back(c);
+        if (!items.empty()) {
+            cudaFree(h->d_packs);
+            h->d_packs = nullptr;
+            CKH(cudaMalloc(&h->d_packs, items.size() * sizeof(uint32_t)));
+            CKH(cudaMemcpy(h->d_packs, items.data(), items.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        }
+        h->seed_off.push_back(0);
+        CKH(cudaMalloc(&h->d_seeds, std::max<size_t>((size_t)na * (size_t)h->wpc * seed_block_bytes(P.k, S0, P.lw), 16)));
+        CKH(cudaMalloc(&h->d_counters, sizeof(unsigned)));
+        const auto recs = step_records(P.k, P.sched);
+        h->wsteps_len = recs.size();
+        auto tb = walk_step_table(recs, P.k, P.k, 1 << P.lw);   // free-slot state: k slots
+        for (int j = 0; j < 32; ++j) tb.push_back(WalkStep{});   // pad: the walk kernel loads 32-record windows
+        CKH(cudaMalloc(&h->d_wsteps, tb.size() * sizeof(WalkStep)));
+        CKH(cudaMemcpy(h->d_wsteps, tb.data(), tb.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
+        if (getenv("BNREG_VERBOSE"))
+            fprintf(stderr, "walk: items %zu (%lld split) S_alloc %d grid %d occ %d\n", items.size(),
+                    (long long)(items.size() - na), S0, c.grid, occ);
     } else {
         // walk kernel: items are sorted costliest first = most walk slots first
         // (a gang's slots: m - |F among its tree levels|).  A launch ("class") takes
@@ -358,6 +404,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         CKH(cudaMemcpy(h->d_lntab9, tab9.data(), kLnEntries * sizeof(double2), cudaMemcpyHostToDevice));
     }
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
+    for (auto& e : h->evl) CKH(cudaEventCreate(&e));
 #undef CKH
     *out = h;
     return BNREG_OK;
@@ -395,6 +442,7 @@ static bnreg_status load_enqueue(bnreg_t* h, const double* X, int32_t x_on_devic
         CK(cudaMemcpyAsync(h->dX, X, nm * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         src = h->dX;
     }
+    if (h->timing) CK(cudaEventRecord(h->evl[0], h->stream));
     CK(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
     CK(launch_centre(src, P.n, P.m, h->d_order, h->dXr, h->d_status, h->stream));
     if (h->root_method == 1) {
@@ -402,6 +450,10 @@ static bnreg_status load_enqueue(bnreg_t* h, const double* X, int32_t x_on_devic
         CK(launch_gram_chol(h->dXr, P.n, P.m, h->d_gram, h->d_root, h->d_status, h->stream));
     } else {
         CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
+    }
+    if (h->timing) {
+        CK(cudaEventRecord(h->evl[1], h->stream));
+        h->load_timed = true;
     }
     CK(cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     h->ran = false;
@@ -670,6 +722,13 @@ static bnreg_status collect_timing(bnreg_t* h)
     CK(cudaEventElapsedTime(&c, h->ev[1], h->ev[2]));
     CK(cudaEventElapsedTime(&d, h->ev[2], h->ev[3]));
     h->acc_ms[0] += a; h->acc_ms[1] += b; h->acc_ms[2] += c; h->acc_ms[3] += d;
+    if (h->load_timed) {
+        float l = 0;
+        CK(cudaEventElapsedTime(&l, h->evl[0], h->evl[1]));
+        h->acc_ms[4] += l;
+        h->acc_ms[5] += 1;
+        h->load_timed = false;
+    }
     h->runs += 1;
     return BNREG_OK;
 }
@@ -844,7 +903,7 @@ bnreg_status bnreg_timing(bnreg_t* h, int32_t enable, double* out_ms, int64_t* r
 {
     if (!h) return fail(BNREG_E_INVAL, "NULL handle");
     if (out_ms)
-        for (int i = 0; i < 4; ++i) out_ms[i] = h->acc_ms[i];
+        for (int i = 0; i < 6; ++i) out_ms[i] = h->acc_ms[i];
     if (runs) *runs = h->runs;
     if (enable == 1) {
         h->timing = true;

@@ -106,7 +106,11 @@ __device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
     const int e = (hi >> 20) - 1023;
     const double f = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     double tx, ty;
+#ifdef BNREG_FAKE_LN   // timing experiment only (wrong logs): every lane reads entry 0 (one broadcast wavefront)
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + (ln_tab_off(hi) & 0)));
+#else
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ln_tab_off(hi)));
+#endif
     const double base = fma((double)e, kLn2, ty);
     return ln_poly(fma(f, tx, -1.0), base);
 }

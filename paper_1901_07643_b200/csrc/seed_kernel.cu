@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
         const int SA = P.cls_SA[c];
         unsigned char* const blk =
             P.seeds + P.cls_off[c] + ((size_t)(item - P.cls_begin[c]) * G + gw) * seed_block_bytes(k, SA, LW);
+        if (P.packs[item] >> 31) continue;       // a split item's second pass: the first pass's seeds
         const uint32_t pack = P.packs[item] | ((uint32_t)gw << gs);
         // the node at depth L1: sn x sn, row-major (stride m) in global memory
         const uint32_t nid = pack & ((1u << P.L1) - 1u);
@@ -209,9 +210,11 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
         // Gray path over the warp variables: start with all of them in F (front
         // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
         // variable j across the free block and the j lower warp variables
-        const size_t wsz = (size_t)k * SA * 16;      // one worker's part of the block
+        // the block is packed with this item's own slot count Sw (<= SA) as the row stride
+        const int SW = k + fv0 + (gs - __popc(P.packs[item] & ((1u << gs) - 1u)));
+        const size_t wsz = (size_t)k * SW * 16;      // one worker's part of the block
         int wcur = P.nw - 1;
-        snapshot_sq(A, SAq, sn, org + p, k, SA, lane, pos, slot, blk + wcur * wsz);
+        snapshot_sq(A, SAq, sn, org + p, k, SW, lane, pos, slot, blk + wcur * wsz);
         for (int i = 1; i < P.nw; ++i) {
             const int j = __ffs(i) - 1;
             const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
                 for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
             }
             wcur ^= 1 << j;
-            snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SA, lane, pos, slot, blk + wcur * wsz);
+            snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SW, lane, pos, slot, blk + wcur * wsz);
         }
         __syncwarp();
     }

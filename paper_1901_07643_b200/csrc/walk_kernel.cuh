@@ -109,7 +109,8 @@ struct LaneC {
     unsigned bbb;     // shared address of bb[slot 0]
     double tiny_bic;  // a lower bound of the BIC of any RSS <= 1e-300 (G13)
     uint32_t tb;      // TMEM address of (this warp's lane quarter, column 0)
-    uint32_t bval;    // bit j: back entry j (slot k + 4j + h) holds a family of this worker
+    uint32_t bval;    // bit j: back entry j (slot k + b0 + 4j + h) holds a family of this worker
+    int hfree;        // this pass harvests the free entries (split items: only the first pass)
     uint32_t w;       // worker id = its warp-variable bits
     uint32_t Xw;      // the worker's warp and gang variables in F (user-id bits)
     uint32_t Fw;      // the worker's F (user ids)
@@ -245,7 +246,7 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
         const double2 a = lds2(bi + sl[j] * kCS);
         rs[JB + j] = s0 ? fma(a.x, a.x, a.y) : a.y;
         ra[JB + j] = L.recb + sl[j] * 16;
-        okv[JB + j] = fo[j];
+        okv[JB + j] = fo[j] && L.hfree;
     }
     const uint32_t Tsh = (fl >> 17) << L.fv0;
     harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
@@ -317,7 +318,7 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
         sts_pair_if(bi + sl[j] * kCS, xa, ru, ya, RS, fo[j]);
         rs[JB + j] = ru;
         ra[JB + j] = L.recb + sl[j] * 16;
-        okv[JB + j] = fo[j];
+        okv[JB + j] = fo[j] && L.hfree;
     }
     if (L.h == 0) sts_pair_if(bi + ((fl >> 13) & 15u) * kCS, hh, 0.0, 0.0, RS, true);   // pivot Y
     __syncwarp();
@@ -346,17 +347,17 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
 // One item (gang) of a warp with JB back entries per lane: fill the lane's TMEM
 // rows from the seed block, the k + 1 seed pseudo-steps, then Upsilon(k).
 template <int JB, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* src, int k, int SA, int NB,
+__device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* src, int k, int SA, int NB, int b0,
                                        const uint4* __restrict__ wsteps, int nsteps)
 {
     if constexpr (JB > 0) {
-        // back slot b = 4j + h of worker w, row l: seed block [w][l][slot] at ((w k + l) SA + k + b) * 16
-        const unsigned char* bs = src + ((size_t)(L.w * k) * SA + k + L.h) * 16;
+        // back slot b = b0 + 4j + h of worker w, row l: seed block [w][l][slot] at ((w k + l) SA + k + b) * 16
+        const unsigned char* bs = src + ((size_t)(L.w * k) * SA + k + b0 + L.h) * 16;
         for (int l = 0; l < k; l += 2) {
             uint32_t v0[4 * JB], v1[4 * JB];
 #pragma unroll
             for (int j = 0; j < JB; ++j) {
-                const bool ok = L.live && (4 * j + L.h < NB);
+                const bool ok = L.live && (b0 + 4 * j + L.h < NB);
                 uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
                 if (ok) {
                     a = __ldg((const uint4*)(bs + ((size_t)l * SA + 4 * j) * 16));
@@ -488,7 +489,12 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         const int item = P.item_begin + (int)s_item;
         __syncthreads();
         if (item >= P.item_end) break;
-        const uint32_t pack = P.packs[item];    // the gang's tree levels (gang bits 0)
+        // split items (back slots beyond the 16 of a 4-entry TMEM lane): the entry
+        // 0x80000000 | a of the item list is a second pass over item a's back slots 16..
+        const uint32_t pk = P.packs[item];
+        const bool passB = (pk >> 31) != 0;
+        const int aitem = passB ? (int)(pk & 0x7fffffffu) : item;
+        const uint32_t pack = passB ? P.packs[aitem] : pk;    // the gang's tree levels (gang bits 0)
         uint32_t Ft = 0;                        // tree variables in F (user ids)
         int nBt = 0;
         for (int l = 0; l < gs; ++l) {
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         // ---- a5: this warp's seeds (seed kernel): worker-major blocks [w][row l][slot] of
         //      16 B E pairs; the free slots go to shared memory [l][f][w] (cp.async), the
         //      back slots to TMEM (walk_item)
-        const unsigned char* src = P.seeds + ((size_t)(item - P.item_begin) * G + wib) * (size_t)(k * SA * kW * 16);
+        const unsigned char* src = P.seeds + ((size_t)(aitem - P.item_begin) * G + wib) * (size_t)(k * SA * kW * 16);
         {
             const unsigned dst = L.sbase - w * 16;
             const int kk = k * k;
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
                 for (int ls = lane; ls < kk; ls += 32) {
                     const int l = ls / k, f = ls - l * k;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((l * k + f) * kW + ww) * 16),
-                                 "l"(src + ((size_t)(ww * k + l) * SA + f) * 16));
+                                 "l"(src + ((size_t)(ww * k + l) * Sw + f) * 16));
                 }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
@@ -550,33 +556,39 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         L.Fw = Ft | L.Xw;                       // the worker's F: tree, gang and warp variables
         L.KCw = KC + __popc(L.Fw);
         L.fh0 = (h - NB) & 3;
+        // pass A: back slots 0..min(NB, 16)-1 and the free entries; pass B (split items):
+        // back slots 16..NB-1 only (the free entries are rotated, not harvested)
+        const int b0 = passB ? 16 : 0;
+        const int nbp = passB ? NB - 16 : (JBMAX <= 4 ? min(NB, 16) : NB);
+        L.hfree = passB ? 0 : 1;
+        L.recB = L.recb + (unsigned)(k + b0 + h) * 16u;
         {
-            // back entry j = slot k + 4j + h: exists for b < NB; absent for this worker
-            // when it is warp or gang variable b (b < fv0) in F
+            // back entry j = slot k + b0 + 4j + h: exists for b < b0 + nbp; absent for this
+            // worker when it is warp or gang variable b (b < fv0) in F
             uint32_t bv = 0;
             for (int j = 0; j < 8; ++j) {
-                const int b = 4 * j + h;
-                if (L.live && b < NB && !(b < fv0 && ((L.Xw >> b) & 1u))) bv |= 1u << j;
+                const int b = b0 + 4 * j + h;
+                if (L.live && b < b0 + nbp && !(b < fv0 && ((L.Xw >> b) & 1u))) bv |= 1u << j;
             }
             L.bval = bv;
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
 
-        const int JB = (NB + 3) >> 2;
+        const int JB = (nbp + 3) >> 2;
         switch (JB) {
-            case 0: walk_item<0, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 1: walk_item<1, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 2: walk_item<2, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
-            case 3: walk_item<3, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps); break;
+            case 0: walk_item<0, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 1: walk_item<1, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 2: walk_item<2, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 3: walk_item<3, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
             default:
                 if constexpr (JBMAX <= 4) {
-                    walk_item<4, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
+                    walk_item<4, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
                 } else {
-                    if (JB == 4) walk_item<4, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
-                    else if (JB == 5) walk_item<5, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
-                    else if (JB == 6) walk_item<6, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
-                    else walk_item<7, HR, HB, HP>(L, src, k, SA, NB, wsteps, nsteps);
+                    if (JB == 4) walk_item<4, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else if (JB == 5) walk_item<5, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else if (JB == 6) walk_item<6, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else walk_item<7, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
                 }
                 break;
         }

@@ -623,3 +623,22 @@ def test_walk7_parity(case):
         _check_full(datagen.dag_data(6, 40, 0.3, 0.5, 2.0, seed=6), bn.options(free_vars=2, pack_bits=5))
     else:
         _check_full(datagen.config_data(3), bn.options(pack_bits=5), o2=True, pairs=True)
+
+
+def test_split_items_cfg3_k3():
+    """Items with more than 16 back slots (the default walk's TMEM holds 4 back entries x 4
+    lanes per warp) run as two passes (the second over back slots 16..): cfg3 with k = 3
+    (m = 20, 17 pinned variables: up to 17 back slots per gang) against the full O2 table,
+    both layouts, exact argmax; and the same with the split disabled (two launch classes)."""
+    import os
+    bn = _bn()
+    X = datagen.config_data(3)
+    info = bn.bnreg_plan_query(20, X.shape[0], bn.options(free_vars=3))
+    assert info["p"] + info["g"] + (info["bh"] - info["g"]) > 16     # some items are split
+    _check_full(X, bn.options(free_vars=3), o2=True, pairs=True)
+    _check_full(X, bn.options(free_vars=3), o2=True, pairs=False)
+    os.environ["BNREG_NO_SPLIT"] = "1"
+    try:
+        _check_full(X, bn.options(free_vars=3), o2=True, pairs=True)
+    finally:
+        del os.environ["BNREG_NO_SPLIT"]

@@ -26,7 +26,8 @@ import datagen, paper_1901_07643_b200 as bn
 cases = [("cfg1", datagen.config_data(1), dict(free_vars=4)),
          ("m12", datagen.dag_data(12, 200, 0.25, 0.5, 2.0, seed=12), dict(free_vars=3, levels_in_warp=1)),
          ("cfg2", datagen.config_data(2), {}),
-         ("cfg3", datagen.config_data(3), {})]
+         ("cfg3", datagen.config_data(3), {}),
+         ("cfg3_k3", datagen.config_data(3), dict(free_vars=3))]   # split items (17 back slots)
 checked = 0
 for name, X, kw in cases:
     n, m = X.shape
