@@ -59,6 +59,9 @@ def parse():
                     help="diagnostic (one GPU, no collectives): run logical rank --sim-rank of a world of this size "
                          "(its shard of the lattice, rank-filtered seed tree) to measure per-rank costs")
     ap.add_argument("--sim-rank", type=int, default=0)
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="load each dataset on the walk's stream (no overlap of dataset s+1's load and seed "
+                         "tree with dataset s's walk)")
     return ap.parse_args()
 
 
@@ -260,10 +263,15 @@ class Pipeline:
                                                          [comm + bnreg_best_merge_async]
     No host synchronisation inside a device step; load errors surface at sync()."""
 
-    def __init__(self, bn, h, X, world, rank, dev, comm=None, pairs=True, outputs="both"):
+    def __init__(self, bn, h, X, world, rank, dev, comm=None, pairs=True, outputs="both", load_stream=None):
         import numpy as np
         import torch
         self.bn, self.h, self.world, self.rank, self.comm = bn, h, world, rank, comm
+        # pipelined datasets: the load (and the R broadcast) of the next dataset on load_stream
+        # while the current one is walked (bnreg_set_load_stream)
+        self.load_stream = load_stream
+        if load_stream is not None:
+            h.set_load_stream(load_stream.cuda_stream)
         n, m = X.shape
         self.m = m
         F = h.num_families()
@@ -290,11 +298,15 @@ class Pipeline:
 
     def _exchange_root(self):
         if self.world > 1:
-            if self.rank == 0:
-                self.h.get_root_device(self.Rt)
-            self.comm.broadcast(self.Rt, 0)
-            if self.rank != 0:
-                self.h.set_root_device(self.Rt)
+            import contextlib
+            import torch
+            ctx = torch.cuda.stream(self.load_stream) if self.load_stream is not None else contextlib.nullcontext()
+            with ctx:
+                if self.rank == 0:
+                    self.h.get_root_device(self.Rt)
+                self.comm.broadcast(self.Rt, 0)
+                if self.rank != 0:
+                    self.h.set_root_device(self.Rt)
 
     def _walk(self):
         bm, bb = self._rec_ptrs(self.rec.data_ptr())
@@ -368,7 +380,9 @@ def bench_ours(args):
     F = h.num_families()
     total = m << (m - 1)
     pairs = args.layout == "pairs" and args.outputs == "both"
-    pipe = Pipeline(bn, h, X, world, rank, dev, NcclComm(dist) if world > 1 else None, pairs, args.outputs)
+    load_stream = None if args.no_pipeline else torch.cuda.Stream(dev)
+    pipe = Pipeline(bn, h, X, world, rank, dev, NcclComm(dist) if world > 1 else None, pairs, args.outputs,
+                    load_stream)
     step_device, step_e2e = pipe.step_device, pipe.step_e2e
 
     def timed(step, k, w, with_clocks=False):
@@ -384,6 +398,8 @@ def bench_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        if load_stream is not None:
+            load_stream.wait_event(e0)          # every timed load starts after e0
         for _ in range(k):
             step()
         e1.record(stream)
@@ -460,6 +476,9 @@ def bench_ours(args):
                           "seed": args.seed if args.seed is not None else 1000 * args.config + 1,
                           "families": total, "k": plan["k"], "pinned": plan["b"], "tree_levels_global": plan["L1"],
                           "packs": plan["npacks"], "parallelism": f"lattice-sharded x{world}",
+                          "pipeline": ("dataset s+1 loaded (H2D, centre, root QR, R broadcast, seed tree) on a "
+                                       "second stream while dataset s is walked" if load_stream is not None
+                                       else "none"),
                           "layout": ("(RSS, BIC) 16 B records, one table (bnreg_run_pairs)" if pairs else
                                      "separate RSS and BIC tables (bnreg_run)"),
                           "l2": "outputs (16 B/family, %.1f GB) >> L2 126 MB: every step evicts L2" % (

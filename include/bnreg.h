@@ -92,8 +92,16 @@ bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device);
  * BNREG_E_RANK; work enqueued in between computes on the rejected data. */
 bnreg_status bnreg_load_async(bnreg_t* h, const double* X, int32_t x_on_device);
 
-/* Wait for the handle's stream; report a CUDA error or a deferred load error. */
+/* Wait for the handle's stream(s); report a CUDA error or a deferred load error. */
 bnreg_status bnreg_sync(bnreg_t* h);
+
+/* Pipelined datasets: run later loads (bnreg_load / bnreg_load_async / bnreg_set_root_device:
+ * the H2D copy, centring, the root QR) and the seed tree of the following run on this
+ * second CUDA stream, so that dataset s+1 is prepared while dataset s is walked.  The load
+ * waits (on the device) until the previous run's seed kernel has consumed the root and the
+ * tree; the next run waits until the load is done.  NULL = loads on the handle's stream
+ * (the default, no overlap).  Synchronises with the previous load stream. */
+bnreg_status bnreg_set_load_stream(bnreg_t* h, void* stream);
 
 /* Number of table entries this handle writes: m 2^(m-1), or this rank's share. */
 int64_t bnreg_num_families(const bnreg_t* h);

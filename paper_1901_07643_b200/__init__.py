@@ -27,7 +27,8 @@ _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNR
           5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
-SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", "bnreg_sync", "bnreg_best_merge_async", "bnreg_num_families", "bnreg_index",
+SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", "bnreg_sync", "bnreg_best_merge_async",
+           "bnreg_set_load_stream", "bnreg_num_families", "bnreg_index",
            "bnreg_local_index", "bnreg_run", "bnreg_run_async", "bnreg_run_pairs", "bnreg_run_pairs_async", "bnreg_set_score", "bnreg_coefficients", "bnreg_coefficients_batch", "bnreg_best_subsets", "bnreg_set_root_method",
            "bnreg_all_rss", "bnreg_bic",
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
@@ -75,6 +76,7 @@ def lib():
         "bnreg_load": ([H, P, i32], i32),
         "bnreg_load_async": ([H, P, i32], i32),
         "bnreg_sync": ([H], i32),
+        "bnreg_set_load_stream": ([H, P], i32),
         "bnreg_best_merge_async": ([H, i32, P, P, i64, P, P], i32),
         "bnreg_num_families": ([H], i64),
         "bnreg_index": ([i32, i32, u32], i64),
@@ -301,6 +303,11 @@ class Bnreg:
 
     def set_stream(self, stream_handle: int | None):
         _check(lib().bnreg_set_stream(self._h, stream_handle))
+
+    def set_load_stream(self, stream_handle: int | None):
+        """bnreg_set_load_stream: prepare the next dataset (load + seed tree) on this stream
+        while the current one is walked (None: loads on the handle's stream)."""
+        _check(lib().bnreg_set_load_stream(self._h, stream_handle))
 
     def root_r(self):
         R = np.zeros((self.m, self.m))

@@ -87,6 +87,12 @@ struct bnreg {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     double acc_ms[6] = {0, 0, 0, 0, 0, 0};   // run, seeds, walk, reduce, load (centre + root QR), loads
     cudaEvent_t evl[2] = {nullptr, nullptr};
+    // pipelined loads (bnreg_set_load_stream): load + seed tree of the next dataset on a
+    // second stream, overlapping the current walk
+    cudaStream_t load_stream = nullptr;
+    cudaEvent_t ev_seeds = nullptr;   // run stream: the seed kernel has consumed d_root / d_nodes
+    cudaEvent_t ev_prep = nullptr;    // load stream: root R and seed tree of the next run are ready
+    bool prepared = false;
     bool load_timed = false;       // a timed load is waiting to be collected
     int64_t runs = 0;
     // walk kernel: one launch per shared-memory class of work items
@@ -136,6 +142,8 @@ static void free_all(bnreg* h)
         if (e) cudaEventDestroy(e);
     for (auto& e : h->evl)
         if (e) cudaEventDestroy(e);
+    if (h->ev_seeds) cudaEventDestroy(h->ev_seeds);
+    if (h->ev_prep) cudaEventDestroy(h->ev_prep);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     if (h->h_status) cudaFreeHost(h->h_status);
 }
@@ -405,6 +413,8 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     }
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
     for (auto& e : h->evl) CKH(cudaEventCreate(&e));
+    CKH(cudaEventCreateWithFlags(&h->ev_seeds, cudaEventDisableTiming));
+    CKH(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
 #undef CKH
     *out = h;
     return BNREG_OK;
@@ -432,31 +442,73 @@ bnreg_status bnreg_set_stream(bnreg_t* h, void* stream)
     return BNREG_OK;
 }
 
+// a5: the seed tree's nodes at depth L1 (one launch; BNREG_TREE_LEVELS=1: level by level)
+static const double* seed_tree_nodes(const bnreg_t* h)
+{
+    const Plan& P = h->plan;
+    if (P.L1 <= 0) return h->d_root;
+    if (getenv("BNREG_TREE_LEVELS")) return h->d_nodes[(P.L1 - 1) & 1];
+    return h->d_nodes[0];
+}
+
+static bnreg_status launch_seed_tree(bnreg_t* h, cudaStream_t st)
+{
+    const Plan& P = h->plan;
+    if (P.L1 <= 0) return BNREG_OK;
+    if (getenv("BNREG_TREE_LEVELS")) {
+        for (int L = 0; L < P.L1; ++L) {
+            const double* par = (L == 0) ? h->d_root : h->d_nodes[(L - 1) & 1];
+            double* ch = h->d_nodes[L & 1];
+            CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
+        }
+    } else {
+        // multi-GPU: only the nodes above this rank's work items (its two selector patterns)
+        const uint32_t t0 = (uint32_t)P.rank, t1 = ((1u << P.r) - 1u) ^ (uint32_t)P.rank;
+        CK(launch_tree_direct(h->d_root, h->d_nodes[0], P.m, P.L1, P.bh, P.p, P.k, P.world > 1 ? P.r : 0, t0, t1, st));
+    }
+    return BNREG_OK;
+}
+
+// pipelined mode: after the root R is in place on the load stream, build the seed tree there too
+static bnreg_status prepare_on_load_stream(bnreg_t* h)
+{
+    bnreg_status s = launch_seed_tree(h, h->load_stream);
+    if (s != BNREG_OK) return s;
+    CK(cudaEventRecord(h->ev_prep, h->load_stream));
+    h->prepared = true;
+    return BNREG_OK;
+}
+
 // a1-a2 enqueued on the handle's stream; the status flags land in d_status
 static bnreg_status load_enqueue(bnreg_t* h, const double* X, int32_t x_on_device)
 {
     const Plan& P = h->plan;
     const size_t nm = (size_t)P.n * P.m;
     const double* src = X;
+    // pipelined mode: the load (and the seed tree) run on the load stream once the previous
+    // run's seed kernel has consumed the root and the tree
+    cudaStream_t ls = h->load_stream ? h->load_stream : h->stream;
+    if (h->load_stream) CK(cudaStreamWaitEvent(ls, h->ev_seeds, 0));
     if (!x_on_device) {
-        CK(cudaMemcpyAsync(h->dX, X, nm * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->dX, X, nm * sizeof(double), cudaMemcpyHostToDevice, ls));
         src = h->dX;
     }
-    if (h->timing) CK(cudaEventRecord(h->evl[0], h->stream));
-    CK(cudaMemsetAsync(h->d_status, 0, sizeof(int), h->stream));
-    CK(launch_centre(src, P.n, P.m, h->d_order, h->dXr, h->d_status, h->stream));
+    if (h->timing) CK(cudaEventRecord(h->evl[0], ls));
+    CK(cudaMemsetAsync(h->d_status, 0, sizeof(int), ls));
+    CK(launch_centre(src, P.n, P.m, h->d_order, h->dXr, h->d_status, ls));
     if (h->root_method == 1) {
         if (!h->d_gram) CK(cudaMalloc(&h->d_gram, (size_t)P.m * P.m * sizeof(double)));
-        CK(launch_gram_chol(h->dXr, P.n, P.m, h->d_gram, h->d_root, h->d_status, h->stream));
+        CK(launch_gram_chol(h->dXr, P.n, P.m, h->d_gram, h->d_root, h->d_status, ls));
     } else {
-        CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, h->stream));
+        CK(launch_tsqr(h->dXr, P.n, P.m, h->d_rbuf, h->d_tcnt, h->nleaf2, h->rb, h->d_root, h->d_status, ls));
     }
     if (h->timing) {
-        CK(cudaEventRecord(h->evl[1], h->stream));
+        CK(cudaEventRecord(h->evl[1], ls));
         h->load_timed = true;
     }
-    CK(cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int), cudaMemcpyDeviceToHost, ls));
     h->ran = false;
+    if (h->load_stream) return prepare_on_load_stream(h);
     return BNREG_OK;
 }
 
@@ -479,7 +531,7 @@ bnreg_status bnreg_load(bnreg_t* h, const double* X, int32_t x_on_device)
     h->loaded = false;
     bnreg_status s = load_enqueue(h, X, x_on_device);
     if (s != BNREG_OK) return s;
-    CK(stream_wait(h->stream));
+    CK(stream_wait(h->load_stream ? h->load_stream : h->stream));
     h->loaded = true;
     return load_status(h);
 }
@@ -500,6 +552,7 @@ bnreg_status bnreg_load_async(bnreg_t* h, const double* X, int32_t x_on_device)
 bnreg_status bnreg_sync(bnreg_t* h)
 {
     if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (h->load_stream) CK(stream_wait(h->load_stream));
     CK(stream_wait(h->stream));
     CK(cudaGetLastError());
     if (h->pending) return load_status(h);
@@ -511,7 +564,8 @@ bnreg_status bnreg_get_root_device(bnreg_t* h, double* R_dev)
     if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
     const int m = h->plan.m;
-    CK(cudaMemcpyAsync(R_dev, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(R_dev, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice,
+                       h->load_stream ? h->load_stream : h->stream));
     return BNREG_OK;
 }
 
@@ -519,10 +573,22 @@ bnreg_status bnreg_set_root_device(bnreg_t* h, const double* R_dev)
 {
     if (!h || !R_dev) return fail(BNREG_E_INVAL, "NULL argument");
     const int m = h->plan.m;
-    CK(cudaMemcpyAsync(h->d_root, R_dev, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    cudaStream_t ls = h->load_stream ? h->load_stream : h->stream;
+    if (h->load_stream) CK(cudaStreamWaitEvent(ls, h->ev_seeds, 0));
+    CK(cudaMemcpyAsync(h->d_root, R_dev, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, ls));
     h->loaded = true;
     h->pending = false;    // the sender checked its data
     h->ran = false;
+    if (h->load_stream) return prepare_on_load_stream(h);
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_set_load_stream(bnreg_t* h, void* stream)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (h->load_stream) CK(stream_wait(h->load_stream));
+    h->load_stream = (cudaStream_t)stream;
+    h->prepared = false;
     return BNREG_OK;
 }
 
@@ -532,6 +598,7 @@ bnreg_status bnreg_root_r(const bnreg_t* h, double* R_host, int32_t* order_host)
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
     const int m = h->plan.m;
     if (R_host) {
+        if (h->load_stream) CK(stream_wait(h->load_stream));
         CK(stream_wait(h->stream));
         CK(cudaMemcpy(R_host, h->d_root, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost));
     }
@@ -621,23 +688,14 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     const Plan& P = h->plan;
     cudaStream_t st = h->stream;
     if (h->timing) CK(cudaEventRecord(h->ev[0], st));
-    // a5: the seed tree's nodes at depth L1 (one launch; BNREG_TREE_LEVELS=1: level by level)
-    const double* nodes = h->d_root;
-    if (P.L1 > 0) {
-        if (getenv("BNREG_TREE_LEVELS")) {
-            for (int L = 0; L < P.L1; ++L) {
-                const double* par = (L == 0) ? h->d_root : h->d_nodes[(L - 1) & 1];
-                double* ch = h->d_nodes[L & 1];
-                CK(launch_tree_level(par, ch, P.m, L, P.bh, P.p, P.k, st));
-                nodes = ch;
-            }
-        } else {
-            // multi-GPU: only the nodes above this rank's work items (its two selector patterns)
-            const uint32_t t0 = (uint32_t)P.rank, t1 = ((1u << P.r) - 1u) ^ (uint32_t)P.rank;
-            CK(launch_tree_direct(h->d_root, h->d_nodes[0], P.m, P.L1, P.bh, P.p, P.k, P.world > 1 ? P.r : 0, t0, t1,
-                                  st));
-            nodes = h->d_nodes[0];
-        }
+    // a5: the seed tree's nodes at depth L1 (already built on the load stream after a pipelined load)
+    const double* nodes = seed_tree_nodes(h);
+    if (h->prepared) {
+        CK(cudaStreamWaitEvent(st, h->ev_prep, 0));
+        h->prepared = false;
+    } else {
+        const bnreg_status ts = launch_seed_tree(h, st);
+        if (ts != BNREG_OK) return ts;
     }
     TravParams T{};
     T.m = P.m; T.k = P.k; T.p = P.p; T.bh = P.bh; T.L1 = P.L1; T.nw = 1 << P.p; T.g = P.g; T.lw = P.lw;
@@ -681,6 +739,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     } else {
         CK(launch_seed(SP, st));
     }
+    if (h->load_stream) CK(cudaEventRecord(h->ev_seeds, st));   // the next load may overwrite root and tree
     if (h->timing) CK(cudaEventRecord(h->ev[1], st));
     // a6-a11: the walk, one launch per shared-memory class
     for (size_t c = 0; c < h->classes.size(); ++c) {
@@ -826,6 +885,7 @@ bnreg_status bnreg_coefficients(bnreg_t* h, const uint32_t* masks, double* beta)
         CK(cudaMemcpyAsync(h->d_cmask, masks, (size_t)m * sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream));
         dm = h->d_cmask;
     }
+    if (h->load_stream) CK(cudaStreamWaitEvent(h->stream, h->ev_prep, 0));   // a pipelined load's root
     CK(launch_coefficients(h->d_root, h->d_order, m, nullptr, dm, m, h->d_coef, h->stream));
     CK(cudaMemcpyAsync(beta, h->d_coef, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(stream_wait(h->stream));
@@ -839,6 +899,7 @@ bnreg_status bnreg_coefficients_batch(bnreg_t* h, const int32_t* children, const
     if (count < 0) return fail(BNREG_E_INVAL, "negative count");
     if (count > 0 && (!children || !masks || !beta)) return fail(BNREG_E_INVAL, "NULL children, masks or beta");
     if (!h->loaded) return fail(BNREG_E_STATE, "no data loaded");
+    if (h->load_stream) CK(cudaStreamWaitEvent(h->stream, h->ev_prep, 0));
     CK(launch_coefficients(h->d_root, h->d_order, h->plan.m, children, masks, count, beta, h->stream));
     return BNREG_OK;
 }

@@ -161,7 +161,10 @@ def _gloo_worker(rank, world, port, cfg, outdir):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     h.set_stream(stream.cuda_stream)
-    pipe = bench.Pipeline(bn, h, X, world, rank, dev, bench.HostStagedComm(dist), pairs=True)
+    # pipelined like the bench (the next dataset's load and R broadcast on a second stream)
+    pipe = bench.Pipeline(bn, h, X, world, rank, dev, bench.HostStagedComm(dist), pairs=True,
+                          load_stream=torch.cuda.Stream(dev))
+    pipe.step_device()
     pipe.step_device()
     pipe.h.sync()
     bm1, bb1 = pipe.best_mask.cpu().numpy().view(np.uint32), pipe.best_bic.cpu().numpy()
@@ -207,3 +210,47 @@ def test_bench_pipeline_two_processes_gloo(tmp_path):
             np.testing.assert_array_equal(d[key_b], fbb)
     assert (seen == 1).all()
     torch.cuda.empty_cache()
+
+
+def test_pipelined_loads_bit_identical():
+    """bnreg_set_load_stream: three datasets loaded on a second stream while the previous
+    one is walked (load_async + run_pairs_async, no host synchronisation in between), on a
+    rank-0 handle that loads X and a rank-1 handle fed by set_root_device: every table is
+    bit-identical to the same dataset run without pipelining."""
+    import torch
+    import paper_1901_07643_b200 as bn
+    datasets = [datagen.config_data(2, seed=2001 + i) for i in range(3)]
+    n, m = datasets[0].shape
+    ref = []
+    for X in datasets:
+        t, _, _ = _full_pairs(bn, X)
+        ref.append(t)
+    for world in (1, 2):
+        hs = [bn.Bnreg(n, m, bn.options(world=world, rank=r)) for r in range(world)]
+        run_st = torch.cuda.Stream()
+        load_st = torch.cuda.Stream()
+        for h in hs:
+            h.set_stream(run_st.cuda_stream)
+            h.set_load_stream(load_st.cuda_stream)
+        Rt = torch.empty(m * m, dtype=torch.float64, device="cuda")
+        Xd = [torch.from_numpy(np.ascontiguousarray(X.T)).cuda() for X in datasets]
+        outs = [[torch.full((h.num_families(), 2), float("nan"), dtype=torch.float64, device="cuda") for h in hs]
+                for _ in datasets]
+        torch.cuda.synchronize()
+        for i in range(len(datasets)):
+            hs[0].load_async(Xd[i])
+            if world > 1:
+                hs[0].get_root_device(Rt)
+                hs[1].set_root_device(Rt)      # both on the load stream, after the rank-0 load
+            for h, o in zip(hs, outs[i]):
+                h.run_pairs_async(o)
+        for h in hs:
+            h.sync()
+        torch.cuda.synchronize()
+        for i in range(len(datasets)):
+            for h, o in zip(hs, outs[i]):
+                starts, lens = h.shard_ranges()
+                gidx = torch.cat([torch.arange(s0, s0 + l, device="cuda") for s0, l in zip(starts, lens)])
+                assert torch.equal(o, ref[i][gidx]), (world, i)
+        for h in hs:
+            h.close()
