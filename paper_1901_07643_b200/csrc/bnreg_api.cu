@@ -110,6 +110,10 @@ struct bnreg {
     uint32_t* d_cmask = nullptr;       // bnreg_coefficients input masks
     uint4* d_wsteps = nullptr;     // per-class walk step tables (plan.h WalkStep)
     unsigned char* d_seeds = nullptr;   // seed kernel output: per class, one walk-state block per (item, warp)
+    unsigned char* d_seeds2 = nullptr;  // pipelined mode: the second buffer (dataset s+1's seeds while s walks)
+    size_t seed_bytes = 0;
+    int cur_buf = 0;                    // the buffer the next / last walk reads
+    cudaEvent_t ev_walk[2] = {nullptr, nullptr};   // a walk reading buffer b has finished
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
     size_t wsteps_len = 0;         // steps per class table
     // walk7 (32 lockstep workers per warp; P.lw == 5)
@@ -135,7 +139,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram};
+                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram, h->d_seeds2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -143,6 +147,8 @@ static void free_all(bnreg* h)
     for (auto& e : h->evl)
         if (e) cudaEventDestroy(e);
     if (h->ev_seeds) cudaEventDestroy(h->ev_seeds);
+    for (auto& e : h->ev_walk)
+        if (e) cudaEventDestroy(e);
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     if (h->h_status) cudaFreeHost(h->h_status);
@@ -273,7 +279,8 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         h->nparts = c.grid * warps;
         h->classes.push_back(c);
         h->seed_off.push_back(0);
-        CKH(cudaMalloc(&h->d_seeds, std::max<size_t>((size_t)ni * h->w7_sblk * sizeof(double), 16)));
+        h->seed_bytes = std::max<size_t>((size_t)ni * h->w7_sblk * sizeof(double), 16);
+        CKH(cudaMalloc(&h->d_seeds, h->seed_bytes));
         CKH(cudaMalloc(&h->d_counters, sizeof(unsigned)));
         const auto recs = step_records(P.k, P.sched);
         h->wsteps_len = recs.size();
@@ -316,7 +323,8 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
             CKH(cudaMemcpy(h->d_packs, items.data(), items.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
         }
         h->seed_off.push_back(0);
-        CKH(cudaMalloc(&h->d_seeds, std::max<size_t>((size_t)na * (size_t)h->wpc * seed_block_bytes(P.k, S0, P.lw), 16)));
+        h->seed_bytes = std::max<size_t>((size_t)na * (size_t)h->wpc * seed_block_bytes(P.k, S0, P.lw), 16);
+        CKH(cudaMalloc(&h->d_seeds, h->seed_bytes));
         CKH(cudaMalloc(&h->d_counters, sizeof(unsigned)));
         const auto recs = step_records(P.k, P.sched);
         h->wsteps_len = recs.size();
@@ -360,7 +368,8 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
                 h->seed_off.push_back(off);
                 off += (size_t)(c.end - c.begin) * (size_t)h->wpc * seed_block_bytes(P.k, c.S_alloc, P.lw);
             }
-            CKH(cudaMalloc(&h->d_seeds, std::max<size_t>(off, 16)));
+            h->seed_bytes = std::max<size_t>(off, 16);
+            CKH(cudaMalloc(&h->d_seeds, h->seed_bytes));
         }
         if (getenv("BNREG_VERBOSE"))
             for (auto& c : h->classes)
@@ -414,6 +423,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     for (auto& e : h->ev) CKH(cudaEventCreate(&e));
     for (auto& e : h->evl) CKH(cudaEventCreate(&e));
     CKH(cudaEventCreateWithFlags(&h->ev_seeds, cudaEventDisableTiming));
+    for (auto& e : h->ev_walk) CKH(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CKH(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
 #undef CKH
     *out = h;
@@ -469,10 +479,42 @@ static bnreg_status launch_seed_tree(bnreg_t* h, cudaStream_t st)
     return BNREG_OK;
 }
 
+// a5: every pack's seeds into seed buffer `buf`, in the walk kernel's layout
+static bnreg_status launch_seeds(bnreg_t* h, cudaStream_t st, int buf)
+{
+    const Plan& P = h->plan;
+    const double* nodes = seed_tree_nodes(h);
+    SeedParams SP{};
+    SP.m = P.m; SP.k = P.k; SP.p = P.p; SP.bh = P.bh; SP.g = P.g; SP.L1 = P.L1; SP.nw = 1 << P.p; SP.lw = P.lw;
+    SP.nclass = (int)h->classes.size();
+    for (size_t c = 0; c < h->classes.size(); ++c) {
+        SP.cls_begin[c] = h->classes[c].begin;
+        SP.cls_end[c] = h->classes[c].end;
+        SP.cls_SA[c] = h->classes[c].S_alloc;
+        SP.cls_off[c] = h->seed_off[c];
+    }
+    SP.item_begin = 0;
+    SP.item_end = (int)P.packs.size();
+    SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = buf ? h->d_seeds2 : h->d_seeds;
+    if (h->w7) {
+        SP.TB = h->w7_TB; SP.nbmax = h->w7_nbmax; SP.sblk = h->w7_sblk;
+        CK(launch_seed7(SP, st));
+    } else {
+        CK(launch_seed(SP, st));
+    }
+    return BNREG_OK;
+}
+
 // pipelined mode: after the root R is in place on the load stream, build the seed tree there too
 static bnreg_status prepare_on_load_stream(bnreg_t* h)
 {
     bnreg_status s = launch_seed_tree(h, h->load_stream);
+    if (s != BNREG_OK) return s;
+    // the seeds of this dataset go to the buffer the current walk does not read; the walk
+    // that read it last (two runs ago) must be done
+    const int b = 1 - h->cur_buf;
+    CK(cudaStreamWaitEvent(h->load_stream, h->ev_walk[b], 0));
+    s = launch_seeds(h, h->load_stream, b);
     if (s != BNREG_OK) return s;
     CK(cudaEventRecord(h->ev_prep, h->load_stream));
     h->prepared = true;
@@ -587,8 +629,12 @@ bnreg_status bnreg_set_load_stream(bnreg_t* h, void* stream)
 {
     if (!h) return fail(BNREG_E_INVAL, "NULL handle");
     if (h->load_stream) CK(stream_wait(h->load_stream));
+    if (h->prepared) CK(cudaStreamWaitEvent(h->stream, h->ev_prep, 0));
+    CK(stream_wait(h->stream));
+    if (stream && !h->d_seeds2) CK(cudaMalloc(&h->d_seeds2, h->seed_bytes));
     h->load_stream = (cudaStream_t)stream;
     h->prepared = false;
+    h->cur_buf = 0;
     return BNREG_OK;
 }
 
@@ -689,10 +735,11 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     cudaStream_t st = h->stream;
     if (h->timing) CK(cudaEventRecord(h->ev[0], st));
     // a5: the seed tree's nodes at depth L1 (already built on the load stream after a pipelined load)
-    const double* nodes = seed_tree_nodes(h);
-    if (h->prepared) {
+    const bool prepared = h->prepared;
+    if (prepared) {
         CK(cudaStreamWaitEvent(st, h->ev_prep, 0));
         h->prepared = false;
+        h->cur_buf = 1 - h->cur_buf;           // the buffer the load stream filled
     } else {
         const bnreg_status ts = launch_seed_tree(h, st);
         if (ts != BNREG_OK) return ts;
@@ -720,26 +767,13 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.k8_selftest = getenv("BNREG_K8_SELFTEST") ? 1 : 0;
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
     CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
-    // a5: every pack's seeds, in the walk kernel's layout
-    SeedParams SP{};
-    SP.m = P.m; SP.k = P.k; SP.p = P.p; SP.bh = P.bh; SP.g = P.g; SP.L1 = P.L1; SP.nw = 1 << P.p; SP.lw = P.lw;
-    SP.nclass = (int)h->classes.size();
-    for (size_t c = 0; c < h->classes.size(); ++c) {
-        SP.cls_begin[c] = h->classes[c].begin;
-        SP.cls_end[c] = h->classes[c].end;
-        SP.cls_SA[c] = h->classes[c].S_alloc;
-        SP.cls_off[c] = h->seed_off[c];
+    // a5: every pack's seeds, in the walk kernel's layout (already derived on the load stream
+    //     after a pipelined load)
+    if (!prepared) {
+        const bnreg_status ss = launch_seeds(h, st, h->cur_buf);
+        if (ss != BNREG_OK) return ss;
     }
-    SP.item_begin = 0;
-    SP.item_end = (int)P.packs.size();
-    SP.nodes = nodes; SP.packs = h->d_packs; SP.seeds = h->d_seeds;
-    if (h->w7) {
-        SP.TB = h->w7_TB; SP.nbmax = h->w7_nbmax; SP.sblk = h->w7_sblk;
-        CK(launch_seed7(SP, st));
-    } else {
-        CK(launch_seed(SP, st));
-    }
-    if (h->load_stream) CK(cudaEventRecord(h->ev_seeds, st));   // the next load may overwrite root and tree
+    if (h->load_stream && !prepared) CK(cudaEventRecord(h->ev_seeds, st));   // the next load may overwrite root and tree
     if (h->timing) CK(cudaEventRecord(h->ev[1], st));
     // a6-a11: the walk, one launch per shared-memory class
     for (size_t c = 0; c < h->classes.size(); ++c) {
@@ -752,7 +786,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         T.item_end = C.end;
         T.part_base = C.part_base;
         T.wsteps = h->d_wsteps + c * h->wsteps_len;
-        T.seeds = h->d_seeds + h->seed_off[c];
+        T.seeds = (h->cur_buf ? h->d_seeds2 : h->d_seeds) + h->seed_off[c];
         if (h->w7) {
             T.KA = h->w7_KA; T.TB = h->w7_TB; T.nbmax = h->w7_nbmax; T.sblk = h->w7_sblk;
             CK(launch_walk7(T, C.grid, h->w7_warps, st));
@@ -760,6 +794,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
             CK(launch_walk(T, C.grid, st));
         }
     }
+    CK(cudaEventRecord(h->ev_walk[h->cur_buf], st));   // buffer cur_buf may be refilled after this
     if (h->timing) CK(cudaEventRecord(h->ev[2], st));
     // the handle keeps its own copy of the best masks whatever the caller's target
     // (bnreg_coefficients with masks NULL reads it)
