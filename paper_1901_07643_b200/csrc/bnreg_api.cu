@@ -114,6 +114,8 @@ struct bnreg {
     size_t seed_bytes = 0;
     int cur_buf = 0;                    // the buffer the next / last walk reads
     cudaEvent_t ev_walk[2] = {nullptr, nullptr};   // a walk reading buffer b has finished
+    unsigned long long* d_trace = nullptr;          // BNREG_TRACE diagnostic
+    long long* d_gbest = nullptr;                   // per child: the best BIC any warp has found (bic_ord)
     std::vector<size_t> seed_off;       // byte offset of each class's blocks
     size_t wsteps_len = 0;         // steps per class table
     // walk7 (32 lockstep workers per warp; P.lw == 5)
@@ -139,7 +141,7 @@ static void free_all(bnreg* h)
     if (!h) return;
     void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
-                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram, h->d_seeds2};
+                    h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram, h->d_seeds2, h->d_trace, h->d_gbest};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& e : h->ev)
@@ -405,6 +407,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         CKH(cudaMemcpy(h->d_part_mask, nm.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
     CKH(cudaMalloc(&h->d_best_bic, m * sizeof(double)));
+    CKH(cudaMalloc(&h->d_gbest, 2 * 32 * sizeof(long long)));   // one floor per seed buffer (pipelining)
     CKH(cudaMalloc(&h->d_best_mask, m * sizeof(uint32_t)));
     CKH(cudaMalloc(&h->d_status, sizeof(int)));
     CKH(cudaMallocHost(&h->h_status, sizeof(int)));
@@ -505,6 +508,21 @@ static bnreg_status launch_seeds(bnreg_t* h, cudaStream_t st, int buf)
     return BNREG_OK;
 }
 
+// the walk's shared candidate floor for the dataset whose root is in d_root (seed buffer `buf`)
+static bnreg_status gbest_init(bnreg_t* h, cudaStream_t st, int buf)
+{
+    const Plan& P = h->plan;
+    long long* g = h->d_gbest + 32 * buf;
+    if (getenv("BNREG_GBEST_NEGINF")) {
+        CK(cudaMemsetAsync(g, 0x80, 32 * sizeof(long long), st));
+    } else {
+        double K[33];
+        score_constants(P.n, h->score, K);
+        CK(launch_gbest_init(h->d_root, h->d_order, P.m, P.mhalf_n, K[0], g, st));
+    }
+    return BNREG_OK;
+}
+
 // pipelined mode: after the root R is in place on the load stream, build the seed tree there too
 static bnreg_status prepare_on_load_stream(bnreg_t* h)
 {
@@ -516,6 +534,10 @@ static bnreg_status prepare_on_load_stream(bnreg_t* h)
     CK(cudaStreamWaitEvent(h->load_stream, h->ev_walk[b], 0));
     s = launch_seeds(h, h->load_stream, b);
     if (s != BNREG_OK) return s;
+    if (!h->w7) {
+        s = gbest_init(h, h->load_stream, b);
+        if (s != BNREG_OK) return s;
+    }
     CK(cudaEventRecord(h->ev_prep, h->load_stream));
     h->prepared = true;
     return BNREG_OK;
@@ -596,6 +618,20 @@ bnreg_status bnreg_sync(bnreg_t* h)
     if (!h) return fail(BNREG_E_INVAL, "NULL handle");
     if (h->load_stream) CK(stream_wait(h->load_stream));
     CK(stream_wait(h->stream));
+    if (h->d_trace && !h->classes.empty()) {
+        // BNREG_TRACE: the last walk launch's per-CTA [start, end, items] relative to the first start
+        const int g = h->classes[0].grid;
+        std::vector<unsigned long long> t(3 * (size_t)g);
+        CK(cudaMemcpy(t.data(), h->d_trace, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull, t1 = 0;
+        for (int c = 0; c < g; ++c) { t0 = std::min(t0, t[3 * c]); t1 = std::max(t1, t[3 * c + 1]); }
+        std::vector<double> ends, starts;
+        for (int c = 0; c < g; ++c) { ends.push_back((t[3 * c + 1] - t0) * 1e-6); starts.push_back((t[3 * c] - t0) * 1e-6); }
+        std::sort(ends.begin(), ends.end());
+        std::sort(starts.begin(), starts.end());
+        fprintf(stderr, "walk trace: span %.3f ms; CTA starts max %.3f ms; CTA ends min %.3f p10 %.3f p50 %.3f p90 %.3f max %.3f ms\n",
+                (t1 - t0) * 1e-6, starts.back(), ends.front(), ends[g / 10], ends[g / 2], ends[9 * g / 10], ends.back());
+    }
     CK(cudaGetLastError());
     if (h->pending) return load_status(h);
     return BNREG_OK;
@@ -765,8 +801,22 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.k8 = h->k8;
     T.k8_n = (unsigned long long)P.local_families;
     T.k8_selftest = getenv("BNREG_K8_SELFTEST") ? 1 : 0;
+    if (getenv("BNREG_TRACE")) {
+        // diagnostic: per-CTA start / end times of the walk launch, printed at the next sync
+        if (!h->d_trace) CK(cudaMalloc(&h->d_trace, 3 * 4096 * sizeof(unsigned long long)));
+        T.trace = h->d_trace;
+    }
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable
     CK(cudaMemsetAsync(h->d_counters, 0, std::max<size_t>(1, h->classes.size()) * sizeof(unsigned), st));
+    // the shared candidate floor starts below every BIC (bytes 0x80: bic_ord of about -7e305)
+    if (!h->w7 && !getenv("BNREG_NO_GBEST")) {
+        // (after a pipelined load the load stream has set this dataset's floor)
+        if (!prepared) {
+            const bnreg_status gs = gbest_init(h, st, h->cur_buf);
+            if (gs != BNREG_OK) return gs;
+        }
+        T.gbest = h->d_gbest + 32 * h->cur_buf;
+    }
     // a5: every pack's seeds, in the walk kernel's layout (already derived on the load stream
     //     after a pipelined load)
     if (!prepared) {

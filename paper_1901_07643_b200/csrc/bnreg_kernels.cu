@@ -315,6 +315,35 @@ __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restri
     }
 }
 
+// ---------------------------------------------------------------- a11 candidate floor
+// The shared floor of the walk's running-best thresholds starts at each child's empty-set
+// score (a family every run visits: RSS(v|{}) = ||x_v||^2 = the squared norm of R's column
+// of v, a12) less a margin far above its rounding, so it is below the child's maximum and
+// the argmax stays exact (G14); families worse than the empty set never take the
+// candidate path.
+__global__ void gbest_init_kernel(const double* __restrict__ R, const int* __restrict__ order, int m, double mhalf_n,
+                                  double K0, long long* gbest)
+{
+    const int pos = threadIdx.x;
+    if (pos >= 32) return;
+    if (pos >= m) {
+        gbest[pos] = bic_ord(-__longlong_as_double(0x7ff0000000000000LL));
+        return;
+    }
+    double s = 0.0;
+    for (int i = 0; i <= pos; ++i) s = fma(R[i * m + pos], R[i * m + pos], s);
+    const double b = fma(mhalf_n, log(s), K0);
+    const double fl = b - (1e-9 * fabs(b) + 1e-6);
+    gbest[order[pos]] = bic_ord(s > 1e-300 && isfinite(fl) ? fl : -__longlong_as_double(0x7ff0000000000000LL));
+}
+
+cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, double K0, long long* gbest,
+                              cudaStream_t st)
+{
+    gbest_init_kernel<<<1, 32, 0, st>>>(R, order, m, mhalf_n, K0, gbest);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev, double* Xr, int* status,
                           cudaStream_t st)

@@ -2,6 +2,7 @@
 // sm_100a kernels (bnreg_kernels.cu).  Plain structs, no torch types.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace bnr {
@@ -51,7 +52,24 @@ struct TravParams {
                                 // k8[k8_n] counts out-of-range accesses (table index, shared state, TMEM)
     unsigned long long k8_n;    // this rank's table entries
     int k8_selftest;            // BNREG_K8: lane 0 of every warp reports one deliberate violation
+    unsigned long long* trace;  // diagnostic (BNREG_TRACE): per CTA [start ns, end ns, items] or null
+    long long* gbest;           // per child: the best BIC any warp has found so far (order-preserving int64
+                                // of the double), a shared floor for the warps' candidate thresholds; or null
 };
+// order-preserving map of doubles to int64 (atomicMax on the running bests)
+__host__ __device__ inline long long bic_ord(double x)
+{
+    long long b;
+    memcpy(&b, &x, 8);
+    return b < 0 ? b ^ 0x7fffffffffffffffLL : b;
+}
+__host__ __device__ inline double bic_unord(long long o)
+{
+    const long long b = o < 0 ? o ^ 0x7fffffffffffffffLL : o;
+    double x;
+    memcpy(&x, &b, 8);
+    return x;
+}
 
 // seed kernel: one warp per pack derives its 2^p workers' seeds (the remaining
 // tree levels + the Gray path over the warp variables) and writes them in the
@@ -98,6 +116,9 @@ cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsign
 cudaError_t launch_gram_chol(const double* Xr, int64_t n, int m, double* G, double* Rroot, int* status,
                              cudaStream_t st);
 cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
+                              cudaStream_t st);
+// the walk's shared candidate floor: each child's empty-set score less a margin
+cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, double K0, long long* gbest,
                               cudaStream_t st);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, uint32_t* mask_copy, cudaStream_t st,

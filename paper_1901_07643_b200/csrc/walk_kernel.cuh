@@ -125,6 +125,7 @@ struct LaneC {
     double* out_rss;
     double* out_bic;
     double* out_pairs;
+    long long* gbest;    // per child: the best BIC found by any warp so far (bic_ord), or null
     unsigned* k8;        // BNREG_K8: write counters (+ the violation counter k8[k8_n])
     unsigned long long k8_n;
     unsigned sb0;        // BNREG_K8 bounds checks: the warp's shared state [sb0, sb0 + sbytes)
@@ -191,6 +192,12 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
                         asm volatile("st.shared.f64 [%0], %1;" ::"r"(ba), "d"(b) : "memory");
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
                         asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(fmin(b, L.tiny_bic)) : "memory");
+                        if (L.gbest) {
+                            // publish: every warp's later items take it as their candidate floor
+                            uint32_t lmv;
+                            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lmv) : "r"(a + 12));
+                            atomicMax(L.gbest + __popc(lmv), bic_ord(b));
+                        }
                     }
                 }
             }
@@ -468,6 +475,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     L.out_pairs = P.out_pairs;
     L.k8 = P.k8;
     L.k8_n = P.k8_n;
+    L.gbest = P.gbest;
     L.sb0 = (unsigned)__cvta_generic_to_shared(st);
     L.sbytes = (unsigned)(k * k * kW * 16);
     L.tmcols = (unsigned)P.tm_cols;
@@ -481,6 +489,8 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
     }
     const int nsteps = P.nsteps;
     const uint4* const wsteps = P.wsteps;
+    unsigned long long t_start = 0, n_items = 0;
+    if (P.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     __syncthreads();
 
     for (;;) {
@@ -489,6 +499,7 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         const int item = P.item_begin + (int)s_item;
         __syncthreads();
         if (item >= P.item_end) break;
+        ++n_items;
         // split items (back slots beyond the 16 of a 4-entry TMEM lane): the entry
         // 0x80000000 | a of the item list is a second pass over item a's back slots 16..
         const uint32_t pk = P.packs[item];
@@ -547,7 +558,10 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
                                           : block_offset<false>(P, Ft, Ft >> 1, lm);
             const uint32_t idx = (uint32_t)((long long)v << shb) + off;
             unsigned char* r = recb + lane * 16;
-            *(double*)r = fmin(wbb[v], P.tiny_bic);
+            // candidate threshold: this warp's best so far, floored by the best any warp has
+            // found (a family's BIC: <= the child's maximum, so the argmax stays exact, G14)
+            const double gb = P.gbest ? bic_unord(((volatile long long*)P.gbest)[v]) : wbb[v];
+            *(double*)r = fmin(fmax(wbb[v], gb), P.tiny_bic);
             bbv[lane] = wbb[v];
             *(uint32_t*)(r + 8) = idx;
             *(uint32_t*)(r + 12) = lm;
@@ -601,6 +615,13 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
         __syncwarp();
     }
     __syncwarp();
+    if (P.trace && tid == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        P.trace[3 * blockIdx.x] = t_start;
+        P.trace[3 * blockIdx.x + 1] = t_end;
+        P.trace[3 * blockIdx.x + 2] = n_items;
+    }
     if (lane < m) {
         const size_t row = (size_t)P.part_base + (size_t)blockIdx.x * G + wib;
         P.part_bic[row * m + lane] = wbb[lane];
