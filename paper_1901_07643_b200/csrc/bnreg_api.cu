@@ -629,6 +629,9 @@ bnreg_status bnreg_sync(bnreg_t* h)
         for (int c = 0; c < g; ++c) { ends.push_back((t[3 * c + 1] - t0) * 1e-6); starts.push_back((t[3 * c] - t0) * 1e-6); }
         std::sort(ends.begin(), ends.end());
         std::sort(starts.begin(), starts.end());
+        unsigned long long cand = 0;
+        CK(cudaMemcpy(&cand, h->d_trace + 3 * 4096, sizeof(cand), cudaMemcpyDeviceToHost));
+        (void)cand;
         fprintf(stderr, "walk trace: span %.3f ms; CTA starts max %.3f ms; CTA ends min %.3f p10 %.3f p50 %.3f p90 %.3f max %.3f ms\n",
                 (t1 - t0) * 1e-6, starts.back(), ends.front(), ends[g / 10], ends[g / 2], ends[9 * g / 10], ends.back());
     }
@@ -803,7 +806,8 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     T.k8_selftest = getenv("BNREG_K8_SELFTEST") ? 1 : 0;
     if (getenv("BNREG_TRACE")) {
         // diagnostic: per-CTA start / end times of the walk launch, printed at the next sync
-        if (!h->d_trace) CK(cudaMalloc(&h->d_trace, 3 * 4096 * sizeof(unsigned long long)));
+        if (!h->d_trace) CK(cudaMalloc(&h->d_trace, (3 * 4096 + 1) * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(h->d_trace + 3 * 4096, 0, sizeof(unsigned long long), st));
         T.trace = h->d_trace;
     }
     T.patlo = (P.world > 1) ? P.pat_lo[0] : 0u;   // child 0 is never a selector variable

@@ -169,7 +169,9 @@ def _gloo_worker(rank, world, port, cfg, outdir):
     pipe.h.sync()
     bm1, bb1 = pipe.best_mask.cpu().numpy().view(np.uint32), pipe.best_bic.cpu().numpy()
     pipe.tab.fill_(float("nan"))
-    bm, bb = pipe.step_e2e()
+    r = pipe.step_e2e()                 # pipelined: returns the previous e2e step's result (none yet)
+    assert r is None
+    bm, bb = pipe.finish_e2e()
     h.sync()
     starts, lens = h.shard_ranges()
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), tab=pipe.tab.cpu().numpy(), bm=bm, bb=bb, bm1=bm1, bb1=bb1,
