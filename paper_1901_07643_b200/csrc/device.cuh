@@ -111,7 +111,13 @@ __device__ __forceinline__ double fast_ln9s(double x, unsigned tab)
 #else
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "r"(tab + ln_tab_off(hi)));
 #endif
+#ifdef BNREG_LN_MAGIC   // the exponent as a double without I2F: (2^52 + E) - (2^52 + 1023) exactly
+    const double ed = __hiloint2double(0x43300000, (int)((unsigned)hi >> 20)) - 4503599627371519.0;
+    (void)e;
+    const double base = fma(ed, kLn2, ty);
+#else
     const double base = fma((double)e, kLn2, ty);
+#endif
     return ln_poly(fma(f, tx, -1.0), base);
 }
 

@@ -100,6 +100,23 @@ inline int walk_tmem_cols_h(int k, int jbmax)
     return c;
 }
 
+// Launch constants: BNREG_LCONST reads them from the kernel parameters (constant bank) in
+// the hot loop instead of per-lane registers (A/B of register pressure)
+#ifdef BNREG_LCONST
+#define LC_mhalf_n P.mhalf_n
+#define LC_out_pairs P.out_pairs
+#define LC_tiny_bic P.tiny_bic
+#define LC_fv0 (P.p + P.g)
+#define LC_RS (P.k * kW * 16)
+#else
+#define LC_mhalf_n L.mhalf_n
+#define LC_out_pairs L.out_pairs
+#define LC_tiny_bic L.tiny_bic
+#define LC_fv0 L.fv0
+#define LC_RS L.RS
+#endif
+#define LC(x) LC_##x
+
 // Per-lane constants of the current item.
 struct LaneC {
     unsigned sbase;   // shared address of the free state (row 0, slot 0, worker w)
@@ -136,8 +153,8 @@ struct LaneC {
 // phase C of a step: ln RSS, BIC (a9), the two table stores (a10) and the
 // running-best candidates; new bests (rare) are resolved warp-serially (a11, G14)
 template <int NE, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const unsigned* ra, const bool* okv,
-                                        double Kw, uint32_t X, uint32_t S)
+__device__ __forceinline__ void harvest(const LaneC& L, const TravParams& P, const double* rs, const unsigned* ra,
+                                        const bool* okv, double Kw, uint32_t X, uint32_t S)
 {
     const double PINF = __longlong_as_double(0x7ff0000000000000LL);
     const uint32_t X1 = X >> 1;
@@ -146,8 +163,12 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
         const double rss = rs[e];
+#ifdef BNREG_FAKE_HARVEST   // timing experiment only (wrong BICs): no log
+        const double lnr = rss;
+#else
         const double lnr = fast_ln9s(rss, L.lnt);
-        const double bic = fma(L.mhalf_n, lnr, Kw);
+#endif
+        const double bic = fma(LC(mhalf_n), lnr, Kw);
         bics[e] = bic;
         const double2 rr = lds2(ra[e]);
         const uint32_t idx = (uint32_t)__double2loint(rr.y);        // table index of (child, F_w)
@@ -155,7 +176,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
         const uint32_t ix = idx + ((X & lm) | (X1 & ~lm));           // + compress(T | w-bits, child)
         if (HR) stg_cs_if(L.out_rss + ix, rss, okv[e]);
         if (HB) stg_cs_if(L.out_bic + ix, bic, okv[e]);
-        if (HP) stg2_cs_if(L.out_pairs + 2 * (size_t)ix, rss, bic, okv[e]);
+        if (HP) stg2_cs_if(LC(out_pairs) + 2 * (size_t)ix, rss, bic, okv[e]);
         K8_COUNT(L, okv[e], ix);   // K8 debug builds: every entry written exactly once, in range
         // candidate: BIC >= the slot's threshold min(running best, tiny_bic); a perfect fit
         // (RSS <= 1e-300, G13: BIC = +inf, fixed on the rare path) has BIC >= tiny_bic
@@ -182,7 +203,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
                         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rr) : "r"(a + 8));
                         const uint32_t idx = (uint32_t)__double2loint(rr), lm = (uint32_t)__double2hiint(rr);
                         if (HB) L.out_bic[idx + ((X & lm) | (X1 & ~lm))] = PINF;
-                        if (HP) L.out_pairs[2 * (size_t)(idx + ((X & lm) | (X1 & ~lm))) + 1] = PINF;
+                        if (HP) LC(out_pairs)[2 * (size_t)(idx + ((X & lm) | (X1 & ~lm))) + 1] = PINF;
                     }
                     double cb;
                     uint32_t cm;
@@ -191,7 +212,7 @@ __device__ __forceinline__ void harvest(const LaneC& L, const double* rs, const 
                     if (tie_better(b, S, cb, cm)) {
                         asm volatile("st.shared.f64 [%0], %1;" ::"r"(ba), "d"(b) : "memory");
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(ma), "r"(S) : "memory");
-                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(fmin(b, L.tiny_bic)) : "memory");
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(fmin(b, LC(tiny_bic))) : "memory");
                         if (L.gbest) {
                             // publish: every warp's later items take it as their candidate floor
                             uint32_t lmv;
@@ -221,7 +242,7 @@ __device__ __forceinline__ void free_entries(const LaneC& L, uint32_t nib, int n
 // Seed pseudo-step (reading G11: the seed prefixes {free 0..j-1}, i = j - 1):
 // RSS = U_{i+1} = E_i.y, or U_0 = R_0^2 + E_0.y for the empty prefix; no rotation.
 template <int JB, int NFE, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
+__device__ __forceinline__ void seed_step(const LaneC& L, const TravParams& P, const uint4 q)
 {
     constexpr int NE = JB + NFE;
     const uint32_t fl = q.w;
@@ -255,8 +276,8 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
         ra[JB + j] = L.recb + sl[j] * 16;
         okv[JB + j] = fo[j] && L.hfree;
     }
-    const uint32_t Tsh = (fl >> 17) << L.fv0;
-    harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
+    const uint32_t Tsh = (fl >> 17) << LC(fv0);
+    harvest<NE, HR, HB, HP>(L, P, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One lockstep GRC step of a lane (a7-a11):
@@ -267,14 +288,15 @@ __device__ __forceinline__ void seed_step(const LaneC& L, const uint4 q)
 //   givens   the next step's rotation from its pivot column (overlaps phase C);
 //   phase C  harvest().
 template <int JB, int NFE, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& c, double& sg, double& hh, bool sync)
+__device__ __forceinline__ void grc_step(const LaneC& L, const TravParams& P, const uint4 q, double& c, double& sg,
+                                         double& hh, bool sync)
 {
     constexpr int NE = JB + NFE;
     const uint32_t fl = q.w;
     const int nf = (int)(fl & 31u);
     const int i = (int)((fl >> 8) & 31u) - 1;
     const unsigned bi = L.sbase + q.x;
-    const int RS = L.RS;
+    const int RS = LC(RS);
     double rs[NE];
     unsigned ra[NE];
     bool okv[NE];
@@ -344,18 +366,18 @@ __device__ __forceinline__ void grc_step(const LaneC& L, const uint4 q, double& 
 #endif
         givens_fr(a, b, c, sg, hh);
     }
-    const uint32_t Tsh = (fl >> 17) << L.fv0;
+    const uint32_t Tsh = (fl >> 17) << LC(fv0);
     // the gang's stores start together (DRAM write combining of the 4 warps' parts of each
     // region) every BNREG_SYNC_EVERY steps: the barrier costs more than the last bit of combining
     if (sync) asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
-    harvest<NE, HR, HB, HP>(L, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
+    harvest<NE, HR, HB, HP>(L, P, rs, ra, okv, L.KCw[(fl >> 8) & 31u], Tsh | L.Xw, L.Fw | Tsh);
 }
 
 // One item (gang) of a warp with JB back entries per lane: fill the lane's TMEM
 // rows from the seed block, the k + 1 seed pseudo-steps, then Upsilon(k).
 template <int JB, bool HR, bool HB, bool HP>
-__device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* src, int k, int SA, int NB, int b0,
-                                       const uint4* __restrict__ wsteps, int nsteps)
+__device__ __forceinline__ void walk_item(const LaneC& L, const TravParams& P, const unsigned char* src, int k, int SA,
+                                       int NB, int b0, const uint4* __restrict__ wsteps, int nsteps)
 {
     if constexpr (JB > 0) {
         // back slot b = b0 + 4j + h of worker w, row l: seed block [w][l][slot] at ((w k + l) SA + k + b) * 16
@@ -395,9 +417,9 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
                                                    __shfl_sync(FULLMASK, win.z, 0), __shfl_sync(FULLMASK, win.w, 0));
         qk = q;
         const int nfe = ((int)(q.w & 31u) + 3) >> 2;
-        if (nfe == 0) seed_step<JB, 0, HR, HB, HP>(L, q);
-        else if (nfe == 1) seed_step<JB, 1, HR, HB, HP>(L, q);
-        else seed_step<JB, 2, HR, HB, HP>(L, q);
+        if (nfe == 0) seed_step<JB, 0, HR, HB, HP>(L, P, q);
+        else if (nfe == 1) seed_step<JB, 1, HR, HB, HP>(L, P, q);
+        else seed_step<JB, 2, HR, HB, HP>(L, P, q);
     }
     double c = 1.0, sg = 0.0, hh = 0.0;
     {
@@ -405,15 +427,15 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const unsigned char* s
         double a = 0.0, b = 1.0;
         if ((qk.w >> 7) & 1u) {
             asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a) : "r"(L.sbase + qk.y));
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(L.sbase + qk.y + L.RS));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b) : "r"(L.sbase + qk.y + LC(RS)));
         }
         givens_fr(a, b, c, sg, hh);
     }
     constexpr int kSync = HP ? BNREG_SYNC_EVERY : 1;
     for (int t = k + 1; t < nsteps; ++t) {
         const uint4 q = record(t);
-        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB, HP>(L, q, c, sg, hh, (t & (kSync - 1)) == 0);
-        else grc_step<JB, 1, HR, HB, HP>(L, q, c, sg, hh, (t & (kSync - 1)) == 0);
+        if ((q.w & 31u) > 4u) grc_step<JB, 2, HR, HB, HP>(L, P, q, c, sg, hh, (t & (kSync - 1)) == 0);
+        else grc_step<JB, 1, HR, HB, HP>(L, P, q, c, sg, hh, (t & (kSync - 1)) == 0);
     }
     tm_wait_st();
 }
@@ -591,18 +613,18 @@ __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __g
 
         const int JB = (nbp + 3) >> 2;
         switch (JB) {
-            case 0: walk_item<0, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
-            case 1: walk_item<1, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
-            case 2: walk_item<2, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
-            case 3: walk_item<3, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 0: walk_item<0, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 1: walk_item<1, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 2: walk_item<2, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps); break;
+            case 3: walk_item<3, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps); break;
             default:
                 if constexpr (JBMAX <= 4) {
-                    walk_item<4, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
+                    walk_item<4, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps);
                 } else {
-                    if (JB == 4) walk_item<4, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
-                    else if (JB == 5) walk_item<5, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
-                    else if (JB == 6) walk_item<6, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
-                    else walk_item<7, HR, HB, HP>(L, src, k, Sw, NB, b0, wsteps, nsteps);
+                    if (JB == 4) walk_item<4, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else if (JB == 5) walk_item<5, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else if (JB == 6) walk_item<6, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps);
+                    else walk_item<7, HR, HB, HP>(L, P, src, k, Sw, NB, b0, wsteps, nsteps);
                 }
                 break;
         }
