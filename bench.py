@@ -59,6 +59,8 @@ def parse():
                     help="diagnostic (one GPU, no collectives): run logical rank --sim-rank of a world of this size "
                          "(its shard of the lattice, rank-filtered seed tree) to measure per-rank costs")
     ap.add_argument("--sim-rank", type=int, default=0)
+    ap.add_argument("--e2e-first", action="store_true",
+                    help="diagnostic: time the e2e steps before the device-resident steps")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="load each dataset on the walk's stream (no overlap of dataset s+1's load and seed "
                          "tree with dataset s's walk)")
@@ -450,6 +452,9 @@ def bench_ours(args):
     # steps), then the same steps again with the handle's per-phase CUDA events (the
     # traversal kernel's own time; collecting them synchronises once per step)
     h.timing(0)
+    if args.e2e_first and not args.no_e2e:
+        ms_e2e_first, clocks_e2e = timed(step_e2e, args.steps, args.warmup, with_clocks=True)
+        pipe.finish_e2e()
     ms, clocks = timed(step_device, args.steps, args.warmup, with_clocks=True)
     h.sync()                                   # deferred load checks (NaN/Inf, rank)
     h.timing(1)
@@ -463,14 +468,19 @@ def bench_ours(args):
     value = (F if sim else total) * args.steps / (ms / 1e3)
     e2e = None
     if not args.no_e2e:
-        ms_e2e, _ = timed(step_e2e, args.steps, 1)
-        pipe.finish_e2e()
+        # the same protocol as the device-resident steps (warm-up, then the clock sampler's
+        # 0.3 s start before the timed region), so both numbers start from the same GPU state
+        if args.e2e_first:
+            ms_e2e = ms_e2e_first
+        else:
+            ms_e2e, clocks_e2e = timed(step_e2e, args.steps, args.warmup, with_clocks=True)
+            pipe.finish_e2e()
         e2e = {"value": total * args.steps / (ms_e2e / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": world * pipe.d2h_bytes(),
                "pipelined": ("each step's best is copied asynchronously to pinned host memory and read on the "
                              "host one step later (the last after the timed loop's synchronisation)"
                              if load_stream is not None else "no"),
-               "ms_per_step": ms_e2e / args.steps}
+               "ms_per_step": ms_e2e / args.steps, "clocks": clocks_e2e}
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_FAMILY * F / (trav_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(f"cfg{args.config}")
