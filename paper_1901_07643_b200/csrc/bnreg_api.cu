@@ -518,7 +518,9 @@ static bnreg_status gbest_init(bnreg_t* h, cudaStream_t st, int buf)
     } else {
         double K[33];
         score_constants(P.n, h->score, K);
-        CK(launch_gbest_init(h->d_root, h->d_order, P.m, P.mhalf_n, K[0], g, st));
+        FloorK fk;
+        for (int q = 0; q <= kFloorDepth; ++q) fk.k[q] = K[q];
+        CK(launch_gbest_init(h->d_root, h->d_order, P.m, P.mhalf_n, fk, g, st));
     }
     return BNREG_OK;
 }

@@ -316,31 +316,83 @@ __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restri
 }
 
 // ---------------------------------------------------------------- a11 candidate floor
-// The shared floor of the walk's running-best thresholds starts at each child's empty-set
-// score (a family every run visits: RSS(v|{}) = ||x_v||^2 = the squared norm of R's column
-// of v, a12) less a margin far above its rounding, so it is below the child's maximum and
-// the argmax stays exact (G14); families worse than the empty set never take the
-// candidate path.
-__global__ void gbest_init_kernel(const double* __restrict__ R, const int* __restrict__ order, int m, double mhalf_n,
-                                  double K0, long long* gbest)
+// The shared floor of the walk's running-best thresholds starts at the score of families
+// every run visits, found greedily: the empty set (a12: RSS(v|{}) = ||x_v||^2, the squared
+// norm of R's column), then up to kFloorDepth forward steps, each adding the parent with the
+// best score (RSS by Householder reflections of R's columns applied to column v: the stable
+// route of the oracle's O2; X = Q0 R0).  The floor must not exceed the child's maximum (else
+// the argmax would be missed), so every RSS is raised by a generous bound of its rounding
+// error (64 m (t+1) eps ||x_v||^2) before the score and 1e-6 is subtracted: near-collinear
+// sets only weaken the floor (G14 stays exact).  One warp per child (root position), lane =
+// row of R.
+
+__global__ void __launch_bounds__(32) gbest_init_kernel(const double* __restrict__ R, const int* __restrict__ order,
+                                                        int m, double mhalf_n, const FloorK K, long long* gbest)
 {
-    const int pos = threadIdx.x;
-    if (pos >= 32) return;
-    if (pos >= m) {
-        gbest[pos] = bic_ord(-__longlong_as_double(0x7ff0000000000000LL));
+    const int pv = blockIdx.x, lane = threadIdx.x;
+    const double NINF = -__longlong_as_double(0x7ff0000000000000LL);
+    if (pv >= 32) return;
+    if (pv >= m) {
+        if (lane == 0) gbest[pv] = bic_ord(NINF);
         return;
     }
-    double s = 0.0;
-    for (int i = 0; i <= pos; ++i) s = fma(R[i * m + pos], R[i * m + pos], s);
-    const double b = fma(mhalf_n, log(s), K0);
-    const double fl = b - (1e-9 * fabs(b) + 1e-6);
-    gbest[order[pos]] = bic_ord(s > 1e-300 && isfinite(fl) ? fl : -__longlong_as_double(0x7ff0000000000000LL));
+    double yr = (lane <= pv && lane < m) ? R[lane * m + pv] : 0.0;   // column v, reflected as S grows
+    const double yy = warp_sum(yr * yr);
+    const double eps = 64.0 * m * 1.1102230246251565e-16 * yy;
+    double best = fma(mhalf_n, log(yy + eps), K.k[0]);
+    double W[kFloorDepth], WW[kFloorDepth];                         // the reflections of S (lane's row)
+    uint32_t S = 0;
+    for (int t = 0; t < kFloorDepth && t < m - 1; ++t) {
+        double bs = NINF;
+        int bu = -1;
+        for (int pu = 0; pu < m; ++pu) {
+            if (pu == pv || ((S >> pu) & 1u)) continue;
+            double a = (lane <= pu && lane < m) ? R[lane * m + pu] : 0.0;
+#pragma unroll
+            for (int q = 0; q < kFloorDepth; ++q)
+                if (q < t) a = fma(-2.0 * warp_sum(W[q] * a) / WW[q], W[q], a);
+            const double at = lane >= t ? a : 0.0;                  // the part orthogonal to S
+            const double aa = warp_sum(at * at);
+            if (!(aa > 0.0)) continue;
+            const double nrm = sqrt(aa);
+            const double a0 = __shfl_sync(FULLMASK, a, t);
+            const double alpha = a0 >= 0.0 ? nrm : -nrm;
+            const double w = lane == t ? at + alpha : at;
+            const double ww = 2.0 * nrm * (nrm + fabs(a0));
+            const double y2 = fma(-2.0 * warp_sum(w * yr) / ww, w, yr);
+            const double rss = warp_sum(lane > t ? y2 * y2 : 0.0);
+            const double sc = fma(mhalf_n, log(rss + (t + 2) * eps), K.k[t + 1]);
+            if (sc > bs) { bs = sc; bu = pu; }
+        }
+        if (bu < 0) break;
+        best = fmax(best, bs);
+        // add bu to S: its reflection in the current coordinates, applied to column v
+        double a = (lane <= bu && lane < m) ? R[lane * m + bu] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kFloorDepth; ++q)
+            if (q < t) a = fma(-2.0 * warp_sum(W[q] * a) / WW[q], W[q], a);
+        const double at = lane >= t ? a : 0.0;
+        const double nrm = sqrt(warp_sum(at * at));
+        const double a0 = __shfl_sync(FULLMASK, a, t);
+        const double alpha = a0 >= 0.0 ? nrm : -nrm;
+#pragma unroll
+        for (int q = 0; q < kFloorDepth; ++q)
+            if (q == t) {
+                W[q] = lane == t ? at + alpha : at;
+                WW[q] = 2.0 * nrm * (nrm + fabs(a0));
+                yr = fma(-2.0 * warp_sum(W[q] * yr) / WW[q], W[q], yr);
+            }
+        S |= 1u << bu;
+    }
+    const double fl = best - (1e-9 * fabs(best) + 1e-6);
+    if (lane == 0)
+        gbest[order[pv]] = bic_ord(isfinite(fl) ? fl : (fl > 0 ? __longlong_as_double(0x7ff0000000000000LL) : NINF));
 }
 
-cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, double K0, long long* gbest,
+cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, const FloorK& K, long long* gbest,
                               cudaStream_t st)
 {
-    gbest_init_kernel<<<1, 32, 0, st>>>(R, order, m, mhalf_n, K0, gbest);
+    gbest_init_kernel<<<32, 32, 0, st>>>(R, order, m, mhalf_n, K, gbest);
     return cudaGetLastError();
 }
 

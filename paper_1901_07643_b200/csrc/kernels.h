@@ -118,7 +118,11 @@ cudaError_t launch_gram_chol(const double* Xr, int64_t n, int m, double* G, doub
 cudaError_t launch_tree_level(const double* parent, double* child, int m, int L, int bh, int p, int k,
                               cudaStream_t st);
 // the walk's shared candidate floor: each child's empty-set score less a margin
-cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, double K0, long long* gbest,
+constexpr int kFloorDepth = 3;                 // greedy forward steps of the candidate floor
+struct FloorK {
+    double k[kFloorDepth + 1];                 // the score constants K(0..kFloorDepth)
+};
+cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, const FloorK& K, long long* gbest,
                               cudaStream_t st);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, uint32_t* mask_copy, cudaStream_t st,

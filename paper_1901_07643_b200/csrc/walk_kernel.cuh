@@ -441,7 +441,14 @@ __device__ __forceinline__ void walk_item(const LaneC& L, const TravParams& P, c
 }
 
 template <bool HR, bool HB, bool HP, int JBMAX>
+#ifndef BNREG_WALK_MAXREG
+#define BNREG_WALK_MAXREG 0      // A/B: cap the walk's registers (e.g. 112 leaves room for one prep CTA per SM)
+#endif
+#if BNREG_WALK_MAXREG > 0
+__global__ void __maxnreg__(JBMAX <= 4 ? BNREG_WALK_MAXREG : 255) walk_kernel(const __grid_constant__ TravParams P)
+#else
 __global__ void __launch_bounds__(128, JBMAX <= 4 ? 4 : 2) walk_kernel(const __grid_constant__ TravParams P)
+#endif
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_item, s_taddr;

@@ -182,6 +182,72 @@ def test_errors_nonfinite_and_rank():
     assert e.value.status == bn.E_INVAL
 
 
+def test_deferred_load_errors_and_recovery():
+    """bnreg_load_async defers the NaN/Inf and rank checks to the next synchronous call
+    (bnreg_sync, bnreg_run): both report the error, the handle refuses to run on the
+    rejected data until a good load, and a good load afterwards gives the oracle's table;
+    the same with a load stream (pipelined mode)."""
+    import torch
+    bn = _bn()
+    good = datagen.config_data(1)
+    n, m = good.shape
+    bad_nan = good.copy(); bad_nan[3, 2] = np.nan
+    bad_rank = good.copy(); bad_rank[:, 5] = 3.0 * bad_rank[:, 1]
+    ref, _ = oracle.table(oracle.centre(good), want_bic=False)
+    for pipelined in (False, True):
+        h = bn.Bnreg(n, m, bn.options(free_vars=4))
+        if pipelined:
+            st = torch.cuda.Stream()
+            h.set_load_stream(st.cuda_stream)
+        for bad, code in ((bad_nan, bn.E_NONFINITE), (bad_rank, bn.E_RANK)):
+            xb = np.asfortranarray(bad)
+            h.load_async(xb)
+            with pytest.raises(bn.BnregError) as e:
+                h.sync()
+            assert e.value.status == code
+            with pytest.raises(bn.BnregError) as e:
+                h.run()
+            assert e.value.status == bn.E_STATE
+            h.load_async(np.asfortranarray(bad))
+            r = torch.empty(h.num_families(), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            with pytest.raises(bn.BnregError) as e:
+                h.run(r, None)                      # the run itself reports the deferred error
+            assert e.value.status == code
+        h.load_async(np.asfortranarray(good))
+        r = torch.full((h.num_families(),), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        h.run(r, None)
+        torch.cuda.synchronize()
+        assert (np.abs(r.cpu().numpy() - ref) / ref).max() <= RSS_RTOL
+        h.close()
+
+
+def test_async_api_argument_errors():
+    """The round-2 entry points reject bad arguments with BNREG_E_INVAL: the device merge
+    (nparts < 1, NULL arrays, a row stride that is not a multiple of 8 or is shorter than
+    m doubles), root export before a load (BNREG_E_STATE)."""
+    import torch
+    bn = _bn()
+    X = datagen.config_data(1)
+    n, m = X.shape
+    h = bn.Bnreg(n, m)
+    R = torch.empty(m * m, dtype=torch.float64, device="cuda")
+    with pytest.raises(bn.BnregError) as e:
+        h.get_root_device(R)
+    assert e.value.status == bn.E_STATE
+    rec = torch.empty((2, 2 * m), dtype=torch.float64, device="cuda")
+    om = torch.empty(m, dtype=torch.int32, device="cuda")
+    ob = torch.empty(m, dtype=torch.float64, device="cuda")
+    base = rec.data_ptr()
+    for args in ((0, base + 8 * m, base, om, ob, 16 * m), (2, 0, base, om, ob, 16 * m),
+                 (2, base + 8 * m, base, om, ob, 12), (2, base + 8 * m, base, om, ob, 8 * m - 8)):
+        with pytest.raises(bn.BnregError) as e:
+            h.best_merge_async(args[0], args[1], args[2], args[3], args[4], row_bytes=args[5])
+        assert e.value.status == bn.E_INVAL
+    h.close()
+
+
 def test_root_r_gram():
     bn = _bn()
     X = datagen.config_data(3)
