@@ -15,8 +15,8 @@ import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu", "walk_pairs.cu", "walk_tables.cu", "walk7_kernel.cu", "walk7_tables.cu", "seed_kernel.cu", "bps_kernel.cu"]
-HEADERS = ["plan.h", "kernels.h", "device.cuh", "walk_kernel.cuh", "tmem.cuh"]
+SOURCES = ["bnreg_api.cu", "bnreg_kernels.cu", "walk_pairs.cu", "walk_tables.cu", "walks_pairs.cu", "walks_tables.cu", "walk7_kernel.cu", "walk7_tables.cu", "seed_kernel.cu", "bps_kernel.cu"]
+HEADERS = ["plan.h", "kernels.h", "device.cuh", "walk_kernel.cuh", "walks_kernel.cuh", "tmem.cuh"]
 OUT = os.path.join(HERE, "libbnreg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -120,6 +120,7 @@ struct bnreg {
     size_t wsteps_len = 0;         // steps per class table
     // walk7 (32 lockstep workers per warp; P.lw == 5)
     bool w7 = false;
+    bool ws = false;                    // slot-split walk (design S, walks_kernel.cuh; BNREG_WALK_S=1)
     int w7_warps = 4, w7_TB = 16, w7_KA = 8, w7_nbmax = 0;
     unsigned long long w7_sblk = 0;     // doubles per item of the seed blocks
     unsigned* k8 = nullptr;             // BNREG_K8 debug builds: caller's per-entry write counters
@@ -330,7 +331,9 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
         CKH(cudaMalloc(&h->d_counters, sizeof(unsigned)));
         const auto recs = step_records(P.k, P.sched);
         h->wsteps_len = recs.size();
-        auto tb = walk_step_table(recs, P.k, P.k, 1 << P.lw);   // free-slot state: k slots
+        h->ws = P.p == 3 && P.g == 2 && getenv("BNREG_WALK_S") != nullptr;
+        auto tb = h->ws ? walk_step_table_s(recs, P.k)                 // design S: shared free-slot state
+                        : walk_step_table(recs, P.k, P.k, 1 << P.lw);   // free-slot state: k slots
         for (int j = 0; j < 32; ++j) tb.push_back(WalkStep{});   // pad: the walk kernel loads 32-record windows
         CKH(cudaMalloc(&h->d_wsteps, tb.size() * sizeof(WalkStep)));
         CKH(cudaMemcpy(h->d_wsteps, tb.data(), tb.size() * sizeof(WalkStep), cudaMemcpyHostToDevice));
@@ -846,6 +849,8 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
         if (h->w7) {
             T.KA = h->w7_KA; T.TB = h->w7_TB; T.nbmax = h->w7_nbmax; T.sblk = h->w7_sblk;
             CK(launch_walk7(T, C.grid, h->w7_warps, st));
+        } else if (h->ws) {
+            CK(launch_walks(T, C.grid, st));
         } else {
             CK(launch_walk(T, C.grid, st));
         }

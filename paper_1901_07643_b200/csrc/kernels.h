@@ -106,6 +106,11 @@ size_t walk_cta_smem(int m, int k, int S_alloc, int g, int lw);
 int walk_tmem_cols(int k, int jbmax);
 int walk_max_ctas_per_sm(int m, int k, int S_alloc, int g, int jbmax);
 cudaError_t launch_walk(const TravParams& P, int grid_ctas, cudaStream_t st);
+// slot-split walk (design S, measured slower: DESIGN.md §4): the gang's 4 warps run the same 32
+// workers (one lane each) and split the walk slots; the same seed blocks and items, the step
+// table of walk_step_table_s, step mbarriers instead of the gang barrier
+size_t walks_cta_smem(int k, int S_alloc);
+cudaError_t launch_walks(const TravParams& P, int grid_ctas, cudaStream_t st);
 
 
 cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev,

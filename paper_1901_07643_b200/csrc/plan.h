@@ -144,6 +144,44 @@ inline std::vector<WalkStep> walk_step_table(const std::vector<StepRec>& recs, i
     return out;
 }
 
+// The same records for the slot-split walk (walks_kernel.cuh, "design S"): the gang's 4
+// warps share the free-slot state E(l, s, worker) (slot stride CS = 32*16 B, row stride
+// RS = k*CS) and deal each step's free list by position (entry f -> warp f mod 4).  Every
+// warp computes a GRC's rotation itself from the pivot column's rows, which one warp,
+// stg(t), copies to a staging buffer in step t - 1: the warp that rotated the pivot's
+// column in step t - 1 (the owner of its list entry), else warp 3 (it writes every pivot,
+// and rows written before the last step barrier are visible to it).
+//   x: i*RS (0 for i < 0)
+//   y: in*RS + Yn*CS | stg(t + 1) << 16, if the next step is a GRC (else 0)
+//   z: the free-list nibbles (as walk_step_table)
+//   w: the flags of walk_step_table
+inline std::vector<WalkStep> walk_step_table_s(const std::vector<StepRec>& recs, int k)
+{
+    const uint32_t CS = 512u, RS = (uint32_t)k * 512u;
+    std::vector<WalkStep> out = walk_step_table(recs, k, k, 8);
+    for (size_t t = 0; t < recs.size(); ++t) {
+        const StepRec& r = recs[t];
+        const int i = (int)(r.meta & 31u) - 1;
+        const int nf = (int)((r.meta >> 13) & 31u);
+        const bool seed = (r.meta >> 18) & 1u;
+        WalkStep& w = out[t];
+        w.offA = i < 0 ? 0u : (uint32_t)i * RS;
+        w.offN = 0;
+        if ((w.flags >> 7) & 1u) {
+            const int in = (int)(recs[t + 1].meta & 31u) - 1;
+            const int Yn = (int)((recs[t + 1].meta >> 9) & 15u);
+            uint32_t sw = 3;
+            if (!seed) {
+                const uint64_t nib = (uint64_t)r.lo | ((uint64_t)r.hi << 32);
+                for (int e = 0; e < nf; ++e)
+                    if ((int)((nib >> (4 * e)) & 15u) == Yn) sw = (uint32_t)(e % 4);
+            }
+            w.offN = ((uint32_t)in * RS + (uint32_t)Yn * CS) | (sw << 16);
+        }
+    }
+    return out;
+}
+
 struct Plan {
     int m = 0, k = 0, b = 0, p = 0, bh = 0;   // b = m - k pinned, p pack bits, bh tree bits (incl. gang)
     int lw = kPackBits;                       // walk kernel: log2 lockstep workers per warp

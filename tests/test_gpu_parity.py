@@ -708,3 +708,25 @@ def test_split_items_cfg3_k3():
         _check_full(X, bn.options(free_vars=3), o2=True, pairs=True)
     finally:
         del os.environ["BNREG_NO_SPLIT"]
+
+
+@pytest.mark.parametrize("case", ["cfg1_k3", "cfg2_k5", "cfg2_k5_tables", "m12_k4", "cfg3_k3", "cfg3"])
+def test_walk_slot_split_parity(case, monkeypatch):
+    """The slot-split walk (design S, walks_kernel.cuh, BNREG_WALK_S=1: the gang's 4 warps
+    run the same 32 workers one lane each and split the walk slots; step mbarriers and a
+    staging buffer for the pivot rows instead of the gang barrier; plans with 3 warp and 2
+    gang variables, m >= k + 5) against the oracle like the default design: every entry
+    written, RSS relative 1e-9, BIC absolute 1e-6, exact argmax; cfg3 with k = 3 has split
+    items (a second pass over back slots 16..)."""
+    bn = _bn()
+    monkeypatch.setenv("BNREG_WALK_S", "1")
+    if case == "cfg1_k3":
+        _check_full(datagen.config_data(1), bn.options(free_vars=3), pairs=True)
+    elif case.startswith("cfg2_k5"):
+        _check_full(datagen.config_data(2), bn.options(free_vars=5), pairs=not case.endswith("tables"))
+    elif case == "m12_k4":
+        _check_full(datagen.dag_data(12, 200, 0.25, 0.5, 2.0, seed=12), bn.options(free_vars=4), pairs=True)
+    elif case == "cfg3_k3":
+        _check_full(datagen.config_data(3), bn.options(free_vars=3), o2=True, pairs=True)
+    else:
+        _check_full(datagen.config_data(3), None, o2=True, pairs=True)
