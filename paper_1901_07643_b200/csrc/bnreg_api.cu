@@ -92,6 +92,10 @@ struct bnreg {
     cudaStream_t load_stream = nullptr;
     cudaEvent_t ev_seeds = nullptr;   // run stream: the seed kernel has consumed d_root / d_nodes
     cudaEvent_t ev_prep = nullptr;    // load stream: root R and seed tree of the next run are ready
+    // the candidate floor (gbest_init: a latency-bound warp per child) runs on its own stream
+    // beside the seed tree and seeds: forked when the root R is ready, joined before the walk
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_root = nullptr, ev_floor = nullptr;
     bool prepared = false;
     bool load_timed = false;       // a timed load is waiting to be collected
     int64_t runs = 0;
@@ -153,6 +157,9 @@ static void free_all(bnreg* h)
     for (auto& e : h->ev_walk)
         if (e) cudaEventDestroy(e);
     if (h->ev_prep) cudaEventDestroy(h->ev_prep);
+    if (h->ev_root) cudaEventDestroy(h->ev_root);
+    if (h->ev_floor) cudaEventDestroy(h->ev_floor);
+    if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     if (h->h_status) cudaFreeHost(h->h_status);
 }
@@ -431,6 +438,9 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaEventCreateWithFlags(&h->ev_seeds, cudaEventDisableTiming));
     for (auto& e : h->ev_walk) CKH(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CKH(cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming));
+    CKH(cudaEventCreateWithFlags(&h->ev_root, cudaEventDisableTiming));
+    CKH(cudaEventCreateWithFlags(&h->ev_floor, cudaEventDisableTiming));
+    CKH(cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking));
 #undef CKH
     *out = h;
     return BNREG_OK;
@@ -528,19 +538,42 @@ static bnreg_status gbest_init(bnreg_t* h, cudaStream_t st, int buf)
     return BNREG_OK;
 }
 
+// the candidate floor of seed buffer `buf` on the auxiliary stream, forked from `st` (the root
+// R is ready there); gbest_join makes `st` wait for it
+static bnreg_status gbest_fork(bnreg_t* h, cudaStream_t st, int buf)
+{
+    CK(cudaEventRecord(h->ev_root, st));
+    CK(cudaStreamWaitEvent(h->aux_stream, h->ev_root, 0));
+    const bnreg_status s = gbest_init(h, h->aux_stream, buf);
+    if (s != BNREG_OK) return s;
+    CK(cudaEventRecord(h->ev_floor, h->aux_stream));
+    return BNREG_OK;
+}
+static bnreg_status gbest_join(bnreg_t* h, cudaStream_t st)
+{
+    CK(cudaStreamWaitEvent(st, h->ev_floor, 0));
+    return BNREG_OK;
+}
+
 // pipelined mode: after the root R is in place on the load stream, build the seed tree there too
 static bnreg_status prepare_on_load_stream(bnreg_t* h)
 {
-    bnreg_status s = launch_seed_tree(h, h->load_stream);
-    if (s != BNREG_OK) return s;
     // the seeds of this dataset go to the buffer the current walk does not read; the walk
     // that read it last (two runs ago) must be done
     const int b = 1 - h->cur_buf;
+    bnreg_status s = BNREG_OK;
+    if (!h->w7) {
+        CK(cudaStreamWaitEvent(h->load_stream, h->ev_walk[b], 0));   // (the floor of buffer b too)
+        s = gbest_fork(h, h->load_stream, b);
+        if (s != BNREG_OK) return s;
+    }
+    s = launch_seed_tree(h, h->load_stream);
+    if (s != BNREG_OK) return s;
     CK(cudaStreamWaitEvent(h->load_stream, h->ev_walk[b], 0));
     s = launch_seeds(h, h->load_stream, b);
     if (s != BNREG_OK) return s;
     if (!h->w7) {
-        s = gbest_init(h, h->load_stream, b);
+        s = gbest_join(h, h->load_stream);
         if (s != BNREG_OK) return s;
     }
     CK(cudaEventRecord(h->ev_prep, h->load_stream));
@@ -821,7 +854,7 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     if (!h->w7 && !getenv("BNREG_NO_GBEST")) {
         // (after a pipelined load the load stream has set this dataset's floor)
         if (!prepared) {
-            const bnreg_status gs = gbest_init(h, st, h->cur_buf);
+            const bnreg_status gs = gbest_fork(h, st, h->cur_buf);   // beside the seeds, joined before the walk
             if (gs != BNREG_OK) return gs;
         }
         T.gbest = h->d_gbest + 32 * h->cur_buf;
@@ -831,6 +864,10 @@ static bnreg_status run_impl(bnreg_t* h, double* out_rss, double* out_bic, uint3
     if (!prepared) {
         const bnreg_status ss = launch_seeds(h, st, h->cur_buf);
         if (ss != BNREG_OK) return ss;
+        if (T.gbest) {
+            const bnreg_status js = gbest_join(h, st);
+            if (js != BNREG_OK) return js;
+        }
     }
     if (h->load_stream && !prepared) CK(cudaEventRecord(h->ev_seeds, st));   // the next load may overwrite root and tree
     if (h->timing) CK(cudaEventRecord(h->ev[1], st));

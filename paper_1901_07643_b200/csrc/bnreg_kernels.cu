@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) centre_kernel(const double* __restrict__ 
 #define TSQR_THREADS 1024
 #endif
 constexpr int kTsqrThreads = TSQR_THREADS;
-__device__ void householder_tile(double* T, int nr, int m, double* sh /* 2 + m */)
+__device__ __forceinline__ void householder_tile(double* T, int nr, int m, double* sh /* 2 + m */)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     double* const diag = sh + 2;
@@ -92,10 +92,12 @@ __device__ void householder_tile(double* T, int nr, int m, double* sh /* 2 + m *
             double f = 0.0;
             if (vtv > 0.0) {
                 double d = 0.0;
+#pragma unroll 4
                 for (int i = j + lane; i < nr; i += 32) d = fma(i == j ? v0 : cj[i], cc[i], d);
                 f = 2.0 * warp_sum(d) / vtv;
             }
             double s2 = 0.0;                            // ||column j+1, rows j+1..||^2 after the update
+#pragma unroll 4
             for (int i = j + lane; i < nr; i += 32) {
                 const double y = fma(-f, i == j ? v0 : cj[i], cc[i]);
                 cc[i] = y;

@@ -26,27 +26,80 @@ namespace bnr {
 // no data moves for the swap itself.
 __host__ __device__ size_t seed_block_bytes(int k, int S_alloc, int lw) { return (size_t)k * S_alloc * (16u << lw); }
 
-// GRC at positions J, J+1 on the square node (lane = physical column, pos = its position).
-__device__ __forceinline__ void grc_cols(double* A, int SA, int J, int lane, int& pos)
+// A bubble: d consecutive GRCs that move one column across d others (each
+// GRC swaps two adjacent columns and restores the triangle with one rotation of their two
+// rows), with every column (lane) carrying its current row in a register: per GRC one
+// shared load and one store per column instead of two each, no per-GRC position updates.
+// Entries below a column's diagonal are exact zeros (the pivot of every GRC gets (h, 0)),
+// so columns a rotation does not touch just rotate zeros: the sweeps need no predicates.
+// The arithmetic is a single GRC's (givens_fr on the pivot's rows J, J+1; x' = c x + s y,
+// y' = c y - s x), so the result is that of the d GRCs one after the other.
+
+// forward: the column at position pj moves to pj + d (GRCs at pj, pj+1, .., pj+d-1); the
+// pivot of GRC t is the column at position pj + t + 1 (it moves to pj + t): its current row
+// J (the carried register) and row J + 1 come from its lane by shuffles
+__device__ __forceinline__ void bubble_fwd(double* A, int SA, int pj, int d, int lane, int& pos, double* cs)
 {
-    const int Y = __ffs(__ballot_sync(FULLMASK, pos == J + 1)) - 1;   // the column at position J+1
-    const double a = A[J * SA + Y], b = A[(J + 1) * SA + Y];
-    double c, s, h;
-    givens_fr(a, b, c, s, h);
-    const bool live = pos < 32;                                        // lanes past the node's columns idle
-    double* const p0 = A + J * SA + (live ? lane : 0);
-    const double x = p0[0], y = p0[SA];
+    int* const lanemap = (int*)cs;           // position -> lane
+    const bool live = pos < 32;
+    if (live) lanemap[pos] = lane;
     __syncwarp();
-    const bool isY = lane == Y;
-    const double xn = isY ? h : fma(c, x, s * y);
-    const double yn = isY ? 0.0 : fma(c, y, -s * x);
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(p0);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q st.shared.f64 [%0], %1;\n\t"
-                 "@q st.shared.f64 [%2], %3;\n\t}" ::"r"(sa), "d"(xn), "r"(sa + SA * 8), "d"(yn),
-                 "r"((unsigned)(live && pos >= J))
-                 : "memory");
+    double* p = A + pj * SA + (live ? lane : 0);
+    double x = live ? p[0] : 0.0;            // the carried row J
+    for (int t = 0; t < d; ++t, p += SA) {
+        const double y = live ? p[SA] : 0.0;
+        const int Y = lanemap[pj + t + 1];
+        double c, s, h;
+        givens_fr(__shfl_sync(FULLMASK, x, Y), __shfl_sync(FULLMASK, y, Y), c, s, h);
+        const bool isY = lane == Y;
+        const double xn = isY ? h : fma(c, x, s * y);
+        const double yn = isY ? 0.0 : fma(c, y, -s * x);
+        if (live) p[0] = xn;
+        x = yn;
+    }
+    if (live) p[0] = x;
     __syncwarp();
-    pos = pos == J ? J + 1 : (pos == J + 1 ? J : pos);
+    pos = pos == pj ? pj + d : (pos > pj && pos <= pj + d ? pos - 1 : pos);
+}
+
+// backward: the column Z at position pj moves to pj - d (GRCs at pj-1, pj-2, .., pj-d);
+// Z is every GRC's pivot: its rows are (h, 0) after each, so the chain needs only its
+// original entries above the diagonal
+__device__ __forceinline__ void bubble_bwd(double* A, int SA, int pj, int d, int lane, int& pos, double* cs)
+{
+    const int Z = __ffs(__ballot_sync(FULLMASK, pos == pj)) - 1;
+    const double* cz = A + Z;
+    double h = cz[pj * SA];
+    for (int t = 1; t <= d; ++t) {
+        const int J = pj - t;
+        double c, s;
+        givens_fr(cz[J * SA], h, c, s, h);
+        if (lane == 0) {
+            cs[3 * t - 3] = c;
+            cs[3 * t - 2] = s;
+            cs[3 * t - 1] = h;
+        }
+    }
+    __syncwarp();
+    const bool live = pos < 32 && lane != Z;
+    double* p = A + pj * SA + (live ? lane : 0);
+    double y = live ? p[0] : 0.0;            // the carried row J + 1
+    for (int t = 1; t <= d; ++t) {
+        p -= SA;                             // row J = pj - t
+        const double ct = cs[3 * t - 3], st = cs[3 * t - 2];
+        const double x = live ? p[0] : 0.0;
+        const double xn = fma(ct, x, st * y), yn = fma(ct, y, -st * x);
+        if (live) p[SA] = yn;
+        y = xn;
+    }
+    if (live) p[0] = y;
+    if (lane == Z) {                         // Z: (h_d, 0, .., 0) in rows pj-d .. pj
+        double* q = A + (pj - d) * SA + Z;
+        q[0] = h;
+        for (int r = 1; r <= d; ++r) q[r * SA] = 0.0;
+    }
+    __syncwarp();
+    pos = pos == pj ? pj - d : (pos >= pj - d && pos < pj ? pos + 1 : pos);
 }
 
 // Seed -> walk state of one worker, written to its part of a worker-major seed
@@ -91,6 +144,7 @@ __global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restri
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
     const uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib;
     const uint32_t nid = rsel > 0 ? (((q >> 1) << rsel) | ((q & 1u) ? t1 : t0)) : q;
     if ((rsel > 0 ? (q >> 1) << rsel : q) >= (1u << L1)) return;
@@ -105,7 +159,7 @@ __global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restri
             continue;
         }
         const int T = (bh - l - 1) + p + k;
-        for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+        bubble_fwd(A, SAq, org, T, lane, pos, cs);
     }
     // write the node in position order, without the dropped front
     const int sn = m - org;
@@ -121,7 +175,7 @@ cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1,
                                uint32_t t0, uint32_t t1, cudaStream_t st)
 {
     if (L1 <= 0) return cudaSuccess;
-    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
     if (rsel > L1) rsel = 0;                       // the selector is below the global tree: all nodes
     const unsigned n = rsel > 0 ? 2u << (L1 - rsel) : 1u << L1;
     cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -139,6 +193,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
     const int fv0 = p + g, gs = bh - g, G = 1 << g;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
     const int npk = (P.item_end - P.item_begin) * G;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
@@ -205,7 +260,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
                 continue;
             }
             const int T = (bh - l - 1) + p + k;
-            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+            bubble_fwd(A, SAq, org, T, lane, pos, cs);
         }
         // Gray path over the warp variables: start with all of them in F (front
         // region [w_{p-1} .. w_0 | free]), flip bit ctz(i) at step i; a flip moves
@@ -219,11 +274,8 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
             const int j = __ffs(i) - 1;
             const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
             const int d = k + j;
-            if ((wcur >> j) & 1) {
-                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
-            } else {
-                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
-            }
+            if ((wcur >> j) & 1) bubble_fwd(A, SAq, pj, d, lane, pos, cs);
+            else bubble_bwd(A, SAq, pj, d, lane, pos, cs);
             wcur ^= 1 << j;
             snapshot_sq(A, SAq, sn, org + __popc(wcur), k, SW, lane, pos, slot, blk + wcur * wsz);
         }
@@ -266,6 +318,7 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
     const int fv0 = p, gs = bh;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
     const int npk = P.item_end - P.item_begin;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
@@ -321,7 +374,7 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
                 continue;
             }
             const int T = (bh - l - 1) + p + k;
-            for (int j = 0; j < T; ++j) grc_cols(A, SAq, org + j, lane, pos);
+            bubble_fwd(A, SAq, org, T, lane, pos, cs);
         }
         int wcur = P.nw - 1;
         snapshot7(A, SAq, sn, org + p, k, lane, pos, slot, haveslot, blk, tails, wcur);
@@ -329,11 +382,8 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
             const int j = __ffs(i) - 1;
             const int pj = __shfl_sync(FULLMASK, pos, __ffs(__ballot_sync(FULLMASK, myvar == j)) - 1);
             const int d = k + j;
-            if ((wcur >> j) & 1) {
-                for (int t = 0; t < d; ++t) grc_cols(A, SAq, pj + t, lane, pos);
-            } else {
-                for (int t = 1; t <= d; ++t) grc_cols(A, SAq, pj - t, lane, pos);
-            }
+            if ((wcur >> j) & 1) bubble_fwd(A, SAq, pj, d, lane, pos, cs);
+            else bubble_bwd(A, SAq, pj, d, lane, pos, cs);
             wcur ^= 1 << j;
             snapshot7(A, SAq, sn, org + __popc(wcur), k, lane, pos, slot, haveslot, blk, tails, wcur);
         }
@@ -344,7 +394,7 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
 cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;
-    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
     const int npk = P.item_end - P.item_begin;
     if (npk <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
@@ -360,7 +410,7 @@ cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st)
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;
-    const size_t smem = (size_t)4 * m * (m | 1) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
     const int npk = (P.item_end - P.item_begin) << P.g;
     if (npk <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
