@@ -68,7 +68,7 @@ struct bnreg {
     double* d_rbuf = nullptr;      // TSQR tree slots
     unsigned* d_tcnt = nullptr;    // TSQR arrival counters
     int nleaf2 = 1;
-    int rb = 256;
+    int rb = 256;                  // TSQR leaf rows (tsqr_leaf_rows)
     double* d_root = nullptr;      // root R (m*m)
     double* d_nodes[2] = {nullptr, nullptr};
     uint32_t* d_packs = nullptr;
@@ -248,6 +248,7 @@ bnreg_status bnreg_create_ex(int64_t n, int32_t m, const bnreg_options* o, bnreg
     CKH(cudaMalloc(&h->dXr, nm * sizeof(double)));
     CKH(cudaMalloc(&h->d_order, m * sizeof(int)));
     CKH(cudaMemcpy(h->d_order, P.root_order.data(), m * sizeof(int), cudaMemcpyHostToDevice));
+    h->rb = tsqr_leaf_rows(n, m);
     int nleaf = (int)((n + h->rb - 1) / h->rb);
     h->nleaf2 = 1;
     while (h->nleaf2 < nleaf) h->nleaf2 <<= 1;

@@ -80,6 +80,7 @@ __device__ __forceinline__ void householder_tile(double* T, int nr, int m, doubl
     const int nj = m < nr ? m : nr;
     for (int j = 0; j < nj; ++j) {
         const double* cj = T + (int64_t)j * nr;
+        if (warp == 0 || j + 1 + warp < m) {           // (warps without a column skip the scalars)
         const double s = sh[j & 1];
         const double x0 = cj[j];
         const double nrm = sqrt(s);
@@ -87,26 +88,27 @@ __device__ __forceinline__ void householder_tile(double* T, int nr, int m, doubl
         const double v0 = x0 - alpha;
         const double vtv = s - x0 * x0 + v0 * v0;      // 0 only for a zero column (alpha = 0)
         if (threadIdx.x == 0) diag[j] = alpha;
+        const double tv = vtv > 0.0 ? 2.0 / vtv : 0.0;   // (off the dot product's chain)
         for (int c = j + 1 + warp; c < m; c += nwarp) {
             double* cc = T + (int64_t)c * nr;
-            double f = 0.0;
-            if (vtv > 0.0) {
-                double d = 0.0;
+            // row j (v's head v0) by lane 0, rows j+1.. (v = x) by all lanes: no per-row selects
+            double d = lane == 0 ? v0 * cc[j] : 0.0;
 #pragma unroll 4
-                for (int i = j + lane; i < nr; i += 32) d = fma(i == j ? v0 : cj[i], cc[i], d);
-                f = 2.0 * warp_sum(d) / vtv;
-            }
-            double s2 = 0.0;                            // ||column j+1, rows j+1..||^2 after the update
+            for (int i = j + 1 + lane; i < nr; i += 32) d = fma(cj[i], cc[i], d);
+            const double f = warp_sum(d) * tv;
+            if (lane == 0) cc[j] = fma(-f, v0, cc[j]);
+            double s2 = 0.0;                            // ||column, rows j+1..||^2 after the update
 #pragma unroll 4
-            for (int i = j + lane; i < nr; i += 32) {
-                const double y = fma(-f, i == j ? v0 : cj[i], cc[i]);
+            for (int i = j + 1 + lane; i < nr; i += 32) {
+                const double y = fma(-f, cj[i], cc[i]);
                 cc[i] = y;
-                if (i > j) s2 = fma(y, y, s2);
+                s2 = fma(y, y, s2);
             }
             if (c == j + 1) {
                 s2 = warp_sum(s2);
                 if (lane == 0) sh[(j + 1) & 1] = s2;
             }
+        }
         }
         __syncthreads();
     }
@@ -118,7 +120,7 @@ __device__ __forceinline__ void householder_tile(double* T, int nr, int m, doubl
 // level up to the root), each m*m row-major.  counters: one zeroed arrival counter per
 // internal node (self-resetting).  A merge of F children is one Householder QR of
 // their stacked R's (F m x m): fewer sequential levels than a binary tree.
-constexpr int kTsqrFanIn = 8;
+constexpr int kTsqrFanIn = 16;   // (kernels.h kTsqrFanInH: the host picks the leaf rows)
 __global__ void __launch_bounds__(kTsqrThreads) tsqr_kernel(const double* __restrict__ Xr, int64_t n, int m, int rb,
                                                    double* rbuf, unsigned* counters, int nleaf2,
                                                    double* Rroot, int* status)

@@ -113,6 +113,17 @@ size_t walks_cta_smem(int k, int S_alloc);
 cudaError_t launch_walks(const TravParams& P, int grid_ctas, cudaStream_t st);
 
 
+// TSQR: leaves of rb rows, merged 16 at a time (one merge level whenever n <= 16 rb): the
+// host picks rb >= 256 so that n fits one level if the leaf tile (rb x m doubles) fits
+constexpr int kTsqrFanInH = 16;
+inline int tsqr_leaf_rows(int64_t n, int m)
+{
+    int rb = (int)(((n + kTsqrFanInH - 1) / kTsqrFanInH + 31) / 32 * 32);
+    const int cap = (227 * 1024 / (8 * m)) / 32 * 32;
+    if (rb < 256) rb = 256;
+    if (rb > cap) rb = cap;
+    return rb;
+}
 cudaError_t launch_centre(const double* X, int64_t n, int m, const int* root_order_dev,
                           double* Xr, int* status, cudaStream_t st);
 cudaError_t launch_tsqr(const double* Xr, int64_t n, int m, double* rbuf, unsigned* counters,
