@@ -527,14 +527,15 @@ static bnreg_status gbest_init(bnreg_t* h, cudaStream_t st, int buf)
 {
     const Plan& P = h->plan;
     long long* g = h->d_gbest + 32 * buf;
-    if (getenv("BNREG_GBEST_NEGINF")) {
+    if (getenv("BNREG_GBEST_NEGINF") || (P.world > 1 && P.r > kFloorSel)) {   // (no floor)
         CK(cudaMemsetAsync(g, 0x80, 32 * sizeof(long long), st));
     } else {
         double K[33];
         score_constants(P.n, h->score, K);
         FloorK fk;
-        for (int q = 0; q <= kFloorDepth; ++q) fk.k[q] = K[q];
-        CK(launch_gbest_init(h->d_root, h->d_order, P.m, P.mhalf_n, fk, g, st));
+        for (int q = 0; q <= kFloorDepth + kFloorSel; ++q) fk.k[q] = K[q];
+        const uint32_t t0 = (uint32_t)P.rank, t1 = ((1u << P.r) - 1u) ^ (uint32_t)P.rank;
+        CK(launch_gbest_init(h->d_root, h->d_order, P.m, P.mhalf_n, fk, g, P.world > 1 ? P.r : 0, t0, t1, st));
     }
     return BNREG_OK;
 }

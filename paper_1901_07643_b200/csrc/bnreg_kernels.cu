@@ -321,17 +321,24 @@ __global__ void __launch_bounds__(256) best_reduce_kernel(const double* __restri
 
 // ---------------------------------------------------------------- a11 candidate floor
 // The shared floor of the walk's running-best thresholds starts at the score of families
-// every run visits, found greedily: the empty set (a12: RSS(v|{}) = ||x_v||^2, the squared
-// norm of R's column), then up to kFloorDepth forward steps, each adding the parent with the
-// best score (RSS by Householder reflections of R's columns applied to column v: the stable
-// route of the oracle's O2; X = Q0 R0).  The floor must not exceed the child's maximum (else
-// the argmax would be missed), so every RSS is raised by a generous bound of its rounding
-// error (64 m (t+1) eps ||x_v||^2) before the score and 1e-6 is subtracted: near-collinear
-// sets only weaken the floor (G14 stays exact).  One warp per child (root position), lane =
-// row of R.
+// the run visits, found greedily: a base set (the empty set, a12: RSS(v|{}) = ||x_v||^2, the
+// squared norm of R's column), then up to kFloorDepth forward steps, each adding the parent
+// with the best score (RSS by Householder reflections of R's columns applied to column v:
+// the stable route of the oracle's O2; X = Q0 R0).  The floor must not exceed the child's
+// maximum over this rank's shard (else its argmax would be missed), so
+//   * with world > 1 every visited set is one the rank owns: the base set is the rank's
+//     selector pattern (root positions 0..r-1 are the selector variables; for a selector
+//     child the pattern with its bit clear, plan.h) and only non-selector parents are
+//     added -- the rank's reported best is its shard's maximum, and the merge is exact;
+//   * every RSS is raised by a generous bound of its rounding error (64 m (s+1) eps
+//     ||x_v||^2 for a set of s parents) before the score and 1e-6 is subtracted:
+//     near-collinear sets only weaken the floor (G14 stays exact).
+// One warp per child (root position), lane = row of R.
+constexpr int kFloorRefl = kFloorDepth + kFloorSel;   // reflections of the base set + the steps
 
 __global__ void __launch_bounds__(32) gbest_init_kernel(const double* __restrict__ R, const int* __restrict__ order,
-                                                        int m, double mhalf_n, const FloorK K, long long* gbest)
+                                                        int m, double mhalf_n, const FloorK K, long long* gbest,
+                                                        int r, uint32_t t0, uint32_t t1)
 {
     const int pv = blockIdx.x, lane = threadIdx.x;
     const double NINF = -__longlong_as_double(0x7ff0000000000000LL);
@@ -343,17 +350,47 @@ __global__ void __launch_bounds__(32) gbest_init_kernel(const double* __restrict
     double yr = (lane <= pv && lane < m) ? R[lane * m + pv] : 0.0;   // column v, reflected as S grows
     const double yy = warp_sum(yr * yr);
     const double eps = 64.0 * m * 1.1102230246251565e-16 * yy;
-    double best = fma(mhalf_n, log(yy + eps), K.k[0]);
-    double W[kFloorDepth], WW[kFloorDepth];                         // the reflections of S (lane's row)
+    double W[kFloorRefl], WW[kFloorRefl];                            // the reflections of S (lane's row)
     uint32_t S = 0;
-    for (int t = 0; t < kFloorDepth && t < m - 1; ++t) {
+    int t = 0;                                                       // |S|
+    // S += {pu}: its reflection in the current coordinates, applied to column v
+    auto add = [&](int pu) {
+        double a = (lane <= pu && lane < m) ? R[lane * m + pu] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kFloorRefl; ++q)
+            if (q < t) a = fma(-2.0 * warp_sum(W[q] * a) / WW[q], W[q], a);
+        const double at = lane >= t ? a : 0.0;
+        const double nrm = sqrt(warp_sum(at * at));
+        const double a0 = __shfl_sync(FULLMASK, a, t);
+        const double alpha = a0 >= 0.0 ? nrm : -nrm;
+#pragma unroll
+        for (int q = 0; q < kFloorRefl; ++q)
+            if (q == t) {
+                W[q] = lane == t ? at + alpha : at;
+                WW[q] = 2.0 * nrm * (nrm + fabs(a0));
+                yr = fma(-2.0 * warp_sum(W[q] * yr) / WW[q], W[q], yr);
+            }
+        S |= 1u << pu;
+        ++t;
+    };
+    if (r > 0) {
+        // the base set: this rank's selector pattern (selector variables = root positions < r)
+        const uint32_t pat = (pv < r && ((t0 >> pv) & 1u)) ? t1 : t0;
+        const uint32_t S0 = pat & ((1u << r) - 1u) & ~(1u << pv);
+        for (int pu = 0; pu < r; ++pu)
+            if ((S0 >> pu) & 1u) add(pu);
+    }
+    const double rss0 = warp_sum(lane >= t ? yr * yr : 0.0);
+    double best = fma(mhalf_n, log(rss0 + (t + 1) * eps), K.k[t]);
+    const uint32_t excl = (r > 0) ? (1u << r) - 1u : 0u;             // never add a selector variable
+    for (int step = 0; step < kFloorDepth && t < m - 1; ++step) {
         double bs = NINF;
         int bu = -1;
         for (int pu = 0; pu < m; ++pu) {
-            if (pu == pv || ((S >> pu) & 1u)) continue;
+            if (pu == pv || ((S >> pu) & 1u) || ((excl >> pu) & 1u)) continue;
             double a = (lane <= pu && lane < m) ? R[lane * m + pu] : 0.0;
 #pragma unroll
-            for (int q = 0; q < kFloorDepth; ++q)
+            for (int q = 0; q < kFloorRefl; ++q)
                 if (q < t) a = fma(-2.0 * warp_sum(W[q] * a) / WW[q], W[q], a);
             const double at = lane >= t ? a : 0.0;                  // the part orthogonal to S
             const double aa = warp_sum(at * at);
@@ -370,23 +407,7 @@ __global__ void __launch_bounds__(32) gbest_init_kernel(const double* __restrict
         }
         if (bu < 0) break;
         best = fmax(best, bs);
-        // add bu to S: its reflection in the current coordinates, applied to column v
-        double a = (lane <= bu && lane < m) ? R[lane * m + bu] : 0.0;
-#pragma unroll
-        for (int q = 0; q < kFloorDepth; ++q)
-            if (q < t) a = fma(-2.0 * warp_sum(W[q] * a) / WW[q], W[q], a);
-        const double at = lane >= t ? a : 0.0;
-        const double nrm = sqrt(warp_sum(at * at));
-        const double a0 = __shfl_sync(FULLMASK, a, t);
-        const double alpha = a0 >= 0.0 ? nrm : -nrm;
-#pragma unroll
-        for (int q = 0; q < kFloorDepth; ++q)
-            if (q == t) {
-                W[q] = lane == t ? at + alpha : at;
-                WW[q] = 2.0 * nrm * (nrm + fabs(a0));
-                yr = fma(-2.0 * warp_sum(W[q] * yr) / WW[q], W[q], yr);
-            }
-        S |= 1u << bu;
+        add(bu);
     }
     const double fl = best - (1e-9 * fabs(best) + 1e-6);
     if (lane == 0)
@@ -394,9 +415,9 @@ __global__ void __launch_bounds__(32) gbest_init_kernel(const double* __restrict
 }
 
 cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, const FloorK& K, long long* gbest,
-                              cudaStream_t st)
+                              int r, uint32_t t0, uint32_t t1, cudaStream_t st)
 {
-    gbest_init_kernel<<<32, 32, 0, st>>>(R, order, m, mhalf_n, K, gbest);
+    gbest_init_kernel<<<32, 32, 0, st>>>(R, order, m, mhalf_n, K, gbest, r, t0, t1);
     return cudaGetLastError();
 }
 

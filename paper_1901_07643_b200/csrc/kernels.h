@@ -135,11 +135,13 @@ cudaError_t launch_tree_level(const double* parent, double* child, int m, int L,
                               cudaStream_t st);
 // the walk's shared candidate floor: each child's empty-set score less a margin
 constexpr int kFloorDepth = 3;                 // greedy forward steps of the candidate floor
+constexpr int kFloorSel = 6;                   // selector variables of a rank's base set (world <= 32)
 struct FloorK {
-    double k[kFloorDepth + 1];                 // the score constants K(0..kFloorDepth)
+    double k[kFloorDepth + kFloorSel + 1];     // the score constants K(0..kFloorDepth + kFloorSel)
 };
+// r, t0, t1: this rank's selector bits and patterns (plan.h; r = 0 for a single rank)
 cudaError_t launch_gbest_init(const double* R, const int* order, int m, double mhalf_n, const FloorK& K, long long* gbest,
-                              cudaStream_t st);
+                              int r, uint32_t t0, uint32_t t1, cudaStream_t st);
 cudaError_t launch_best_reduce(const double* part_bic, const uint32_t* part_mask, int nparts, int m,
                                double* best_bic, uint32_t* best_mask, uint32_t* mask_copy, cudaStream_t st,
                                size_t row_bytes = 0);   // bytes between rows (0: dense m-entry rows)
