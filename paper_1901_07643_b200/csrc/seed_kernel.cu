@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(128) tree_direct_kernel(const double* __restri
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
-    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 48 * wib;   // bubble scratch: 3 d <= 36 doubles, or 32 ints
     const uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib;
     const uint32_t nid = rsel > 0 ? (((q >> 1) << rsel) | ((q & 1u) ? t1 : t0)) : q;
     if ((rsel > 0 ? (q >> 1) << rsel : q) >= (1u << L1)) return;
@@ -175,7 +175,7 @@ cudaError_t launch_tree_direct(const double* root, double* nodes, int m, int L1,
                                uint32_t t0, uint32_t t1, cudaStream_t st)
 {
     if (L1 <= 0) return cudaSuccess;
-    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 48) * sizeof(double);
     if (rsel > L1) rsel = 0;                       // the selector is below the global tree: all nodes
     const unsigned n = rsel > 0 ? 2u << (L1 - rsel) : 1u << L1;
     cudaError_t e = cudaFuncSetAttribute(tree_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(128) seed_kernel(const __grid_constant__ SeedP
     const int fv0 = p + g, gs = bh - g, G = 1 << g;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
-    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 48 * wib;   // bubble scratch: 3 d <= 36 doubles, or 32 ints
     const int npk = (P.item_end - P.item_begin) * G;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
     const int fv0 = p, gs = bh;
     const int SAq = m | 1;
     double* const A = (double*)smem + (size_t)wib * m * SAq;
-    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 96 * wib;   // bubble chain scratch
+    double* const cs = (double*)smem + (size_t)(blockDim.x >> 5) * m * SAq + 48 * wib;   // bubble scratch: 3 d <= 36 doubles, or 32 ints
     const int npk = P.item_end - P.item_begin;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     for (int q = blockIdx.x * (blockDim.x >> 5) + wib; q < npk; q += nwarps) {
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(128) seed7_kernel(const __grid_constant__ Seed
 cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;
-    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 48) * sizeof(double);
     const int npk = P.item_end - P.item_begin;
     if (npk <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
@@ -410,7 +410,7 @@ cudaError_t launch_seed7(const SeedParams& P, cudaStream_t st)
 cudaError_t launch_seed(const SeedParams& P, cudaStream_t st)
 {
     const int m = P.m;
-    const size_t smem = (size_t)4 * (m * (m | 1) + 96) * sizeof(double);
+    const size_t smem = (size_t)4 * (m * (m | 1) + 48) * sizeof(double);
     const int npk = (P.item_end - P.item_begin) << P.g;
     if (npk <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
