@@ -51,7 +51,8 @@ typedef enum {
     BNREG_E_RANK = 3,       /* |r_jj| <= 1e-12 max_j ||x_j - mean||  (reading G26) */
     BNREG_E_NOMEM = 4,      /* device allocation failed                                       */
     BNREG_E_CUDA = 5,       /* any other CUDA error (message in bnreg_last_error)             */
-    BNREG_E_STATE = 6       /* call out of order (e.g. run before data/root is loaded)        */
+    BNREG_E_STATE = 6,      /* call out of order (e.g. run before data/root is loaded)        */
+    BNREG_E_NCCL = 7        /* NCCL missing or failing (bnreg_create_dist, bnreg_run_pairs_dist) */
 } bnreg_status;
 
 typedef struct {
@@ -284,7 +285,34 @@ bnreg_status bnreg_debug_write_counts(bnreg_t* h, uint32_t* counts_dev);
 
 const char* bnreg_last_error(void);
 
-void bnreg_destroy(bnreg_t* h);   /* NULL-safe; frees device state */
+void bnreg_destroy(bnreg_t* h);   /* NULL-safe; frees device state (and a dist handle's communicator) */
+
+/* ---- Multi-GPU with the library's own NCCL communicator (SURVEY §8(b) bnreg_create_dist;
+ * PAPER.md:299-324 §6 Alg.2: the lattice split over p processors; north_star: R
+ * NCCL-broadcast from rank 0, per-child maxima gathered with NCCL).  One process per GPU;
+ * NCCL is opened at run time (libnccl.so.2: the copy the process already has, e.g.
+ * torch's, else the system one), so the library has no link-time NCCL dependency.
+ *
+ * bnreg_nccl_unique_id: rank 0 creates the communicator id (128 bytes, caller-owned
+ * HOST buffer) and hands it to the other ranks out of band (e.g. torch.distributed).
+ * bnreg_create_dist: a rank-r handle of a world-rank job on the current device (world a
+ * power of two); X is rank 0's HOST column-major n x m data (NULL on the other ranks).
+ * Collective: every rank calls it.  Rank 0 centres and factors X (a1-a2); R is broadcast
+ * (a3, ncclBroadcast of 8 m^2 bytes) and every rank prepares its shard (a4-a5).
+ * bnreg_load_dist: the same for new data of the same n, m (collective).
+ * bnreg_run_pairs_dist: every rank writes its shard (out_pairs: DEVICE buffer of
+ * bnreg_num_families(h) 16 B records, the rank-local layout of bnreg_shard_ranges), then
+ * the ranks all-gather their 16 m-byte best records (ncclAllGather) and merge them on the
+ * device (G14): best_mask / best_bic (HOST, m entries, may be NULL) receive the GLOBAL
+ * per-child best on every rank.  Collective, synchronous.
+ * Errors: BNREG_E_NCCL (NCCL not loadable, or an NCCL call failing: message in
+ * bnreg_last_error), the errors of bnreg_create_ex / bnreg_load / bnreg_run_pairs.
+ * bnreg_run_pairs_dist on a handle not made by bnreg_create_dist: BNREG_E_STATE. */
+bnreg_status bnreg_nccl_unique_id(void* id128);
+bnreg_status bnreg_create_dist(const double* X, int64_t n, int32_t m, const void* nccl_id, int32_t rank,
+                               int32_t world, bnreg_t** out);
+bnreg_status bnreg_load_dist(bnreg_t* h, const double* X);
+bnreg_status bnreg_run_pairs_dist(bnreg_t* h, double* out_pairs, uint32_t* best_mask, double* best_bic);
 
 #ifdef __cplusplus
 }

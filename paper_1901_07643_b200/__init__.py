@@ -20,11 +20,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # from its own path; the in-tree libbnreg.so is never overwritten by a variant
 LIB_PATH = os.environ.get("BNREG_LIB") or os.path.join(_HERE, "libbnreg.so")
 
-OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE = range(7)
+OK, E_INVAL, E_NONFINITE, E_RANK, E_NOMEM, E_CUDA, E_STATE, E_NCCL = range(8)
 SCORE_BIC, SCORE_AIC, SCORE_LOGLIK = 0, 1, 2
 ROOT_TSQR, ROOT_CHOLESKY = 0, 1
 _NAMES = {1: "BNREG_E_INVAL", 2: "BNREG_E_NONFINITE", 3: "BNREG_E_RANK", 4: "BNREG_E_NOMEM",
-          5: "BNREG_E_CUDA", 6: "BNREG_E_STATE"}
+          5: "BNREG_E_CUDA", 6: "BNREG_E_STATE", 7: "BNREG_E_NCCL"}
 
 # every symbol include/bnreg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", "bnreg_sync", "bnreg_best_merge_async",
@@ -34,7 +34,7 @@ SYMBOLS = ["bnreg_create", "bnreg_create_ex", "bnreg_load", "bnreg_load_async", 
            "bnreg_set_stream", "bnreg_root_r", "bnreg_get_root_device", "bnreg_set_root_device",
            "bnreg_shard_ranges", "bnreg_plan_shard_ranges", "bnreg_plan_local_index", "bnreg_best_merge", "bnreg_timing", "bnreg_launches_per_run", "bnreg_plan_query",
            "bnreg_schedule", "bnreg_plan_packs", "bnreg_debug_ln", "bnreg_debug_write_counts", "bnreg_last_error",
-           "bnreg_destroy"]
+           "bnreg_destroy", "bnreg_nccl_unique_id", "bnreg_create_dist", "bnreg_load_dist", "bnreg_run_pairs_dist"]
 
 
 class BnregError(RuntimeError):
@@ -109,6 +109,10 @@ def lib():
         "bnreg_debug_write_counts": ([H, P], i32),
         "bnreg_last_error": ([], ctypes.c_char_p),
         "bnreg_destroy": ([H], None),
+        "bnreg_nccl_unique_id": ([P], i32),
+        "bnreg_create_dist": ([P, i64, i32, P, i32, i32, PH], i32),
+        "bnreg_load_dist": ([H, P], i32),
+        "bnreg_run_pairs_dist": ([H, P, P, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -178,6 +182,13 @@ def bnreg_plan_shard_ranges(m: int, n: int, opt: Options | None = None):
 
 def bnreg_plan_local_index(m: int, n: int, opt: Options | None, g: int) -> int:
     return lib().bnreg_plan_local_index(m, n, ctypes.byref(opt) if opt else None, g)
+
+
+def nccl_unique_id() -> bytes:
+    """bnreg_nccl_unique_id: a fresh NCCL communicator id (rank 0; hand it to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bnreg_nccl_unique_id(buf))
+    return buf.raw
 
 
 def bnreg_best_merge(m: int, masks: np.ndarray, bics: np.ndarray):
@@ -314,6 +325,41 @@ class Bnreg:
         order = np.zeros(self.m, dtype=np.int32)
         _check(lib().bnreg_root_r(self._h, _hptr(R), _hptr(order)))
         return R, order
+
+    @classmethod
+    def create_dist(cls, X, n: int, m: int, nccl_id: bytes, rank: int, world: int):
+        """bnreg_create_dist (collective): a rank of a world-rank job with the library's own
+        NCCL communicator; X = rank 0's host data (None on the other ranks)."""
+        self = cls.__new__(cls)
+        self.n, self.m, self._keep = int(n), int(m), None
+        self.opt = options(world=world, rank=rank)
+        h = ctypes.c_void_p()
+        Xp = None
+        if X is not None:
+            X = np.asfortranarray(X, dtype=np.float64)
+            if X.shape != (n, m):
+                raise ValueError("shape mismatch")
+            Xp = _hptr(X)
+        idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().bnreg_create_dist(Xp, n, m, idb, rank, world, ctypes.byref(h)))
+        self._h = h
+        return self
+
+    def load_dist(self, X=None):
+        """bnreg_load_dist (collective): new host data on rank 0 (None elsewhere)."""
+        Xp = None
+        if X is not None:
+            X = np.asfortranarray(X, dtype=np.float64)
+            Xp = _hptr(X)
+        _check(lib().bnreg_load_dist(self._h, Xp))
+
+    def run_pairs_dist(self, out_pairs):
+        """bnreg_run_pairs_dist (collective): this rank's shard into out_pairs, returns the
+        GLOBAL per-child best (mask, BIC) merged over the ranks."""
+        bm = np.zeros(self.m, dtype=np.uint32)
+        bb = np.zeros(self.m)
+        _check(lib().bnreg_run_pairs_dist(self._h, _dptr(out_pairs), _hptr(bm), _hptr(bb)))
+        return bm, bb
 
     def get_root_device(self, R_dev):
         """Copy the root R (m*m doubles) into a device buffer (for the broadcast)."""

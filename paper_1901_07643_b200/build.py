@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
         if bad:
             sys.stderr.write("\n".join(logs))
             raise RuntimeError("nvcc failed")
-        r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+        r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"],
                            capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -1,6 +1,9 @@
 // bnreg_api.cu -- the C ABI (include/bnreg.h): argument checks, device state,
 // host plan (plan.h) and the launch sequence of the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <nccl.h>          // types only: NCCL is opened at run time (dlopen), never linked
+#include <dlfcn.h>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -128,7 +131,47 @@ struct bnreg {
     int w7_warps = 4, w7_TB = 16, w7_KA = 8, w7_nbmax = 0;
     unsigned long long w7_sblk = 0;     // doubles per item of the seed blocks
     unsigned* k8 = nullptr;             // BNREG_K8 debug builds: caller's per-entry write counters
+    // bnreg_create_dist: the library's NCCL communicator and its device buffers
+    ncclComm_t comm = nullptr;
+    double* d_Rt = nullptr;             // the broadcast root R (m*m)
+    double* d_rec = nullptr;            // world rows of [m BICs | m masks]: the all-gathered bests
+    uint32_t* d_gm = nullptr;           // the merged best
+    double* d_gb = nullptr;
 };
+
+// NCCL, opened at run time: the process's copy if one is loaded (torch's), else the system's
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+static NcclApi& nccl()
+{
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            api.why = std::string("cannot open libnccl.so.2: ") + dlerror();
+            return;
+        }
+        api.getUniqueId = (decltype(api.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))dlsym(lib, "ncclCommInitRank");
+        api.commDestroy = (decltype(api.commDestroy))dlsym(lib, "ncclCommDestroy");
+        api.broadcast = (decltype(api.broadcast))dlsym(lib, "ncclBroadcast");
+        api.allGather = (decltype(api.allGather))dlsym(lib, "ncclAllGather");
+        api.errorString = (decltype(api.errorString))dlsym(lib, "ncclGetErrorString");
+        api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.broadcast && api.allGather && api.errorString;
+        if (!api.ok) api.why = "libnccl.so.2 lacks an NCCL entry point";
+    });
+    return api;
+}
 
 static bnreg_options defaults(const bnreg_options* o)
 {
@@ -144,7 +187,9 @@ static bnreg_options defaults(const bnreg_options* o)
 static void free_all(bnreg* h)
 {
     if (!h) return;
-    void* ptrs[] = {h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
+    if (h->comm && nccl().ok) nccl().commDestroy(h->comm);
+    h->comm = nullptr;
+    void* ptrs[] = {h->d_Rt, h->d_rec, h->d_gm, h->d_gb, h->dX, h->dXr, h->d_order, h->d_rbuf, h->d_tcnt, h->d_root, h->d_nodes[0], h->d_nodes[1],
                     h->d_packs, h->d_part_bic, h->d_part_mask, h->d_best_bic,
                     h->d_best_mask, h->d_status, h->d_lntab9, h->d_counters, h->d_wsteps, h->d_seeds, h->d_coef, h->d_cmask, h->d_gram, h->d_seeds2, h->d_trace, h->d_gbest};
     for (void* p : ptrs)
@@ -1126,5 +1171,112 @@ void bnreg_destroy(bnreg_t* h)
     free_all(h);
     delete h;
 }
+
+// ---- multi-GPU with the library's own NCCL communicator (include/bnreg.h)
+#define NCK(call)                                                                                  \
+    do {                                                                                           \
+        const ncclResult_t r_ = (call);                                                            \
+        if (r_ != ncclSuccess) return fail(BNREG_E_NCCL, std::string(#call) + ": " + nccl().errorString(r_)); \
+    } while (0)
+
+bnreg_status bnreg_nccl_unique_id(void* id128)
+{
+    if (!id128) return fail(BNREG_E_INVAL, "id is NULL");
+    if (!nccl().ok) return fail(BNREG_E_NCCL, nccl().why);
+    ncclUniqueId id;
+    NCK(nccl().getUniqueId(&id));
+    memcpy(id128, &id, sizeof(id));
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_load_dist(bnreg_t* h, const double* X)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (!h->comm) return fail(BNREG_E_STATE, "not a bnreg_create_dist handle");
+    const Plan& P = h->plan;
+    const size_t mm = (size_t)P.m * P.m;
+    bnreg_status s = BNREG_OK;
+    std::string why;
+    if (P.rank == 0) {
+        // rank 0 factors X; on failure it still takes part in the broadcast (a NaN R tells
+        // the other ranks), then returns its error
+        s = X ? bnreg_load(h, X, 0) : fail(BNREG_E_INVAL, "rank 0 needs X");
+        why = g_err;
+        if (s == BNREG_OK) s = bnreg_get_root_device(h, h->d_Rt);
+        if (s == BNREG_OK) CK(stream_wait(h->load_stream ? h->load_stream : h->stream));
+        else CK(cudaMemsetAsync(h->d_Rt, 0xff, mm * sizeof(double), h->stream));
+    }
+    NCK(nccl().broadcast(h->d_Rt, h->d_Rt, mm, ncclFloat64, 0, h->comm, h->stream));
+    CK(stream_wait(h->stream));
+    if (P.rank == 0) {
+        if (s != BNREG_OK) g_err = why;
+        return s;
+    }
+    double r00 = 0.0;
+    CK(cudaMemcpy(&r00, h->d_Rt, sizeof(double), cudaMemcpyDeviceToHost));
+    if (!(r00 == r00)) return fail(BNREG_E_STATE, "rank 0 could not load its data");
+    s = bnreg_set_root_device(h, h->d_Rt);
+    if (s != BNREG_OK) return s;
+    CK(stream_wait(h->load_stream ? h->load_stream : h->stream));
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_create_dist(const double* X, int64_t n, int32_t m, const void* nccl_id, int32_t rank,
+                               int32_t world, bnreg_t** out)
+{
+    if (!out || !nccl_id) return fail(BNREG_E_INVAL, "NULL argument");
+    *out = nullptr;
+    if (!nccl().ok) return fail(BNREG_E_NCCL, nccl().why);
+    bnreg_options o = defaults(nullptr);
+    o.world = world;
+    o.rank = rank;
+    bnreg_t* h = nullptr;
+    bnreg_status s = bnreg_create_ex(n, m, &o, &h);
+    if (s != BNREG_OK) return s;
+    auto bail = [&](bnreg_status st) {
+        const std::string keep = g_err;
+        bnreg_destroy(h);
+        g_err = keep;
+        return st;
+    };
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    const ncclResult_t r = nccl().commInitRank(&h->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        h->comm = nullptr;
+        return bail(fail(BNREG_E_NCCL, std::string("ncclCommInitRank: ") + nccl().errorString(r)));
+    }
+    if (cudaMalloc(&h->d_Rt, (size_t)m * m * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&h->d_rec, (size_t)world * 2 * m * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&h->d_gm, (size_t)m * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_gb, (size_t)m * sizeof(double)) != cudaSuccess)
+        return bail(fail(BNREG_E_NOMEM, "cudaMalloc of the dist buffers"));
+    s = bnreg_load_dist(h, X);
+    if (s != BNREG_OK) return bail(s);
+    *out = h;
+    return BNREG_OK;
+}
+
+bnreg_status bnreg_run_pairs_dist(bnreg_t* h, double* out_pairs, uint32_t* best_mask, double* best_bic)
+{
+    if (!h) return fail(BNREG_E_INVAL, "NULL handle");
+    if (!h->comm) return fail(BNREG_E_STATE, "not a bnreg_create_dist handle");
+    const Plan& P = h->plan;
+    const int m = P.m;
+    // this rank's best into its row of the gather buffer: [m BICs | m masks]
+    double* row = h->d_rec + (size_t)P.rank * 2 * m;
+    bnreg_status s = bnreg_run_pairs_async(h, out_pairs, (uint32_t*)(row + m), row);
+    if (s != BNREG_OK) return s;
+    NCK(nccl().allGather(row, h->d_rec, (size_t)2 * m, ncclFloat64, h->comm, h->stream));
+    s = bnreg_best_merge_async(h, P.world, (const uint32_t*)(h->d_rec + m), h->d_rec, (int64_t)16 * m, h->d_gm,
+                               h->d_gb);
+    if (s != BNREG_OK) return s;
+    if (best_mask) CK(cudaMemcpyAsync(best_mask, h->d_gm, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+    if (best_bic) CK(cudaMemcpyAsync(best_bic, h->d_gb, m * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(stream_wait(h->stream));
+    if (h->pending) return load_status(h);
+    return BNREG_OK;
+}
+#undef NCK
 
 }  // extern "C"

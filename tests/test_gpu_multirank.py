@@ -256,3 +256,42 @@ def test_pipelined_loads_bit_identical():
                 assert torch.equal(o, ref[i][gidx]), (world, i)
         for h in hs:
             h.close()
+
+
+def test_create_dist_in_library_nccl():
+    """bnreg_create_dist / bnreg_run_pairs_dist: the library's own NCCL communicator
+    (dlopen'd libnccl.so.2), R broadcast from rank 0, the per-rank bests all-gathered and
+    merged on the device.  One process and one device here (NCCL refuses two ranks on one
+    GPU), so world = 1: the table and the merged best must equal the plain handle's bit for
+    bit, and the argmax the oracle's; a handle not made by create_dist is refused."""
+    import torch
+    import paper_1901_07643_b200 as bn
+    X = datagen.config_data(2)
+    n, m = X.shape
+    full, fbm, fbb = _full_pairs(bn, X)
+    uid = bn.nccl_unique_id()
+    assert len(uid) == 128
+    h = bn.Bnreg.create_dist(X, n, m, uid, 0, 1)
+    t = torch.full((h.num_families(), 2), float("nan"), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    bm, bb = h.run_pairs_dist(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, full)
+    np.testing.assert_array_equal(bm, fbm)
+    np.testing.assert_array_equal(bb, fbb)
+    # new data through the collective load: the same as a plain load of it
+    X2 = datagen.dag_data(m, n, 0.2, 0.5, 2.0, seed=77)
+    h.load_dist(X2)
+    bm2, bb2 = h.run_pairs_dist(t)
+    torch.cuda.synchronize()
+    full2, fbm2, fbb2 = _full_pairs(bn, X2)
+    assert torch.equal(t, full2)
+    np.testing.assert_array_equal(bm2, fbm2)
+    h.close()
+    _, refb = oracle.table(oracle.centre(X))
+    om, _ = oracle.best(refb, m)
+    np.testing.assert_array_equal(bm, om)
+    plain = bn.Bnreg.create(X)
+    with pytest.raises(bn.BnregError, match="BNREG_E_STATE"):
+        plain.run_pairs_dist(t)
+    plain.close()
