@@ -80,24 +80,26 @@ __device__ __forceinline__ void tm_st(uint32_t a, const uint32_t* r)
     else if constexpr (N >= 8) { tm_st8(a, r); tm_st<N - 8>(a + 8, r + 8); }
     else if constexpr (N >= 4) { tm_st4(a, r); tm_st<N - 4>(a + 4, r + 4); }
 }
-// wait for the lane's outstanding tcgen05.ld, then pin the destination
-// registers behind the wait (the compiler does not know the wait defines them)
+// wait for the lane's outstanding tcgen05.ld.  BNREG_TM_PIN: also pin the destination
+// registers behind the wait with empty asm (the front end does not know the wait defines
+// them); without it -- the default since round 2, 2.5% fewer walk instructions -- the SASS
+// LDTM's scoreboard orders every use of its registers behind the load (parity-tested)
 template <int N>
 __device__ __forceinline__ void tm_wait_ld(uint32_t* r)
 {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifndef BNREG_TM_NOPIN
+#ifdef BNREG_TM_PIN
 #pragma unroll
     for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
 #else
-    (void)r;   // (the SASS LDTM is scoreboarded: ptxas orders every use of its registers)
+    (void)r;
 #endif
 }
 // pin more destination registers behind an already issued wait
 template <int N>
 __device__ __forceinline__ void tm_pin(uint32_t* r)
 {
-#ifndef BNREG_TM_NOPIN
+#ifdef BNREG_TM_PIN
 #pragma unroll
     for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
 #else
