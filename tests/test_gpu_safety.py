@@ -3,7 +3,8 @@
 * K8 exactly-once: the debug library libbnreg_k8.so (built by __graft_entry__.build(),
   -DBNREG_K8) counts every table store per entry; every entry of every table must be
   written exactly once (reading G11: the Alg.2 workers partition the families, PAPER.md
-  :299-324) -- for both walk designs, both output layouts, world 1, 2 and 4, m <= 20.
+  :299-324) -- for the three walk designs (default, walk7, design S), both output layouts,
+  world 1, 2 and 4, m <= 20.
   (The NaN-prefilled parity tests show every entry is written at least once.)
 * bounds checks (the same debug build): every walk-kernel table index, shared-memory
   state address and TMEM column range is checked in range; violations are counted in
@@ -20,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 K8_LIB = os.path.join(ROOT, "paper_1901_07643_b200", "libbnreg_k8.so")
 
 K8_SCRIPT = r"""
-import sys, numpy as np, torch
+import os, sys, numpy as np, torch
 sys.path.insert(0, %r)
 import datagen, paper_1901_07643_b200 as bn
 cases = [("cfg1", datagen.config_data(1), dict(free_vars=4)),
@@ -31,7 +32,11 @@ cases = [("cfg1", datagen.config_data(1), dict(free_vars=4)),
 checked = 0
 for name, X, kw in cases:
     n, m = X.shape
-    for pb in (3, 5):
+    for pb, ws in ((3, False), (5, False), (3, True)):      # the default walk, walk7, design S
+        if ws:
+            os.environ["BNREG_WALK_S"] = "1"
+        else:
+            os.environ.pop("BNREG_WALK_S", None)
         for world in ((1, 2, 4) if m <= 16 else (1, 2)):
             try:
                 bn.bnreg_plan_query(m, n, bn.options(pack_bits=pb, world=world, **kw))
@@ -58,13 +63,13 @@ for name, X, kw in cases:
                         h.run(r, b)
                     torch.cuda.synchronize()
                     c = cnt.cpu().numpy()
-                    assert c[F] == 0, (name, pb, world, rank, pairs, "bounds violations", int(c[F]))
+                    assert c[F] == 0, (name, pb, ws, world, rank, pairs, "bounds violations", int(c[F]))
                     c = c[:F]
-                    assert c.min() == 1 and c.max() == 1, (name, pb, world, rank, pairs, int(c.min()), int(c.max()),
+                    assert c.min() == 1 and c.max() == 1, (name, pb, ws, world, rank, pairs, int(c.min()), int(c.max()),
                                                            int((c != 1).sum()))
                     h.close()
                     checked += 1
-assert checked >= 40, checked
+assert checked >= 60, checked
 print("K8 exactly-once:", checked, "runs")
 """ % ROOT
 
