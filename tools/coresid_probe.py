@@ -1,6 +1,8 @@
 """Does a small kernel on another stream run beside the walk?  A 1-ms spin kernel
-(tmpvar/spin.so; CTAs x threads, smem bytes) launched on a second stream right after
-the walk (bnreg_run_pairs_async): its end time relative to the walk's start."""
+(tools/spin.cu, built on first use; CTAs x threads, smem bytes) launched on a second
+stream right after the walk (bnreg_run_pairs_async): its end time relative to the walk's
+start (DESIGN.md §4 "background prep").  The first launch of the spin kernel also pays
+its lazy module load, which waits for the running walk."""
 import ctypes
 import os
 import sys
@@ -12,7 +14,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import datagen  # noqa: E402
 import paper_1901_07643_b200 as bn  # noqa: E402
 
-spin = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tmpvar", "spin.so"))
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "spin.so")
+if not os.path.exists(SO):
+    import subprocess
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared",
+                           "-o", SO, os.path.join(HERE, "spin.cu")])
+spin = ctypes.CDLL(SO)
 X = datagen.config_data(5, 5005)
 n, m = X.shape
 dev = torch.device("cuda", 0)
