@@ -92,18 +92,34 @@ __device__ __forceinline__ void householder_tile(double* T, int nr, int m, doubl
         for (int c = j + 1 + warp; c < m; c += nwarp) {
             double* cc = T + (int64_t)c * nr;
             // row j (v's head v0) by lane 0, rows j+1.. (v = x) by all lanes: no per-row selects
-            double d = lane == 0 ? v0 * cc[j] : 0.0;
-#pragma unroll 4
-            for (int i = j + 1 + lane; i < nr; i += 32) d = fma(cj[i], cc[i], d);
-            const double f = warp_sum(d) * tv;
+            // two accumulators (rows 64 apart): half the dependent-FMA chain of the column's warp,
+            // which every other warp waits for at the column's barrier
+            double d = lane == 0 ? v0 * cc[j] : 0.0, d1 = 0.0;
+            int i = j + 1 + lane;
+#pragma unroll 2
+            for (; i + 32 < nr; i += 64) {
+                d = fma(cj[i], cc[i], d);
+                d1 = fma(cj[i + 32], cc[i + 32], d1);
+            }
+            if (i < nr) d = fma(cj[i], cc[i], d);
+            const double f = warp_sum(d + d1) * tv;
             if (lane == 0) cc[j] = fma(-f, v0, cc[j]);
-            double s2 = 0.0;                            // ||column, rows j+1..||^2 after the update
-#pragma unroll 4
-            for (int i = j + 1 + lane; i < nr; i += 32) {
+            double s2 = 0.0, s3 = 0.0;                  // ||column, rows j+1..||^2 after the update
+            i = j + 1 + lane;
+#pragma unroll 2
+            for (; i + 32 < nr; i += 64) {
+                const double y = fma(-f, cj[i], cc[i]), y1 = fma(-f, cj[i + 32], cc[i + 32]);
+                cc[i] = y;
+                cc[i + 32] = y1;
+                s2 = fma(y, y, s2);
+                s3 = fma(y1, y1, s3);
+            }
+            if (i < nr) {
                 const double y = fma(-f, cj[i], cc[i]);
                 cc[i] = y;
                 s2 = fma(y, y, s2);
             }
+            s2 += s3;
             if (c == j + 1) {
                 s2 = warp_sum(s2);
                 if (lane == 0) sh[(j + 1) & 1] = s2;
